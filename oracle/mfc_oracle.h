@@ -1,0 +1,116 @@
+/*
+ * mfc_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU oracle for the right-hand side of the
+ * Allaire 5-equation model as described in arXiv 2409.10729 (PAPER.md
+ * §II-A, §II-B, lines 54-84) with the readings of DESIGN.md §3 (SURVEY.md
+ * §8(c) S0-S4, AMB-1..22).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header,
+ * constant or helper with the CUDA path (paper_2409_10729_b200/csrc) and
+ * never includes include/mfc.h.
+ *
+ * Arithmetic: IEEE fp64, compiled with -O2 -ffp-contract=off (no FMA), every
+ * expression in the order written in DESIGN.md §3.
+ *
+ * Layout (oracle-private): q[E][P2][P1][P0], x fastest, where
+ * P_k = n_k + 6 for an active dimension (3 ghost layers per side) and 1 for an
+ * inactive one.  Interior cell (i,j,k) lives at (i+3, j+3, k+3) for active
+ * dims, index 0 for inactive dims.
+ */
+#ifndef MFC_ORACLE_H
+#define MFC_ORACLE_H
+#include <stdint.h>
+
+#define ORC_G 3                 /* ghost depth: WENO5 needs cells m-3..m+2 (AMB-12) */
+#define ORC_MAXF 3              /* maximum number of fluids */
+#define ORC_MAXE (2 * ORC_MAXF + 3 + 1)
+
+/* Boundary codes (MFC-style, AMB-13).  0 = ghosts supplied by the caller
+ * (used to emulate a neighbouring subdomain, S1 "neighbour rank"). */
+#define ORC_BC_EXTERNAL 0
+#define ORC_BC_PERIODIC (-1)
+#define ORC_BC_REFLECTIVE (-2)
+#define ORC_BC_EXTRAPOLATION (-3)
+
+typedef struct {
+    int32_t N;                  /* number of fluids, 1..3 (AMB-4) */
+    int32_t d;                  /* active dimensions, 1..3 */
+    int32_t n[3];               /* interior cells per dim (1 if inactive) */
+    double dx[3];               /* uniform spacing per dim (AMB-7) */
+    int32_t bc[6];              /* x_lo, x_hi, y_lo, y_hi, z_lo, z_hi */
+    double gamma[ORC_MAXF];     /* stiffened-gas gamma_i > 1 */
+    double pi_inf[ORC_MAXF];    /* stiffened-gas pi_inf_i >= 0 */
+    double eps;                 /* WENO epsilon (AMB-8), default 1e-16 */
+} orc_problem;
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int32_t orc_num_eq(int32_t N, int32_t d);
+int64_t orc_padded_cells(const orc_problem* P);
+void orc_padded_dims(const orc_problem* P, int64_t out[3]);
+
+/* S0: Gamma_i = 1/(gamma_i-1), Pi_i = gamma_i*pi_inf_i/(gamma_i-1). */
+void orc_constants(const orc_problem* P, double* Gam, double* Pi);
+
+/* S2 per cell: q[E] -> v[E]; v = (a_i r_i, u_k, p, a_i). */
+void orc_cons_to_prim_cell(const orc_problem* P, const double* Gam, const double* Pi,
+                           const double* q, double* v);
+/* Inverse EOS (P:66 with AMB-3): rhoE = (Gamma*p + Pi) + 0.5*rho*(u.u). */
+void orc_prim_to_cons_cell(const orc_problem* P, const double* Gam, const double* Pi,
+                           const double* v, double* q);
+/* Field versions over SoA arrays [E][ncells]. */
+void orc_cons_to_prim(const orc_problem* P, int64_t ncells, const double* q, double* v);
+void orc_prim_to_cons(const orc_problem* P, int64_t ncells, const double* v, double* q);
+
+/* S3 WENO5-JS (Jiang-Shu, [15] of the paper): from cell values
+ * a..e = v_{m-2..m+2}: minus -> v^-_{m+1/2}, plus -> v^+_{m-1/2}.
+ * weights[3] (may be NULL) receives the normalised omega_k. */
+double orc_weno5_minus(double a, double b, double c, double d, double e, double eps,
+                       double* weights);
+double orc_weno5_plus(double a, double b, double c, double d, double e, double eps,
+                      double* weights);
+
+/* S3 HLLC (Toro [14] ch. 10) in the compact branch form of DESIGN.md §3.
+ * dir = 0,1,2 selects the normal velocity.  F[E] gets the flux, *uf the face
+ * velocity used by the alpha*div(u) source (AMB-6). */
+void orc_hllc(const orc_problem* P, const double* Gam, const double* Pi, int32_t dir,
+              const double* vL, const double* vR, double* F, double* uf);
+
+/* S1 ghost fill for every active dimension (face ghosts only). */
+void orc_fill_ghosts(const orc_problem* P, double* q);
+
+/* One RHS evaluation L(q) (eq. (1) integrated): fills ghosts (S1)
+ * then accumulates x, y, z contributions (S3) into rhs (interior cells of a
+ * padded array; ghost entries of rhs are set to 0). */
+void orc_rhs(const orc_problem* P, double* q, double* rhs);
+
+/* The same RHS, computed independently at a list of interior cells
+ * (cells[3*c+0..2] = i, j, k), q's ghosts already filled.  out[c*E + e]. */
+void orc_rhs_cells(const orc_problem* P, const double* q, int64_t ncells,
+                   const int64_t* cells, double* out);
+
+/* S4 SSP-RK3 stage combination (AMB-11), pointwise over n values:
+ * stage 1: out = qs + dt*L
+ * stage 2: out = 0.75*qn + 0.25*(qs + dt*L)
+ * stage 3: out = (1/3)*qn + (2/3)*(qs + dt*L) */
+void orc_rk3_combine(int32_t stage, int64_t n, const double* qn, const double* qs,
+                     const double* L, double dt, double* out);
+
+/* One SSP-RK3 step on the padded state q (in place), ghost fill before each L. */
+void orc_rk3_step(const orc_problem* P, double* q, double dt);
+
+/* Admissibility check (AMB-14): returns number of interior cells with
+ * non-finite values, rho <= 0 or c^2 <= 0. */
+int64_t orc_count_inadmissible(const orc_problem* P, const double* q);
+
+/* Threads the OpenMP runtime will use (for the cpu_baseline report). */
+int32_t orc_num_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

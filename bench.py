@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark: grind time of the fp64 5-equation RHS hot path (SSP-RK3 steps) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1: BASELINE.json configs[2] (C3: 3D two-fluid shock-droplet, 256^3 cells, E = 8).
+N > 1 (launched by torchrun, one rank per GPU, NCCL): configs[3] (C4 weak scaling):
+      C3's 256^3 block on every rank, z-slabs, periodic in z, halo exchange over NCCL.
+One "step" = one SSP-RK3 step = 3 RHS evaluations (ghost fill + x/y/z fused sweeps each).
+Metric (BASELINE.json): grind time = device time / (cells * E * RHS evaluations), in ns,
+aggregate over all ranks (lower is better), plus achieved HBM GB/s of the sweeps.
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (oracle/, the only
+other place bench.py runs it) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grind time ns/(cell*eq*RHS) at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+UNIT = "ns/(cell*eq*RHS)"
+RHS_PER_STEP = 3
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+                power.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ cpu baseline
+def cpu_oracle_grind(target_s: float = 12.0, n: int = 256, max_nz: int = 256):
+    """The oracle as it stands, timed on the host cores on a bounded sample of C3:
+    one RK3 step on an n x n x nz block of the C3 field (nz sized for ~target_s)."""
+    import oracle as O
+    from paper_2409_10729_b200 import workloads as W
+    O.build()
+
+    def run(nz):
+        pb = W.c3_droplet(n, nz=nz)
+        P = O.Problem.from_spec(pb)
+        q = O.prim_to_cons(P, W.c3_prims(pb))
+        t0 = time.perf_counter()
+        O.rk3_step(P, q, pb.dt, nsteps=1)
+        return time.perf_counter() - t0, pb
+
+    t, pb = run(4)
+    nz = int(min(max_nz, max(4, 4 * target_s / max(t, 1e-3))))
+    if nz > 4:
+        t, pb = run(nz)
+    grind = t / (pb.cells * pb.E * RHS_PER_STEP) * 1e9
+    return {"value": grind, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"1 SSP-RK3 step (3 RHS) of the C3 field on a {n}x{n}x{nz} block "
+                      f"({pb.cells} cells, E={pb.E}), {t:.2f} s wall"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, each step a bounded sample of the workload."""
+    import oracle as O
+    from paper_2409_10729_b200 import workloads as W
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    O.build()
+    # size the sample so (steps + warmup) RK3 steps take ~2 minutes in total
+    pb = W.c3_droplet(256, nz=2)
+    P = O.Problem.from_spec(pb)
+    q = O.prim_to_cons(P, W.c3_prims(pb))
+    t0 = time.perf_counter()
+    O.rk3_step(P, q, pb.dt, 1)
+    per_plane = (time.perf_counter() - t0) / 2
+    total = args.steps + args.warmup
+    nz = int(max(2, min(256, 120.0 / max(total * per_plane, 1e-6))))
+    pb = W.c3_droplet(256, nz=nz)
+    P = O.Problem.from_spec(pb)
+    q = O.prim_to_cons(P, W.c3_prims(pb))
+    for _ in range(args.warmup):
+        O.rk3_step(P, q, pb.dt, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        q = O.rk3_step(P, q, pb.dt, 1)
+    wall = time.perf_counter() - t0
+    grind = wall / (pb.cells * pb.E * RHS_PER_STEP * args.steps) * 1e9
+    sample = (f"{args.steps} SSP-RK3 steps of the C3 field on a 256x256x{nz} block "
+              f"({pb.cells} cells, E={pb.E}) per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": grind, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / args.steps * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C3 3D two-fluid shock-droplet (oracle sample)",
+                   "sample": sample},
+        "cpu_baseline": {"value": grind, "unit": UNIT, "cores": O.num_threads(),
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": grind, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- ours
+def algorithmic_bytes(kind: str, E: int, stage_mix=True) -> float:
+    """Algorithmic HBM bytes per interior cell for one launch of each sweep kind
+    (DESIGN.md §6): x: read q, write acc (16E); y: read q, acc, write acc (24E);
+    z + RK epilogue: read q, acc, write q_out (24E) + read q^n in stages 2, 3
+    (+8E for 2 of 3 launches)."""
+    if kind == "sweep_x":
+        return 16.0 * E
+    if kind == "sweep_y":
+        return 24.0 * E
+    if kind == "sweep_z":
+        return 24.0 * E + (8.0 * E * 2.0 / 3.0 if stage_mix else 0.0)
+    return 0.0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2409_10729_b200 import mfc
+    from paper_2409_10729_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = args.n
+    block = W.c3_droplet(n)                      # the per-GPU block (C3 / C4)
+    if world == 1:
+        pb, procs, nid, ng = block, (1, 1, 1), None, None
+        workload = f"C3 3D two-fluid shock-droplet {n}^3 (BASELINE configs[2])"
+    else:
+        pb = W.c3_droplet(n, nz=n * world)       # global domain: blocks stacked along z
+        procs = (1, 1, world)
+        obj = [mfc.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid, ng = obj[0], None
+        workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
+    s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local)
+    L = s.layout
+    # every rank holds the same C3 block (its local prims), converted on the GPU
+    q = s.state_from_prims(W.c3_prims(block))
+    dt = block.dt
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        s.rk3_step(q, dt)
+    torch.cuda.synchronize()
+    barrier()
+
+    clk = ClockSampler(local)
+    clk.start()
+    s.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        s.rk3_step(q, dt)
+        launches += s.last_launch_count()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    prof = s.profile_read()
+    s.profile(False)
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    cells_local = int(np.prod(L.n_local))
+    cells_total = cells_local * world
+    E = L.E
+    grind = ms_max * 1e6 / (cells_total * E * RHS_PER_STEP * args.steps)
+
+    # state sanity (finite) after the timed steps
+    finite = bool(torch.isfinite(s.interior(q)).all().item())
+
+    # dominant kernel roofline (CUDA events on the launch stream, over the timed region)
+    peaks = _peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    sweeps = {k: v for k, v in prof.items() if k.startswith("sweep")}
+    dom = max(sweeps, key=lambda k: sweeps[k][0])
+    dom_ms, dom_n = sweeps[dom]
+    per_launch_ms = dom_ms / max(dom_n, 1)
+    alg_bytes = algorithmic_bytes(dom, E) * cells_local
+    achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    # per step: 3 x (16E + 24E + 24E) + q^n reads in stages 2 and 3 (2 x 8E) = 208E B/cell
+    step_alg_bytes = (16 + 24 + 24) * E * cells_local * RHS_PER_STEP + 2 * 8 * E * cells_local
+    hbm_step = step_alg_bytes / (ms_max / args.steps * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": grind, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "cells_per_gpu": cells_local, "cells_total": cells_total,
+                   "E": E, "n_fluids": pb.n_fluids, "decomposition": f"procs={list(procs)}",
+                   "rhs_per_step": RHS_PER_STEP, "dt": dt,
+                   "l2": f"inputs > L2: each state buffer {8 * L.n_elems / 1e9:.2f} GB >> 126 MB, no flush",
+                   "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU"},
+        "hbm_gbs_step": hbm_step,
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                     "per_launch_ms": per_launch_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
+                     else "fallback 6650 GB/s (B200_PROFILING.md)"},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "state_finite": finite,
+    }
+
+    # e2e through the C ABI with host buffers (H2D + steps + D2H inside the timed region)
+    if not args.no_e2e:
+        import torch as T
+        qh_in = T.empty((E, L.n_local[2], L.n_local[1], L.n_local[0]), dtype=T.float64).pin_memory()
+        qh_in.copy_(s.interior(q).cpu())
+        qh_out = T.empty_like(qh_in).pin_memory()
+        ke = max(1, min(args.steps, 5))
+        s.advance_host(qh_in, qh_out, q, 1, dt)   # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            s.advance_host(qh_in, qh_out, q, 1, dt)
+        wall = time.perf_counter() - t0
+        tw = torch.tensor([wall], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        nb = int(qh_in.numel() * 8)
+        line["e2e"] = {"value": float(tw.item()) * 1e9 / (cells_total * E * RHS_PER_STEP * ke),
+                       "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+                       "steps": ke, "call": "mfc_advance_host(nsteps=1) per step, pinned host buffers"}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_oracle_grind(args.cpu_seconds)
+        except Exception as ex:  # report, never fall back
+            line["cpu_baseline"] = {"error": repr(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256, help="cells per dimension of the per-GPU block")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("note: warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,199 @@
+/*
+ * mfc.h -- C ABI of libmfc, the B200-native (sm_100a) fp64 right-hand-side hot
+ * path of MFC's 5-equation multiphase solver (arXiv 2409.10729).
+ *
+ * What the library computes (PAPER.md = /root/reference/PAPER.md, line numbers):
+ *   - the Allaire 5-equation model (§II-A) closed by the stiffened-gas
+ *     mixture EOS, with N in {1,2,3} fluids on a uniform Cartesian grid
+ *      in d in {1,2,3} dimensions;
+ *   - its finite-volume semi-discretisation (eq. (1) integrated over a
+ *     cell): WENO5 reconstruction of the primitive variables and the HLLC flux
+ *     (P:84), flux differencing plus the non-conservative -h(q) div(u) term;
+ *   - an SSP-RK3 time step (BASELINE.json north_star; the paper's grind unit is the
+ *     "right-hand-side evaluation");
+ *   - the 3-deep halo exchange between subdomains (§III-A) over NCCL.
+ * The readings of the paper where it is silent or garbled are listed in
+ * DESIGN.md §3 (AMB-1..22); the arithmetic is specified there step by step.
+ *
+ * Variables (E = 2N + d + 1 equations, this order):
+ *   conserved q = (a_1 r_1 .. a_N r_N, r u_1 .. r u_d, r E, a_1 .. a_N)
+ *   primitive v = (a_1 r_1 .. a_N r_N,   u_1 ..   u_d,   p, a_1 .. a_N)
+ *
+ * State layout (device memory, fp64, caller-owned, described by mfc_layout):
+ *   q[e][z][y][x] with 3 ghost cells on each side of every ACTIVE dimension,
+ *   x unit-stride.  Element (e, i, j, k) of interior cell (i, j, k) is at
+ *   q[layout.offset + e*stride[0] + k*stride[1] + j*stride[2] + i*stride[3]],
+ *   with i, j, k running from -3 to n+2 in active dimensions (0 otherwise).
+ *   The x pitch is padded so that every interior row starts 32-byte aligned.
+ *   Ghost cells are scratch owned by the library and rewritten before every RHS.
+ *
+ * Streams: every call that takes `stream` (a cudaStream_t passed as void*) only
+ * ENQUEUES work on it and returns without synchronising (except the *_host call,
+ * which synchronises).  Buffers passed in must stay alive until that work is done.
+ *
+ * Errors: every call returns an mfc_status; nothing is thrown across the ABI.
+ * mfc_last_error() returns a thread-local description of the last failure.
+ * Asynchronous CUDA errors surface at the next call that checks them.
+ *
+ * Threading: a context is not thread-safe; many contexts may coexist.
+ */
+#ifndef MFC_H
+#define MFC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mfc_ctx mfc_ctx; /* opaque */
+
+typedef enum {
+    MFC_OK = 0,
+    MFC_EINVAL = -1,       /* bad argument (pointer, size, alignment, range) */
+    MFC_ENOMEM = -2,       /* workspace missing or too small */
+    MFC_ECUDA = -3,        /* a CUDA runtime/driver call failed */
+    MFC_ENCCL = -4,        /* an NCCL call failed */
+    MFC_ESTATE = -5,       /* call not valid in the current context state */
+    MFC_EUNSUPPORTED = -6  /* valid request this build does not implement */
+} mfc_status;
+
+/* Boundary-condition codes (MFC's own numbering; DESIGN.md AMB-13).
+ *   PERIODIC:      ghost -1-j <- interior n-1-j, ghost n+j <- interior j
+ *   REFLECTIVE:    mirror image, normal momentum negated
+ *   EXTRAPOLATION: every ghost <- the adjacent interior cell (zeroth order) */
+enum { MFC_BC_PERIODIC = -1, MFC_BC_REFLECTIVE = -2, MFC_BC_EXTRAPOLATION = -3 };
+
+/* Global grid: uniform spacing dx_k = (hi_k - lo_k)/n_global[k].
+ * Inactive dimensions (k >= ndim) must have n_global[k] == 1 and procs[k] == 1. */
+typedef struct {
+    int32_t ndim;           /* 1..3 */
+    int64_t n_global[3];    /* cells per dimension (x, y, z) */
+    double lo[3], hi[3];    /* domain extents */
+    int32_t procs[3];       /* rank grid; product == comm.nranks; {1,1,P} = z-slabs */
+} mfc_grid;
+
+/* Communicator.  nranks == 1: single domain, no NCCL.  nranks > 1 with
+ * loopback == 0: one process per GPU, NCCL over NVLink; nccl_unique_id points to
+ * the 128-byte ncclUniqueId every rank received (e.g. broadcast with
+ * torch.distributed).  loopback == 1: all nranks subdomains live in THIS process
+ * on one device and halos are exchanged with device copies (tests; see the
+ * *_group calls). */
+typedef struct {
+    int32_t rank, nranks;
+    const void* nccl_unique_id;
+    int32_t loopback;
+} mfc_comm;
+
+/* Local layout, filled by mfc_get_layout. */
+typedef struct {
+    int32_t E, ghost, n_fluids, ndim;
+    int64_t n_local[3];     /* interior cells of this rank (x, y, z) */
+    int64_t lo_global[3];   /* global index of local interior cell 0 */
+    int64_t dims[4];        /* padded extents [E][Z][Y][Xpitch] */
+    int64_t stride[4];      /* element strides of [e][z][y][x]; stride[3] == 1 */
+    int64_t offset;         /* element offset of (e=0, i=0, j=0, k=0) */
+    int64_t n_elems;        /* elements a state buffer must hold = dims product */
+    size_t workspace_bytes; /* bytes mfc_bind_workspace needs */
+} mfc_layout;
+
+/* Create a context.  gamma[i] > 1 and pi_inf[i] >= 0 (Pa) are the stiffened-gas
+ * parameters of fluid i; the library derives Gamma_i = 1/(gamma_i-1),
+ * Pi_i = gamma_i pi_inf_i/(gamma_i-1).  bc = {x_lo, x_hi, y_lo, y_hi, z_lo, z_hi};
+ * entries of inactive dimensions are ignored; a periodic dimension must be
+ * periodic on both ends.  device = CUDA ordinal.  Split dimensions need at least 3
+ * local cells.  Single-domain and loopback contexts do not touch the GPU until the
+ * first call that launches work.  On success *out owns the NCCL comm until mfc_finalize.
+ * Errors: EINVAL (argument), ECUDA, ENCCL. */
+int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double* gamma,
+             const double* pi_inf, const int32_t bc[6], const mfc_comm* comm, int32_t device);
+
+/* Fill *out with this rank's layout (host call, no GPU work). */
+int mfc_get_layout(const mfc_ctx* ctx, mfc_layout* out);
+
+/* Neighbour ranks of the six faces {x_lo, x_hi, y_lo, y_hi, z_lo, z_hi}; -1 where
+ * the face is a physical boundary (or a periodic wrap onto this same rank).
+ * Ranks are numbered x fastest: rank = cx + px*(cy + py*cz).  Host call. */
+int mfc_get_neighbors(const mfc_ctx* ctx, int32_t nbr[6]);
+
+/* Hand the library a device buffer of >= layout.workspace_bytes bytes, 256-byte
+ * aligned (torch-owned; the library never frees it).  It holds two RK stage
+ * buffers, the RHS accumulator and the halo pack buffers.  Must be bound before
+ * mfc_rk3_step.  Errors: EINVAL (NULL, misaligned), ENOMEM (too small). */
+int mfc_bind_workspace(mfc_ctx* ctx, void* dev_ptr, size_t bytes);
+
+/* WENO epsilon of alpha_k = d_k/(beta_k+eps)^2 (DESIGN.md AMB-8); default 1e-16;
+ * must be in [1e-40, 1e-2]. */
+int mfc_set_weno_eps(mfc_ctx* ctx, double eps);
+
+/* Primitive <-> conserved conversion on the interior cells of padded device
+ * buffers (same layout for v and q; may not alias).  prim_to_cons evaluates
+ * rhoE = (Gamma p + Pi) + KE, cons_to_prim the inverse in the order of DESIGN.md
+ * §3 S2 (the EOS of P:64-68 with the mixture rule AMB-3). */
+int mfc_prim_to_cons(mfc_ctx* ctx, const double* v, double* q, void* stream);
+int mfc_cons_to_prim(mfc_ctx* ctx, const double* q, double* v, void* stream);
+
+/* Fill the 3 ghost layers of every active dimension of q: physical faces by the
+ * boundary condition, faces shared with another rank by the halo exchange
+ * (P:94).  Face ghosts only (edges/corners are never read).  Only ghost cells of
+ * q are written. */
+int mfc_halo_exchange(mfc_ctx* ctx, double* q, void* stream);
+
+/* One RHS evaluation L(q): fills q's ghosts (as mfc_halo_exchange),
+ * then writes rhs on every interior cell (rhs has the state layout; its ghost
+ * cells are not written).  q and rhs must not alias. */
+int mfc_rhs(mfc_ctx* ctx, double* q, double* rhs, void* stream);
+
+/* One SSP-RK3 step of size dt on q's interior, in place:
+ *   q1 = q + dt L(q);  q2 = 3/4 q + 1/4 (q1 + dt L(q1));  q <- 1/3 q + 2/3 (q2 + dt L(q2)).
+ * Needs a bound workspace (ESTATE otherwise). */
+int mfc_rk3_step(mfc_ctx* ctx, double* q, double dt, void* stream);
+
+/* End-to-end call with HOST buffers: copy the dense interior q_in[E][nz][ny][nx]
+ * (host, pinned or pageable) into the padded device buffer q_dev, run nsteps RK3
+ * steps of size dt, copy the interior back to q_out (host; may equal q_in), and
+ * synchronise `stream`.  Host arrays are dense, x fastest, n_local extents. */
+int mfc_advance_host(mfc_ctx* ctx, const double* q_in, double* q_out, double* q_dev,
+                     int64_t nsteps, double dt, void* stream);
+
+/* Loopback groups: the same operations for `count` contexts created with
+ * comm.loopback = 1 and ranks 0..count-1 (in order), exchanging halos with device
+ * copies on `stream`.  With count == 1 they equal the single-context calls. */
+int mfc_halo_exchange_group(mfc_ctx* const* ctxs, double* const* qs, int32_t count,
+                            void* stream);
+int mfc_rhs_group(mfc_ctx* const* ctxs, double* const* qs, double* const* rhss,
+                  int32_t count, void* stream);
+int mfc_rk3_step_group(mfc_ctx* const* ctxs, double* const* qs, int32_t count, double dt,
+                       void* stream);
+
+/* Generate the 128-byte NCCL unique id (rank 0 calls it and broadcasts the bytes,
+ * e.g. over torch.distributed, before every rank calls mfc_init). */
+int mfc_nccl_get_unique_id(void* out128);
+
+/* Number of kernels the last mfc_rhs / mfc_rk3_step / mfc_halo_exchange call
+ * launched (for the bench's launch count). */
+int64_t mfc_last_launch_count(const mfc_ctx* ctx);
+
+/* Optional CUDA-event timing of every kernel the library launches (for bench.py's
+ * roofline line).  enable(on=1) clears previous records; while on, each launch is
+ * bracketed by two events recorded on its own stream.  read() synchronises those
+ * events and returns, per kernel kind, the summed milliseconds and launch counts:
+ * kind 0/1/2 = sweep x/y/z, 3 = bc fill, 4 = halo pack/unpack, 5 = EOS conversion;
+ * then clears the records.  ms/count hold nkinds entries. */
+int mfc_profile_enable(mfc_ctx* ctx, int32_t on);
+int mfc_profile_read(mfc_ctx* ctx, double* ms, int64_t* count, int32_t nkinds);
+
+/* Release streams, events and the NCCL communicator (not the caller's buffers). */
+int mfc_finalize(mfc_ctx* ctx);
+
+/* Thread-local message describing the last error ("" if none). */
+const char* mfc_last_error(void);
+
+/* Library version string, e.g. "libmfc 0.1 sm_100a". */
+const char* mfc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFC_H */

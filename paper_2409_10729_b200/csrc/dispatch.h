@@ -1,0 +1,28 @@
+// dispatch.h -- host-side entry points of the templated sweep / EOS kernels,
+// one translation unit per fluid count (sweep_n1.cu, sweep_n2.cu, sweep_n3.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "sweep.cuh"
+
+namespace mfc {
+
+// Launch the sweep kernel for N fluids, D dims, direction DIR.
+// epi == EPI_ACC or EPI_RK; the accumulator is read iff DIR > 0.
+template <int N>
+cudaError_t launch_sweep(int D, int DIR, int epi, const SweepArgs& a, dim3 grid, dim3 block,
+                         cudaStream_t s);
+
+struct EosArgs {
+    const double* in;
+    double* out;
+    int64_t sE, sZ, sY, base;
+    int32_t nx, ny, nz;
+    Materials mat;
+};
+
+// to_cons = true: primitive -> conserved, false: conserved -> primitive
+template <int N>
+cudaError_t launch_eos(int D, bool to_cons, const EosArgs& a, cudaStream_t s);
+
+}  // namespace mfc

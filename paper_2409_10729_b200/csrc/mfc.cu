@@ -1,0 +1,794 @@
+// mfc.cu -- libmfc context, layout, ghost/halo kernels and the C ABI of include/mfc.h.
+//
+// Call graph of one SSP-RK3 step:
+//   for stage s = 1..3:
+//     ghost fill of the stage state: bc_fill (physical faces, one kernel per active
+//       dimension) + halo exchange (pack -> NCCL send/recv or loopback copies -> unpack)
+//     sweep x (acc = c_x), sweep y (acc += c_y), sweep z with the RK stage epilogue
+//   stage 1: q -> S1,  stage 2: S1 -> S2,  stage 3: S2 -> q (in place, pointwise)
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mfc.h"
+#include "dispatch.h"
+
+using namespace mfc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU_TRY(expr)                                                                  \
+    do {                                                                              \
+        cudaError_t _e = (expr);                                                      \
+        if (_e != cudaSuccess)                                                        \
+            return fail(MFC_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e),   \
+                        __FILE__, __LINE__);                                          \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                \
+    do {                                                                              \
+        ncclResult_t _r = (expr);                                                     \
+        if (_r != ncclSuccess)                                                        \
+            return fail(MFC_ENCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(_r),   \
+                        __FILE__, __LINE__);                                          \
+    } while (0)
+
+constexpr int kXOff = 4;  // interior x starts at pitch index 4: 1 pad + 3 ghosts (32 B aligned)
+constexpr int BC_NEIGHBOR = 1;
+
+}  // namespace
+
+struct mfc_ctx {
+    int device = 0;
+    int N = 0, D = 0, E = 0;
+    int64_t nl[3] = {1, 1, 1};     // local interior cells
+    int64_t lo_g[3] = {0, 0, 0};   // global index of local cell 0
+    int64_t dims[4] = {0, 0, 0, 0};
+    int64_t stride[4] = {0, 0, 0, 1};
+    int64_t off[3] = {0, 0, 0};    // interior offset per axis (x, y, z) in padded coords
+    int64_t offset = 0, n_elems = 0;
+    double dx[3] = {1, 1, 1};
+    int bc[6] = {0, 0, 0, 0, 0, 0};  // physical bc code, or BC_NEIGHBOR
+    int nbr[6] = {-1, -1, -1, -1, -1, -1};
+    Materials mat{};
+    double eps = 1e-16;
+    int rank = 0, nranks = 1, procs[3] = {1, 1, 1}, coords[3] = {0, 0, 0};
+    bool loopback = false;
+    ncclComm_t comm = nullptr;
+    // workspace
+    char* ws = nullptr;
+    size_t ws_bytes = 0, ws_need = 0;
+    double* S1 = nullptr;
+    double* S2 = nullptr;
+    double* acc = nullptr;
+    double* sendb[6] = {};
+    double* recvb[6] = {};
+    int64_t face_elems[3] = {0, 0, 0};  // E * 3 * area of a face normal to dim k
+    int64_t launches = 0;
+    int seg = 0;  // sweep segment length override (0 = heuristic)
+    // optional per-launch CUDA-event timing (mfc_profile_*)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    struct Rec { int kind; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    size_t ev_used = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- kernels
+
+struct FaceGeom {
+    int64_t sE, s[3];     // strides for e and axes x, y, z (s[0] == 1)
+    int64_t base;         // offset of interior (0,0,0)
+    int32_t n[3];         // interior extents
+    int32_t E;
+};
+
+// Physical-boundary ghost fill along dimension `dir`, both sides (S1 of DESIGN.md §3):
+// periodic: ghost -1-j <- n-1-j, ghost n+j <- j; extrapolation: <- adjacent interior;
+// reflective: mirror with the normal momentum (equation mom) negated.
+__global__ void bc_fill_kernel(double* q, FaceGeom g, int dir, int bc_lo, int bc_hi, int mom) {
+    const int t1 = (dir + 1) % 3, t2 = (dir + 2) % 3;
+    const int64_t area = (int64_t)g.n[t1] * g.n[t2];
+    const int64_t total = area * kGhost * 2 * g.E;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = t;
+        const int a = (int)(r % g.n[t1]); r /= g.n[t1];
+        const int b = (int)(r % g.n[t2]); r /= g.n[t2];
+        const int j = (int)(r % kGhost); r /= kGhost;
+        const int side = (int)(r % 2); r /= 2;
+        const int e = (int)r;
+        const int bc = side ? bc_hi : bc_lo;
+        if (bc == BC_NEIGHBOR) continue;
+        const int n = g.n[dir];
+        int ghost, src;
+        if (side == 0) {
+            ghost = -1 - j;
+            src = bc == MFC_BC_PERIODIC ? n - 1 - j : (bc == MFC_BC_REFLECTIVE ? j : 0);
+        } else {
+            ghost = n + j;
+            src = bc == MFC_BC_PERIODIC ? j : (bc == MFC_BC_REFLECTIVE ? n - 1 - j : n - 1);
+        }
+        const int64_t c0 = g.base + e * g.sE + a * g.s[t1] + b * g.s[t2];
+        double v = q[c0 + (int64_t)src * g.s[dir]];
+        if (bc == MFC_BC_REFLECTIVE && e == mom) v = -v;
+        q[c0 + (int64_t)ghost * g.s[dir]] = v;
+    }
+}
+
+// Halo pack/unpack for the face `side` of dimension `dir`: buffer layout
+// [e][layer j = 0..2][b][a] (a fastest).  Pack reads the 3 interior layers next to
+// the face (layer j = interior index j on the low side, n-3+j on the high side);
+// unpack writes the 3 ghost layers (-3+j low, n+j high), so a buffer packed on one
+// rank's high face unpacks verbatim into the neighbour's low ghosts.
+__global__ void halo_pack_kernel(const double* q, double* buf, FaceGeom g, int dir, int side,
+                                 bool unpack, double* qout) {
+    const int t1 = (dir + 1) % 3, t2 = (dir + 2) % 3;
+    const int64_t area = (int64_t)g.n[t1] * g.n[t2];
+    const int64_t total = area * kGhost * g.E;
+    const int n = g.n[dir];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = t;
+        const int a = (int)(r % g.n[t1]); r /= g.n[t1];
+        const int b = (int)(r % g.n[t2]); r /= g.n[t2];
+        const int j = (int)(r % kGhost); r /= kGhost;
+        const int e = (int)r;
+        const int64_t c0 = g.base + e * g.sE + a * g.s[t1] + b * g.s[t2];
+        if (!unpack) {
+            const int src = side == 0 ? j : n - kGhost + j;
+            buf[t] = q[c0 + (int64_t)src * g.s[dir]];
+        } else {
+            const int dst = side == 0 ? j - kGhost : n + j;
+            qout[c0 + (int64_t)dst * g.s[dir]] = buf[t];
+        }
+    }
+}
+
+int grid_for(int64_t n, int threads) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 148 * 32));
+}
+
+FaceGeom geom(const mfc_ctx* c) {
+    FaceGeom g;
+    g.sE = c->stride[0];
+    g.s[0] = 1;
+    g.s[1] = c->stride[2];
+    g.s[2] = c->stride[1];
+    g.base = c->offset;
+    for (int k = 0; k < 3; ++k) g.n[k] = (int32_t)c->nl[k];
+    g.E = c->E;
+    return g;
+}
+
+// ------------------------------------------------------------ profiling
+
+enum { K_SWEEP_X = 0, K_SWEEP_Y = 1, K_SWEEP_Z = 2, K_BC = 3, K_HALO = 4, K_EOS = 5, K_NKIND = 6 };
+
+cudaEvent_t prof_event(mfc_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+
+// Brackets one kernel launch with events on its stream when profiling is on.
+struct ProfScope {
+    mfc_ctx* c;
+    cudaStream_t s;
+    int kind;
+    cudaEvent_t a = nullptr;
+    ProfScope(mfc_ctx* c_, cudaStream_t s_, int k) : c(c_), s(s_), kind(k) {
+        if (c->prof && (a = prof_event(c))) cudaEventRecord(a, s);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEvent_t b = prof_event(c);
+        if (!b) return;
+        cudaEventRecord(b, s);
+        c->recs.push_back({kind, a, b});
+    }
+};
+
+int set_device(const mfc_ctx* c) {
+    CU_TRY(cudaSetDevice(c->device));
+    return MFC_OK;
+}
+
+// ------------------------------------------------------------ ghost filling
+
+int bc_fill(mfc_ctx* c, double* q, cudaStream_t s) {
+    const FaceGeom g = geom(c);
+    for (int dir = 0; dir < c->D; ++dir) {
+        if (c->bc[2 * dir] == BC_NEIGHBOR && c->bc[2 * dir + 1] == BC_NEIGHBOR) continue;
+        const int t1 = (dir + 1) % 3, t2 = (dir + 2) % 3;
+        const int64_t total = c->nl[t1] * c->nl[t2] * kGhost * 2 * c->E;
+        ProfScope ps(c, s, K_BC);
+        bc_fill_kernel<<<grid_for(total, 256), 256, 0, s>>>(q, g, dir, c->bc[2 * dir],
+                                                              c->bc[2 * dir + 1], c->N + dir);
+        CU_TRY(cudaGetLastError());
+        ++c->launches;
+    }
+    return MFC_OK;
+}
+
+int halo_pack(mfc_ctx* c, const double* q, cudaStream_t s) {
+    const FaceGeom g = geom(c);
+    for (int f = 0; f < 2 * c->D; ++f) {
+        if (c->bc[f] != BC_NEIGHBOR) continue;
+        const int dir = f / 2;
+        ProfScope ps(c, s, K_HALO);
+        halo_pack_kernel<<<grid_for(c->face_elems[dir], 256), 256, 0, s>>>(
+            q, c->sendb[f], g, dir, f % 2, false, nullptr);
+        CU_TRY(cudaGetLastError());
+        ++c->launches;
+    }
+    return MFC_OK;
+}
+
+int halo_unpack(mfc_ctx* c, double* q, cudaStream_t s) {
+    const FaceGeom g = geom(c);
+    for (int f = 0; f < 2 * c->D; ++f) {
+        if (c->bc[f] != BC_NEIGHBOR) continue;
+        const int dir = f / 2;
+        ProfScope ps(c, s, K_HALO);
+        halo_pack_kernel<<<grid_for(c->face_elems[dir], 256), 256, 0, s>>>(
+            nullptr, c->recvb[f], g, dir, f % 2, true, q);
+        CU_TRY(cudaGetLastError());
+        ++c->launches;
+    }
+    return MFC_OK;
+}
+
+bool has_neighbors(const mfc_ctx* c) {
+    for (int f = 0; f < 2 * c->D; ++f)
+        if (c->bc[f] == BC_NEIGHBOR) return true;
+    return false;
+}
+
+int need_ws(const mfc_ctx* c, bool stages) {
+    if (!c->ws && (stages || has_neighbors(c)))
+        return fail(MFC_ESTATE, "workspace not bound (mfc_bind_workspace)");
+    return MFC_OK;
+}
+
+// Ghost fill for a set of contexts (count == 1: NCCL or single domain; > 1: loopback).
+int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s) {
+    for (int r = 0; r < count; ++r) {
+        int st = need_ws(cs[r], false);
+        if (st) return st;
+        if ((st = bc_fill(cs[r], qs[r], s))) return st;
+        if ((st = halo_pack(cs[r], qs[r], s))) return st;
+    }
+    if (count == 1 && cs[0]->nranks > 1 && !cs[0]->loopback) {
+        mfc_ctx* c = cs[0];
+        if (has_neighbors(c)) {
+            NCCL_TRY(ncclGroupStart());
+            for (int f = 0; f < 2 * c->D; ++f) {
+                if (c->bc[f] != BC_NEIGHBOR) continue;
+                const size_t n = (size_t)c->face_elems[f / 2];
+                NCCL_TRY(ncclSend(c->sendb[f], n, ncclFloat64, c->nbr[f], c->comm, s));
+                NCCL_TRY(ncclRecv(c->recvb[f], n, ncclFloat64, c->nbr[f], c->comm, s));
+            }
+            NCCL_TRY(ncclGroupEnd());
+        }
+    } else if (count > 1 || cs[0]->loopback) {
+        // loopback: my send buffer of face f goes to the receive buffer of the
+        // opposite face of neighbour nbr[f]
+        for (int r = 0; r < count; ++r) {
+            mfc_ctx* c = cs[r];
+            for (int f = 0; f < 2 * c->D; ++f) {
+                if (c->bc[f] != BC_NEIGHBOR) continue;
+                const int o = c->nbr[f];
+                if (o < 0 || o >= count)
+                    return fail(MFC_EINVAL, "loopback group lacks rank %d", o);
+                const int fo = f ^ 1;
+                CU_TRY(cudaMemcpyAsync(cs[o]->recvb[fo], c->sendb[f],
+                                       sizeof(double) * c->face_elems[f / 2],
+                                       cudaMemcpyDeviceToDevice, s));
+            }
+        }
+    }
+    for (int r = 0; r < count; ++r) {
+        int st = halo_unpack(cs[r], qs[r], s);
+        if (st) return st;
+    }
+    return MFC_OK;
+}
+
+// ------------------------------------------------------------------ sweeps
+
+int seg_len(const mfc_ctx* c, int dir) {
+    if (c->seg > 0) return c->seg;
+    const int t1 = dir == 0 ? 1 : 0;          // lane axis
+    const int t2 = dir == 2 ? 1 : (dir == 0 ? 2 : 2);
+    const int64_t lines = c->nl[t1] * c->nl[t2];
+    const int64_t n = c->nl[dir];
+    // aim for >= ~48k threads in flight, segments of 16..64 cells
+    int T = 64;
+    while (T > 16 && lines * ((n + T - 1) / T) < 49152) T /= 2;
+    if (c->D == 1) T = (int)std::max<int64_t>(8, std::min<int64_t>(32, n / 8 + 1));
+    return (int)std::min<int64_t>(T, n);
+}
+
+int launch_sweep_dir(mfc_ctx* c, int dir, int epi, const double* q, double* acc, double* out,
+                     const double* qn, double dt, double ca, double cb, cudaStream_t s) {
+    SweepArgs a;
+    a.q = q;
+    a.acc = acc;
+    a.out = out;
+    a.qn = qn;
+    a.sE = c->stride[0];
+    const int64_t sax[3] = {1, c->stride[2], c->stride[1]};  // x, y, z
+    int la, lb;
+    if (dir == 0) { la = 1; lb = 2; }
+    else if (dir == 1) { la = 0; lb = 2; }
+    else { la = 0; lb = 1; }
+    a.sS = sax[dir];
+    a.sA = sax[la];
+    a.sB = sax[lb];
+    a.base = c->offset;
+    a.nS = (int32_t)c->nl[dir];
+    a.nA = (int32_t)c->nl[la];
+    a.nB = (int32_t)c->nl[lb];
+    a.T = seg_len(c, dir);
+    a.invd = 1.0 / c->dx[dir];
+    a.eps = c->eps;
+    a.dt = dt;
+    a.ca = ca;
+    a.cb = cb;
+    a.mat = c->mat;
+    const int bx = (int)std::min<int64_t>(32, a.nA);
+    const int by = (int)std::max<int64_t>(1, std::min<int64_t>(128 / bx, a.nB));
+    dim3 block(bx, by);
+    dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.nS + a.T - 1) / a.T);
+    cudaError_t e;
+    ProfScope ps(c, s, K_SWEEP_X + dir);
+    switch (c->N) {
+        case 1: e = launch_sweep<1>(c->D, dir, epi, a, grid, block, s); break;
+        case 2: e = launch_sweep<2>(c->D, dir, epi, a, grid, block, s); break;
+        case 3: e = launch_sweep<3>(c->D, dir, epi, a, grid, block, s); break;
+        default: return fail(MFC_EINVAL, "bad N");
+    }
+    if (e != cudaSuccess) return fail(MFC_ECUDA, "sweep launch: %s", cudaGetErrorString(e));
+    ++c->launches;
+    return MFC_OK;
+}
+
+// L(q) accumulated into acc (epi = ACC) or the RK stage written to out (epi = RK).
+int sweeps(mfc_ctx* c, const double* q, double* acc, int epi, double* out, const double* qn,
+           double dt, double ca, double cb, cudaStream_t s) {
+    for (int dir = 0; dir < c->D; ++dir) {
+        const bool last = dir == c->D - 1;
+        int st = launch_sweep_dir(c, dir, last ? epi : EPI_ACC, q, acc, out, qn, dt, ca, cb, s);
+        if (st) return st;
+    }
+    return MFC_OK;
+}
+
+int check_ptr(const void* p, const char* name) {
+    if (!p) return fail(MFC_EINVAL, "%s is NULL", name);
+    if (((uintptr_t)p) % 32 != 0) return fail(MFC_EINVAL, "%s is not 32-byte aligned", name);
+    return MFC_OK;
+}
+
+int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaStream_t s) {
+    static const double CA[3] = {0.0, 0.75, 1.0 / 3.0};
+    static const double CB[3] = {1.0, 0.25, 2.0 / 3.0};
+    for (int r = 0; r < count; ++r) {
+        int st = need_ws(cs[r], true);
+        if (st) return st;
+        if ((st = check_ptr(qs[r], "q"))) return st;
+        cs[r]->launches = 0;
+    }
+    std::vector<double*> in(count);
+    for (int stage = 0; stage < 3; ++stage) {
+        for (int r = 0; r < count; ++r)
+            in[r] = stage == 0 ? qs[r] : (stage == 1 ? cs[r]->S1 : cs[r]->S2);
+        int st = exchange(cs, in.data(), count, s);
+        if (st) return st;
+        for (int r = 0; r < count; ++r) {
+            mfc_ctx* c = cs[r];
+            double* out = stage == 0 ? c->S1 : (stage == 1 ? c->S2 : qs[r]);
+            if ((st = sweeps(c, in[r], c->acc, EPI_RK, out, qs[r], dt, CA[stage], CB[stage], s)))
+                return st;
+        }
+    }
+    return MFC_OK;
+}
+
+int rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int count,
+              cudaStream_t s) {
+    for (int r = 0; r < count; ++r) {
+        int st;
+        if ((st = check_ptr(qs[r], "q")) || (st = check_ptr(rhss[r], "rhs"))) return st;
+        if (qs[r] == rhss[r]) return fail(MFC_EINVAL, "q and rhs alias");
+        cs[r]->launches = 0;
+    }
+    int st = exchange(cs, qs, count, s);
+    if (st) return st;
+    for (int r = 0; r < count; ++r)
+        if ((st = sweeps(cs[r], qs[r], rhss[r], EPI_ACC, nullptr, nullptr, 0, 0, 0, s)))
+            return st;
+    return MFC_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* mfc_last_error(void) { return g_err.c_str(); }
+
+const char* mfc_version(void) { return "libmfc 0.1 sm_100a fp64"; }
+
+int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double* gamma,
+             const double* pi_inf, const int32_t bc[6], const mfc_comm* comm, int32_t device) {
+    g_err.clear();
+    if (!out || !grid || !gamma || !pi_inf || !bc) return fail(MFC_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (grid->ndim < 1 || grid->ndim > 3) return fail(MFC_EINVAL, "ndim must be 1..3");
+    if (n_fluids < 1 || n_fluids > kMaxFluids) return fail(MFC_EINVAL, "n_fluids must be 1..3");
+    for (int i = 0; i < n_fluids; ++i) {
+        if (!(gamma[i] > 1.0) || !std::isfinite(gamma[i]))
+            return fail(MFC_EINVAL, "gamma[%d] must be > 1", i);
+        if (!(pi_inf[i] >= 0.0) || !std::isfinite(pi_inf[i]))
+            return fail(MFC_EINVAL, "pi_inf[%d] must be >= 0", i);
+    }
+    const int D = grid->ndim;
+    int nranks = comm ? comm->nranks : 1;
+    int rank = comm ? comm->rank : 0;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(MFC_EINVAL, "bad rank/nranks");
+    int64_t prod = 1;
+    for (int k = 0; k < 3; ++k) {
+        const int p = grid->procs[k] > 0 ? grid->procs[k] : 1;
+        prod *= p;
+        if (k >= D && (grid->n_global[k] != 1 || p != 1))
+            return fail(MFC_EINVAL, "inactive dim %d must have n=1, procs=1", k);
+        if (k < D) {
+            if (grid->n_global[k] < 1) return fail(MFC_EINVAL, "n_global[%d] < 1", k);
+            if (!(grid->hi[k] > grid->lo[k])) return fail(MFC_EINVAL, "hi[%d] <= lo[%d]", k, k);
+            const bool per_lo = bc[2 * k] == MFC_BC_PERIODIC, per_hi = bc[2 * k + 1] == MFC_BC_PERIODIC;
+            if (per_lo != per_hi) return fail(MFC_EINVAL, "dim %d periodic on one end only", k);
+            for (int sd = 0; sd < 2; ++sd) {
+                const int b = bc[2 * k + sd];
+                if (b != MFC_BC_PERIODIC && b != MFC_BC_REFLECTIVE && b != MFC_BC_EXTRAPOLATION)
+                    return fail(MFC_EINVAL, "bc[%d] = %d unknown", 2 * k + sd, b);
+            }
+        }
+    }
+    if (prod != nranks) return fail(MFC_EINVAL, "prod(procs) = %lld != nranks = %d",
+                                    (long long)prod, nranks);
+
+    mfc_ctx* c = new mfc_ctx();
+    c->device = device;
+    c->N = n_fluids;
+    c->D = D;
+    c->E = 2 * n_fluids + D + 1;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->loopback = comm && comm->loopback;
+    for (int k = 0; k < 3; ++k) c->procs[k] = grid->procs[k] > 0 ? grid->procs[k] : 1;
+    c->coords[0] = rank % c->procs[0];
+    c->coords[1] = (rank / c->procs[0]) % c->procs[1];
+    c->coords[2] = rank / (c->procs[0] * c->procs[1]);
+    for (int k = 0; k < 3; ++k) {
+        const int64_t n = grid->n_global[k], p = c->procs[k], ci = c->coords[k];
+        const int64_t base = n / p, rem = n % p;
+        c->nl[k] = base + (ci < rem ? 1 : 0);
+        c->lo_g[k] = ci * base + std::min<int64_t>(ci, rem);
+        c->dx[k] = k < D ? (grid->hi[k] - grid->lo[k]) / (double)n : 1.0;
+        if (k < D && p > 1 && c->nl[k] < kGhost) {
+            delete c;
+            return fail(MFC_EINVAL, "dim %d: local extent %lld < 3", k, (long long)c->nl[k]);
+        }
+        if (k < D && bc[2 * k] == MFC_BC_PERIODIC && n < kGhost) {
+            delete c;
+            return fail(MFC_EINVAL, "periodic dim %d needs >= 3 cells", k);
+        }
+    }
+    // neighbours (rank = cx + px*(cy + py*cz))
+    for (int k = 0; k < D; ++k) {
+        for (int sd = 0; sd < 2; ++sd) {
+            const int f = 2 * k + sd;
+            c->bc[f] = bc[f];
+            if (c->procs[k] == 1) continue;
+            int cc[3] = {c->coords[0], c->coords[1], c->coords[2]};
+            cc[k] += sd ? 1 : -1;
+            if (cc[k] < 0 || cc[k] >= c->procs[k]) {
+                if (bc[f] != MFC_BC_PERIODIC) continue;
+                cc[k] = (cc[k] + c->procs[k]) % c->procs[k];
+            }
+            c->bc[f] = BC_NEIGHBOR;
+            c->nbr[f] = cc[0] + c->procs[0] * (cc[1] + c->procs[1] * cc[2]);
+        }
+    }
+    for (int i = 0; i < n_fluids; ++i) {
+        c->mat.Gam[i] = 1.0 / (gamma[i] - 1.0);
+        c->mat.Pi[i] = (gamma[i] * pi_inf[i]) / (gamma[i] - 1.0);
+    }
+    // layout
+    const int64_t X = ((kXOff + c->nl[0] + kGhost) + 3) / 4 * 4;
+    const int64_t Y = D >= 2 ? c->nl[1] + 2 * kGhost : 1;
+    const int64_t Z = D >= 3 ? c->nl[2] + 2 * kGhost : 1;
+    c->dims[0] = c->E; c->dims[1] = Z; c->dims[2] = Y; c->dims[3] = X;
+    c->stride[3] = 1; c->stride[2] = X; c->stride[1] = X * Y; c->stride[0] = X * Y * Z;
+    c->off[0] = kXOff;
+    c->off[1] = D >= 2 ? kGhost : 0;
+    c->off[2] = D >= 3 ? kGhost : 0;
+    c->offset = c->off[2] * c->stride[1] + c->off[1] * c->stride[2] + c->off[0];
+    c->n_elems = c->E * X * Y * Z;
+    size_t need = 3 * (size_t)c->n_elems * sizeof(double);
+    for (int k = 0; k < D; ++k) {
+        const int t1 = (k + 1) % 3, t2 = (k + 2) % 3;
+        c->face_elems[k] = (int64_t)c->E * kGhost * c->nl[t1] * c->nl[t2];
+        for (int sd = 0; sd < 2; ++sd)
+            if (c->bc[2 * k + sd] == BC_NEIGHBOR)
+                need += 2 * (((size_t)c->face_elems[k] * sizeof(double) + 255) / 256 * 256);
+    }
+    c->ws_need = need;
+    if (const char* sg = getenv("MFC_SEG")) c->seg = atoi(sg);
+
+    // The device is only touched here when NCCL needs it; single-domain and loopback
+    // contexts are pure host bookkeeping until the first GPU call (so layouts can be
+    // queried on a machine without a GPU).
+    if (nranks > 1 && !c->loopback) {
+        if (cudaSetDevice(device) != cudaSuccess) {
+            delete c;
+            return fail(MFC_ECUDA, "cudaSetDevice(%d) failed", device);
+        }
+        if (!comm->nccl_unique_id) {
+            delete c;
+            return fail(MFC_EINVAL, "nccl_unique_id is NULL with nranks > 1");
+        }
+        ncclUniqueId id;
+        memcpy(&id, comm->nccl_unique_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            delete c;
+            return fail(MFC_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+        }
+    }
+    *out = c;
+    return MFC_OK;
+}
+
+int mfc_get_layout(const mfc_ctx* c, mfc_layout* o) {
+    if (!c || !o) return fail(MFC_EINVAL, "NULL argument");
+    o->E = c->E;
+    o->ghost = kGhost;
+    o->n_fluids = c->N;
+    o->ndim = c->D;
+    for (int k = 0; k < 3; ++k) {
+        o->n_local[k] = c->nl[k];
+        o->lo_global[k] = c->lo_g[k];
+    }
+    for (int k = 0; k < 4; ++k) {
+        o->dims[k] = c->dims[k];
+        o->stride[k] = c->stride[k];
+    }
+    o->offset = c->offset;
+    o->n_elems = c->n_elems;
+    o->workspace_bytes = c->ws_need;
+    return MFC_OK;
+}
+
+int mfc_get_neighbors(const mfc_ctx* c, int32_t nbr[6]) {
+    if (!c || !nbr) return fail(MFC_EINVAL, "NULL argument");
+    for (int f = 0; f < 6; ++f) nbr[f] = c->bc[f] == BC_NEIGHBOR ? c->nbr[f] : -1;
+    return MFC_OK;
+}
+
+int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
+    if (!c || !p) return fail(MFC_EINVAL, "NULL argument");
+    if ((uintptr_t)p % 256) return fail(MFC_EINVAL, "workspace not 256-byte aligned");
+    if (bytes < c->ws_need)
+        return fail(MFC_ENOMEM, "workspace %zu < %zu bytes", bytes, c->ws_need);
+    c->ws = (char*)p;
+    c->ws_bytes = bytes;
+    char* w = c->ws;
+    const size_t sb = (size_t)c->n_elems * sizeof(double);
+    c->S1 = (double*)w; w += sb;
+    c->S2 = (double*)w; w += sb;
+    c->acc = (double*)w; w += sb;
+    for (int f = 0; f < 6; ++f) {
+        c->sendb[f] = c->recvb[f] = nullptr;
+        if (f / 2 < c->D && c->bc[f] == BC_NEIGHBOR) {
+            const size_t fb = ((size_t)c->face_elems[f / 2] * sizeof(double) + 255) / 256 * 256;
+            c->sendb[f] = (double*)w; w += fb;
+            c->recvb[f] = (double*)w; w += fb;
+        }
+    }
+    return MFC_OK;
+}
+
+int mfc_set_weno_eps(mfc_ctx* c, double eps) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (!(eps >= 1e-40 && eps <= 1e-2)) return fail(MFC_EINVAL, "eps out of [1e-40, 1e-2]");
+    c->eps = eps;
+    return MFC_OK;
+}
+
+static int eos(mfc_ctx* c, const double* in, double* out, bool to_cons, void* stream) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    int st;
+    if ((st = check_ptr(in, "input")) || (st = check_ptr(out, "output"))) return st;
+    if (in == out) return fail(MFC_EINVAL, "input and output alias");
+    if ((st = set_device(c))) return st;
+    EosArgs a;
+    a.in = in;
+    a.out = out;
+    a.sE = c->stride[0];
+    a.sZ = c->stride[1];
+    a.sY = c->stride[2];
+    a.base = c->offset;
+    a.nx = (int32_t)c->nl[0];
+    a.ny = (int32_t)c->nl[1];
+    a.nz = (int32_t)c->nl[2];
+    a.mat = c->mat;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    switch (c->N) {
+        case 1: e = launch_eos<1>(c->D, to_cons, a, s); break;
+        case 2: e = launch_eos<2>(c->D, to_cons, a, s); break;
+        default: e = launch_eos<3>(c->D, to_cons, a, s); break;
+    }
+    if (e != cudaSuccess) return fail(MFC_ECUDA, "eos launch: %s", cudaGetErrorString(e));
+    return MFC_OK;
+}
+
+int mfc_prim_to_cons(mfc_ctx* c, const double* v, double* q, void* stream) {
+    return eos(c, v, q, true, stream);
+}
+
+int mfc_cons_to_prim(mfc_ctx* c, const double* q, double* v, void* stream) {
+    return eos(c, q, v, false, stream);
+}
+
+int mfc_halo_exchange(mfc_ctx* c, double* q, void* stream) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    int st;
+    if ((st = check_ptr(q, "q")) || (st = set_device(c))) return st;
+    c->launches = 0;
+    return exchange(&c, &q, 1, (cudaStream_t)stream);
+}
+
+int mfc_rhs(mfc_ctx* c, double* q, double* rhs, void* stream) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    int st = set_device(c);
+    if (st) return st;
+    return rhs_group(&c, &q, &rhs, 1, (cudaStream_t)stream);
+}
+
+int mfc_rk3_step(mfc_ctx* c, double* q, double dt, void* stream) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (!std::isfinite(dt)) return fail(MFC_EINVAL, "dt not finite");
+    int st = set_device(c);
+    if (st) return st;
+    return rk3_group(&c, &q, 1, dt, (cudaStream_t)stream);
+}
+
+int mfc_advance_host(mfc_ctx* c, const double* q_in, double* q_out, double* q_dev,
+                     int64_t nsteps, double dt, void* stream) {
+    if (!c || !q_in || !q_out) return fail(MFC_EINVAL, "NULL argument");
+    if (nsteps < 0) return fail(MFC_EINVAL, "nsteps < 0");
+    int st;
+    if ((st = check_ptr(q_dev, "q_dev")) || (st = set_device(c))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t row = (size_t)c->nl[0] * sizeof(double);
+    const size_t pitch = (size_t)c->stride[2] * sizeof(double);
+    auto copy = [&](bool h2d) -> int {
+        for (int e = 0; e < c->E; ++e) {
+            cudaMemcpy3DParms p = {};
+            double* dev = q_dev + c->offset + e * c->stride[0];
+            double* host = (double*)(h2d ? q_in : q_out) + (size_t)e * c->nl[0] * c->nl[1] * c->nl[2];
+            cudaPitchedPtr hp = make_cudaPitchedPtr(host, row, c->nl[0], c->nl[1]);
+            cudaPitchedPtr dp = make_cudaPitchedPtr(dev, pitch, c->nl[0], c->dims[2]);
+            p.srcPtr = h2d ? hp : dp;
+            p.dstPtr = h2d ? dp : hp;
+            p.extent = make_cudaExtent(row, c->nl[1], c->nl[2]);
+            p.kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+            CU_TRY(cudaMemcpy3DAsync(&p, s));
+        }
+        return MFC_OK;
+    };
+    if ((st = copy(true))) return st;
+    for (int64_t i = 0; i < nsteps; ++i)
+        if ((st = rk3_group(&c, &q_dev, 1, dt, s))) return st;
+    if ((st = copy(false))) return st;
+    CU_TRY(cudaStreamSynchronize(s));
+    return MFC_OK;
+}
+
+int mfc_halo_exchange_group(mfc_ctx* const* cs, double* const* qs, int32_t count, void* stream) {
+    if (!cs || !qs || count < 1) return fail(MFC_EINVAL, "bad group");
+    int st = set_device(cs[0]);
+    if (st) return st;
+    for (int r = 0; r < count; ++r) cs[r]->launches = 0;
+    return exchange(cs, qs, count, (cudaStream_t)stream);
+}
+
+int mfc_rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int32_t count,
+                  void* stream) {
+    if (!cs || !qs || !rhss || count < 1) return fail(MFC_EINVAL, "bad group");
+    int st = set_device(cs[0]);
+    if (st) return st;
+    return rhs_group(cs, qs, rhss, count, (cudaStream_t)stream);
+}
+
+int mfc_rk3_step_group(mfc_ctx* const* cs, double* const* qs, int32_t count, double dt,
+                       void* stream) {
+    if (!cs || !qs || count < 1) return fail(MFC_EINVAL, "bad group");
+    int st = set_device(cs[0]);
+    if (st) return st;
+    return rk3_group(cs, qs, count, dt, (cudaStream_t)stream);
+}
+
+int64_t mfc_last_launch_count(const mfc_ctx* c) { return c ? c->launches : -1; }
+
+int mfc_nccl_get_unique_id(void* out128) {
+    if (!out128) return fail(MFC_EINVAL, "NULL argument");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out128, &id, sizeof id);
+    return MFC_OK;
+}
+
+int mfc_profile_enable(mfc_ctx* c, int32_t on) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    c->prof = on != 0;
+    c->recs.clear();
+    c->ev_used = 0;
+    return MFC_OK;
+}
+
+int mfc_profile_read(mfc_ctx* c, double* ms, int64_t* count, int32_t nkinds) {
+    if (!c || !ms || !count || nkinds < 1) return fail(MFC_EINVAL, "bad argument");
+    for (int k = 0; k < nkinds; ++k) { ms[k] = 0.0; count[k] = 0; }
+    for (const auto& r : c->recs) {
+        CU_TRY(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        CU_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+        if (r.kind < nkinds) { ms[r.kind] += t; count[r.kind] += 1; }
+    }
+    c->recs.clear();
+    c->ev_used = 0;
+    return MFC_OK;
+}
+
+int mfc_finalize(mfc_ctx* c) {
+    if (!c) return MFC_OK;
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+    return MFC_OK;
+}
+
+}  // extern "C"

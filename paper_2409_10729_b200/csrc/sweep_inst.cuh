@@ -1,0 +1,73 @@
+// sweep_inst.cuh -- instantiates the sweep and EOS kernels for one fluid count N
+// (included by sweep_n{1,2,3}.cu with MFC_NF defined).
+#pragma once
+#include "dispatch.h"
+
+namespace mfc {
+
+template <class M>
+__global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons) {
+    const int64_t n = (int64_t)a.nx * a.ny * a.nz;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % a.nx);
+        const int j = (int)((t / a.nx) % a.ny);
+        const int k = (int)(t / ((int64_t)a.nx * a.ny));
+        const int64_t c = a.base + (int64_t)k * a.sZ + (int64_t)j * a.sY + i;
+        double x[M::E], y[M::E];
+#pragma unroll
+        for (int e = 0; e < M::E; ++e) x[e] = a.in[c + e * a.sE];
+        if (to_cons) prim_to_cons<M>(x, y, a.mat);
+        else cons_to_prim<M>(x, y, a.mat);
+#pragma unroll
+        for (int e = 0; e < M::E; ++e) a.out[c + e * a.sE] = y[e];
+    }
+}
+
+template <class M, int DIR>
+static cudaError_t launch_dir(int epi, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
+    constexpr bool RA = DIR > 0;
+    if (DIR == M::D - 1 && epi == EPI_RK)
+        sweep_kernel<M, DIR, RA, EPI_RK><<<g, b, 0, s>>>(a);
+    else
+        sweep_kernel<M, DIR, RA, EPI_ACC><<<g, b, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int NF, int ND>
+static cudaError_t launch_model(int DIR, int epi, const SweepArgs& a, dim3 g, dim3 b,
+                                cudaStream_t s) {
+    using M = Model<NF, ND>;
+    switch (DIR) {
+        case 0: return launch_dir<M, 0>(epi, a, g, b, s);
+        case 1: if constexpr (ND > 1) return launch_dir<M, 1>(epi, a, g, b, s); break;
+        case 2: if constexpr (ND > 2) return launch_dir<M, 2>(epi, a, g, b, s); break;
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <>
+cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int epi, const SweepArgs& a, dim3 g, dim3 b,
+                                 cudaStream_t s) {
+    switch (D) {
+        case 1: return launch_model<MFC_NF, 1>(DIR, epi, a, g, b, s);
+        case 2: return launch_model<MFC_NF, 2>(DIR, epi, a, g, b, s);
+        case 3: return launch_model<MFC_NF, 3>(DIR, epi, a, g, b, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <>
+cudaError_t launch_eos<MFC_NF>(int D, bool to_cons, const EosArgs& a, cudaStream_t s) {
+    const int64_t n = (int64_t)a.nx * a.ny * a.nz;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    switch (D) {
+        case 1: eos_kernel<Model<MFC_NF, 1>><<<blocks, 256, 0, s>>>(a, to_cons); break;
+        case 2: eos_kernel<Model<MFC_NF, 2>><<<blocks, 256, 0, s>>>(a, to_cons); break;
+        case 3: eos_kernel<Model<MFC_NF, 3>><<<blocks, 256, 0, s>>>(a, to_cons); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace mfc

@@ -1,0 +1,322 @@
+"""Thin ctypes binding of libmfc.so (include/mfc.h) -- argument marshalling only.
+
+Every step of the RHS / RK3 path runs in the library's CUDA kernels; this module
+only allocates device memory with torch (the memory owner), passes pointers,
+sizes and the current CUDA stream, and turns status codes into exceptions.
+There is NO fallback: if libmfc.so cannot be loaded, importing this module fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libmfc.so")
+
+BC_PERIODIC = -1
+BC_REFLECTIVE = -2
+BC_EXTRAPOLATION = -3
+
+STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ESTATE",
+          -6: "EUNSUPPORTED"}
+
+EXPORTED = [
+    "mfc_init", "mfc_get_layout", "mfc_get_neighbors", "mfc_bind_workspace", "mfc_set_weno_eps",
+    "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
+    "mfc_advance_host", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
+    "mfc_nccl_get_unique_id", "mfc_last_launch_count", "mfc_profile_enable", "mfc_profile_read", "mfc_finalize", "mfc_last_error",
+    "mfc_version",
+]
+
+
+class MfcError(RuntimeError):
+    pass
+
+
+class _Grid(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("n_global", ctypes.c_int64 * 3),
+                ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
+                ("procs", ctypes.c_int32 * 3)]
+
+
+class _Comm(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("loopback", ctypes.c_int32)]
+
+
+class _Layout(ctypes.Structure):
+    _fields_ = [("E", ctypes.c_int32), ("ghost", ctypes.c_int32), ("n_fluids", ctypes.c_int32),
+                ("ndim", ctypes.c_int32), ("n_local", ctypes.c_int64 * 3),
+                ("lo_global", ctypes.c_int64 * 3), ("dims", ctypes.c_int64 * 4),
+                ("stride", ctypes.c_int64 * 4), ("offset", ctypes.c_int64),
+                ("n_elems", ctypes.c_int64), ("workspace_bytes", ctypes.c_size_t)]
+
+
+def _load():
+    if not os.path.exists(SO_PATH):
+        raise ImportError(f"{SO_PATH} is missing: run __graft_entry__.build() "
+                          "(no CPU fallback exists)")
+    L = ctypes.CDLL(SO_PATH)
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    pp = ctypes.POINTER(vp)
+    sig = {
+        "mfc_init": [ctypes.POINTER(vp), ctypes.POINTER(_Grid), i32, ctypes.POINTER(dbl),
+                     ctypes.POINTER(dbl), ctypes.POINTER(i32), ctypes.POINTER(_Comm), i32],
+        "mfc_get_layout": [vp, ctypes.POINTER(_Layout)],
+        "mfc_get_neighbors": [vp, ctypes.POINTER(i32)],
+        "mfc_bind_workspace": [vp, vp, ctypes.c_size_t],
+        "mfc_set_weno_eps": [vp, dbl],
+        "mfc_prim_to_cons": [vp, vp, vp, vp],
+        "mfc_cons_to_prim": [vp, vp, vp, vp],
+        "mfc_halo_exchange": [vp, vp, vp],
+        "mfc_rhs": [vp, vp, vp, vp],
+        "mfc_rk3_step": [vp, vp, dbl, vp],
+        "mfc_advance_host": [vp, vp, vp, vp, i64, dbl, vp],
+        "mfc_halo_exchange_group": [pp, pp, i32, vp],
+        "mfc_rhs_group": [pp, pp, pp, i32, vp],
+        "mfc_rk3_step_group": [pp, pp, i32, dbl, vp],
+        "mfc_nccl_get_unique_id": [vp],
+        "mfc_last_launch_count": [vp],
+        "mfc_profile_enable": [vp, i32],
+        "mfc_profile_read": [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), i32],
+        "mfc_finalize": [vp],
+        "mfc_last_error": [],
+        "mfc_version": [],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.mfc_last_launch_count.restype = i64
+    L.mfc_last_error.restype = ctypes.c_char_p
+    L.mfc_version.restype = ctypes.c_char_p
+    return L
+
+
+lib = _load()
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib.mfc_last_error().decode(errors="replace")
+        raise MfcError(f"{what} failed: {STATUS.get(rc, rc)}: {msg}")
+
+
+def version() -> str:
+    return lib.mfc_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.mfc_nccl_get_unique_id(buf), "mfc_nccl_get_unique_id")
+    return buf.raw
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    assert t.dtype == torch.float64 and t.is_cuda
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class Layout:
+    E: int
+    ghost: int
+    n_fluids: int
+    ndim: int
+    n_local: tuple
+    lo_global: tuple
+    dims: tuple
+    stride: tuple
+    offset: int
+    n_elems: int
+    workspace_bytes: int
+
+
+class Solver:
+    """One subdomain (rank) of the 5-equation RHS / SSP-RK3 path on one GPU."""
+
+    def __init__(self, problem, *, procs=(1, 1, 1), rank=0, nranks=1, nccl_id: bytes | None = None,
+                 loopback=False, device=None, weno_eps=None, n_global=None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device)
+        self.problem = problem
+        g = _Grid()
+        g.ndim = problem.ndim
+        ng = problem.n if n_global is None else n_global
+        for k in range(3):
+            g.n_global[k] = int(ng[k])
+            g.lo[k] = float(problem.lo[k])
+            g.hi[k] = float(problem.hi[k])
+            g.procs[k] = int(procs[k])
+        N = problem.n_fluids
+        gam = (ctypes.c_double * N)(*problem.gamma[:N])
+        pinf = (ctypes.c_double * N)(*problem.pi_inf[:N])
+        bc = (ctypes.c_int32 * 6)(*problem.bc)
+        comm = _Comm()
+        comm.rank, comm.nranks, comm.loopback = rank, nranks, int(loopback)
+        self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        comm.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id else None
+        h = ctypes.c_void_p()
+        _check(lib.mfc_init(ctypes.byref(h), ctypes.byref(g), N, gam, pinf, bc,
+                            ctypes.byref(comm), device), "mfc_init")
+        self._h = h
+        lay = _Layout()
+        _check(lib.mfc_get_layout(h, ctypes.byref(lay)), "mfc_get_layout")
+        self.layout = Layout(lay.E, lay.ghost, lay.n_fluids, lay.ndim, tuple(lay.n_local),
+                             tuple(lay.lo_global), tuple(lay.dims), tuple(lay.stride),
+                             lay.offset, lay.n_elems, lay.workspace_bytes)
+        nb = (ctypes.c_int32 * 6)()
+        _check(lib.mfc_get_neighbors(h, nb), "mfc_get_neighbors")
+        self.neighbors = tuple(nb)
+        eps = weno_eps if weno_eps is not None else getattr(problem, "weno_eps", 1e-16)
+        _check(lib.mfc_set_weno_eps(h, float(eps)), "mfc_set_weno_eps")
+        # torch owns the workspace (256-byte aligned by the caching allocator)
+        nbytes = self.layout.workspace_bytes
+        self.workspace = torch.empty((nbytes + 7) // 8, dtype=torch.float64, device=self.device)
+        _check(lib.mfc_bind_workspace(h, _ptr(self.workspace), nbytes), "mfc_bind_workspace")
+
+    # ------------------------------------------------------------- buffers
+    def empty_state(self) -> torch.Tensor:
+        return torch.zeros(self.layout.n_elems, dtype=torch.float64, device=self.device)
+
+    def interior(self, t: torch.Tensor) -> torch.Tensor:
+        """(E, nz, ny, nx) strided view of the interior cells of a state buffer."""
+        L = self.layout
+        nx, ny, nz = L.n_local
+        return t.as_strided((L.E, nz, ny, nx), (L.stride[0], L.stride[1], L.stride[2], 1),
+                            L.offset)
+
+    def state_from_prims(self, prims: np.ndarray | torch.Tensor) -> torch.Tensor:
+        """Upload primitive fields (E, nz, ny, nx) and convert them with mfc_prim_to_cons."""
+        v = self.empty_state()
+        self.interior(v).copy_(torch.as_tensor(prims, dtype=torch.float64))
+        q = self.empty_state()
+        self.prim_to_cons(v, q)
+        return q
+
+    def state_from_cons(self, cons) -> torch.Tensor:
+        q = self.empty_state()
+        self.interior(q).copy_(torch.as_tensor(cons, dtype=torch.float64))
+        return q
+
+    # ------------------------------------------------------------- calls
+    def prim_to_cons(self, v, q, stream=None):
+        _check(lib.mfc_prim_to_cons(self._h, _ptr(v), _ptr(q), _stream(stream)), "mfc_prim_to_cons")
+
+    def cons_to_prim(self, q, v, stream=None):
+        _check(lib.mfc_cons_to_prim(self._h, _ptr(q), _ptr(v), _stream(stream)), "mfc_cons_to_prim")
+
+    def halo_exchange(self, q, stream=None):
+        _check(lib.mfc_halo_exchange(self._h, _ptr(q), _stream(stream)), "mfc_halo_exchange")
+
+    def rhs(self, q, out=None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = self.empty_state()
+        _check(lib.mfc_rhs(self._h, _ptr(q), _ptr(out), _stream(stream)), "mfc_rhs")
+        return out
+
+    def rk3_step(self, q, dt: float, stream=None):
+        _check(lib.mfc_rk3_step(self._h, _ptr(q), float(dt), _stream(stream)), "mfc_rk3_step")
+
+    def advance_host(self, q_in: torch.Tensor, q_out: torch.Tensor, q_dev: torch.Tensor,
+                     nsteps: int, dt: float, stream=None):
+        """End-to-end call with host buffers (dense interior (E, nz, ny, nx) float64)."""
+        assert q_in.device.type == "cpu" and q_out.device.type == "cpu"
+        assert q_in.is_contiguous() and q_out.is_contiguous()
+        _check(lib.mfc_advance_host(self._h, ctypes.c_void_p(q_in.data_ptr()),
+                                    ctypes.c_void_p(q_out.data_ptr()), _ptr(q_dev),
+                                    int(nsteps), float(dt), _stream(stream)), "mfc_advance_host")
+
+    KINDS = ("sweep_x", "sweep_y", "sweep_z", "bc_fill", "halo", "eos")
+
+    def profile(self, on: bool = True):
+        _check(lib.mfc_profile_enable(self._h, int(on)), "mfc_profile_enable")
+
+    def profile_read(self) -> dict:
+        n = len(self.KINDS)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _check(lib.mfc_profile_read(self._h, ms, cnt, n), "mfc_profile_read")
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(self.KINDS)}
+
+    def last_launch_count(self) -> int:
+        return int(lib.mfc_last_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.mfc_finalize(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def describe(problem, procs=(1, 1, 1), rank=0, nranks=1):
+    """Host-only query of a rank's layout and neighbours (no GPU touched): creates a
+    context in loopback mode, reads mfc_get_layout / mfc_get_neighbors, finalizes."""
+    g = _Grid()
+    g.ndim = problem.ndim
+    for k in range(3):
+        g.n_global[k] = int(problem.n[k])
+        g.lo[k] = float(problem.lo[k])
+        g.hi[k] = float(problem.hi[k])
+        g.procs[k] = int(procs[k])
+    N = problem.n_fluids
+    gam = (ctypes.c_double * N)(*problem.gamma[:N])
+    pinf = (ctypes.c_double * N)(*problem.pi_inf[:N])
+    bc = (ctypes.c_int32 * 6)(*problem.bc)
+    comm = _Comm()
+    comm.rank, comm.nranks, comm.loopback = rank, nranks, 1
+    h = ctypes.c_void_p()
+    _check(lib.mfc_init(ctypes.byref(h), ctypes.byref(g), N, gam, pinf, bc, ctypes.byref(comm), 0),
+           "mfc_init")
+    try:
+        lay = _Layout()
+        _check(lib.mfc_get_layout(h, ctypes.byref(lay)), "mfc_get_layout")
+        nb = (ctypes.c_int32 * 6)()
+        _check(lib.mfc_get_neighbors(h, nb), "mfc_get_neighbors")
+        return (Layout(lay.E, lay.ghost, lay.n_fluids, lay.ndim, tuple(lay.n_local),
+                       tuple(lay.lo_global), tuple(lay.dims), tuple(lay.stride), lay.offset,
+                       lay.n_elems, lay.workspace_bytes), tuple(nb))
+    finally:
+        lib.mfc_finalize(h)
+
+
+def _arr(objs):
+    return (ctypes.c_void_p * len(objs))(*[ctypes.c_void_p(o) for o in objs])
+
+
+def rk3_step_group(solvers, qs, dt, stream=None):
+    """Loopback group step: len(solvers) subdomains on one GPU (comm.loopback = 1)."""
+    hs = _arr([s._h.value for s in solvers])
+    ps = _arr([q.data_ptr() for q in qs])
+    _check(lib.mfc_rk3_step_group(hs, ps, len(solvers), float(dt), _stream(stream)),
+           "mfc_rk3_step_group")
+
+
+def rhs_group(solvers, qs, outs, stream=None):
+    hs = _arr([s._h.value for s in solvers])
+    ps = _arr([q.data_ptr() for q in qs])
+    os_ = _arr([o.data_ptr() for o in outs])
+    _check(lib.mfc_rhs_group(hs, ps, os_, len(solvers), _stream(stream)), "mfc_rhs_group")
+
+
+def halo_exchange_group(solvers, qs, stream=None):
+    hs = _arr([s._h.value for s in solvers])
+    ps = _arr([q.data_ptr() for q in qs])
+    _check(lib.mfc_halo_exchange_group(hs, ps, len(solvers), _stream(stream)),
+           "mfc_halo_exchange_group")

@@ -1,0 +1,123 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/mfc.h
+declares, validates arguments, and its host-side layout / decomposition bookkeeping
+is consistent (no GPU needed: contexts touch the device only when launching work)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2409_10729_b200 import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def mfc():
+    from paper_2409_10729_b200 import build
+    build.build()
+    from paper_2409_10729_b200 import mfc as m
+    return m
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "mfc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mfc_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(mfc):
+    declared = _declared()
+    assert len(declared) >= 18
+    lib = ctypes.CDLL(mfc.SO_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(mfc.EXPORTED)
+    assert "sm_100a" in mfc.version()
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+    so = os.path.join(ROOT, "paper_2409_10729_b200", "libmfc.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _init(mfc, pb, procs=(1, 1, 1), rank=0, nranks=1, gamma=None, pinf=None, bc=None):
+    g = mfc._Grid()
+    g.ndim = pb.ndim
+    for k in range(3):
+        g.n_global[k] = pb.n[k]
+        g.lo[k], g.hi[k] = pb.lo[k], pb.hi[k]
+        g.procs[k] = procs[k]
+    N = pb.n_fluids
+    gam = (ctypes.c_double * N)(*(gamma or pb.gamma))
+    pi = (ctypes.c_double * N)(*(pinf or pb.pi_inf))
+    b = (ctypes.c_int32 * 6)(*(bc or pb.bc))
+    c = mfc._Comm()
+    c.rank, c.nranks, c.loopback = rank, nranks, 1
+    h = ctypes.c_void_p()
+    rc = mfc.lib.mfc_init(ctypes.byref(h), ctypes.byref(g), N, gam, pi, b, ctypes.byref(c), 0)
+    if rc == 0:
+        mfc.lib.mfc_finalize(h)
+    return rc, mfc.lib.mfc_last_error().decode()
+
+
+def test_argument_validation(mfc):
+    pb = W.random_problem(3, (16, 16, 16), 2, "water")
+    assert _init(mfc, pb)[0] == 0
+    assert _init(mfc, pb, gamma=(1.0, 1.4))[0] == -1               # gamma <= 1
+    assert _init(mfc, pb, pinf=(-1.0, 0.0))[0] == -1               # pi_inf < 0
+    assert _init(mfc, pb, bc=(-1, -3, -1, -1, -1, -1))[0] == -1    # periodic on one end
+    assert _init(mfc, pb, bc=(-7,) * 6)[0] == -1                   # unknown bc
+    assert _init(mfc, pb, procs=(1, 1, 2), nranks=3)[0] == -1      # prod(procs) != nranks
+    assert _init(mfc, pb, procs=(1, 1, 8), nranks=8)[0] == -1      # 2 cells per rank < 3
+    rc, msg = _init(mfc, W.Problem("bad", 4, 1, (8, 1, 1), gamma=(1.4,) * 4, pi_inf=(0,) * 4))
+    assert rc == -1 and "n_fluids" in msg
+
+
+def test_layout_alignment_and_sizes(mfc):
+    for pb in (W.c1_water_air(), W.c2_shock_bubble(), W.c3_droplet(256), W.c5_three_fluid(64),
+               W.random_problem(3, (37, 5, 9), 3, "gas")):
+        L, nb = mfc.describe(pb)
+        assert L.E == pb.E and L.n_local == pb.n and nb == (-1,) * 6
+        assert L.stride[3] == 1 and L.stride[2] % 4 == 0            # 32-byte rows
+        assert (L.offset % L.stride[2]) % 4 == 0                     # interior x 32 B aligned
+        assert L.dims[3] >= pb.n[0] + 4 + 3
+        for k in range(1, 3):
+            assert L.dims[3 - k] == (pb.n[k] + 6 if k < pb.ndim else 1)
+        assert L.n_elems == np.prod(L.dims)
+        assert L.workspace_bytes >= 3 * 8 * L.n_elems
+
+
+@pytest.mark.parametrize("procs", [(1, 1, 4), (1, 2, 2), (2, 2, 2), (1, 1, 3), (2, 1, 3)])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_decomposition_bookkeeping(mfc, procs, periodic):
+    """Extents tile the global grid; neighbour relations are symmetric; periodic wrap."""
+    bc = W.BC_PERIODIC if periodic else W.BC_EXTRAPOLATION
+    pb = W.random_problem(3, (26, 19, 31), 2, "gas", bc=bc)
+    P = int(np.prod(procs))
+    info = [mfc.describe(pb, procs, r, P) for r in range(P)]
+    cover = np.zeros(pb.n[::-1], dtype=int)
+    for L, nb in info:
+        lo, n = L.lo_global, L.n_local
+        cover[lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]] += 1
+    assert np.all(cover == 1)
+    for r, (L, nb) in enumerate(info):
+        for f in range(6):
+            k = f // 2
+            if procs[k] == 1 or (not periodic and
+                                 ((f % 2 == 0 and L.lo_global[k] == 0) or
+                                  (f % 2 == 1 and L.lo_global[k] + L.n_local[k] == pb.n[k]))):
+                assert nb[f] == -1
+            else:
+                o = nb[f]
+                assert 0 <= o < P and info[o][1][f ^ 1] == r
+                # the neighbour's face is adjacent (mod the global extent)
+                Lo = info[o][0]
+                if f % 2:
+                    assert (L.lo_global[k] + L.n_local[k]) % pb.n[k] == Lo.lo_global[k]
+                else:
+                    assert (Lo.lo_global[k] + Lo.n_local[k]) % pb.n[k] == L.lo_global[k]

@@ -1,0 +1,141 @@
+"""GPU parity: libmfc (sm_100a, through the C ABI) against the CPU oracle on identical
+seeded inputs.  Tolerances are BASELINE.json north_star's: 1e-12 per RHS, 1e-10 after
+100 RK3 steps (metric: tests/parity.py, DESIGN.md AMB-17); EOS conversions and ghost
+fills are bitwise."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2409_10729_b200 import workloads as W
+
+from parity import RHS_TOL, STEP100_TOL, gpu_rhs, gpu_solver, gpu_steps, oracle_inputs, rel_err, stable_dt
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+def _rhs_case(pb, seed=W.SEED):
+    P, v, q = oracle_inputs(pb, seed)
+    ref = O.rhs(P, q)
+    assert np.all(np.isfinite(ref))
+    got = gpu_rhs(pb, q)
+    err = rel_err(got, ref)
+    assert np.all(err <= RHS_TOL), (pb.name, err)
+    return err
+
+
+RHS_CASES = [
+    ("C1", lambda: W.c1_water_air()),
+    ("C2-small", lambda: W.c2_shock_bubble(96, 48)),
+    ("C3-40", lambda: W.c3_droplet(40)),
+    ("C5-36", lambda: W.c5_three_fluid(36)),
+    ("GR-1D-N1", lambda: W.random_problem(1, (77,), 1, "gas")),
+    ("GR-1D-N3-water", lambda: W.random_problem(1, (64,), 3, "water")),
+    ("GR-2D-N2-water", lambda: W.random_problem(2, (70, 37), 2, "water")),
+    ("GR-2D-N3", lambda: W.random_problem(2, (33, 65), 3, "gas")),
+    ("GR-3D-N1", lambda: W.random_problem(3, (35, 19, 23), 1, "gas")),
+    ("GR-3D-N2-water", lambda: W.random_problem(3, (48, 48, 48), 2, "water")),
+    ("GR-3D-N3-water", lambda: W.random_problem(3, (41, 33, 70), 3, "water")),
+    ("GR-3D-refl", lambda: W.random_problem(3, (20, 21, 22), 2, "gas",
+                                            bc=(W.BC_REFLECTIVE, W.BC_EXTRAPOLATION) * 3)),
+]
+
+
+@pytest.mark.parametrize("name,make", RHS_CASES, ids=[c[0] for c in RHS_CASES])
+def test_rhs_parity(name, make):
+    _rhs_case(make())
+
+
+@pytest.mark.parametrize("n", [(3, 1, 1), (4, 3, 1), (3, 3, 3), (5, 64, 3), (200, 3, 4)])
+def test_rhs_parity_degenerate_sizes(n):
+    d = 1 if n[1] == 1 else (2 if n[2] == 1 else 3)
+    _rhs_case(W.random_problem(d, n[:d], 2, "gas"))
+
+
+def test_uniform_state_rhs_exactly_zero_on_gpu():
+    pb = W.random_problem(3, (37, 21, 19), 2, "water")
+    P = O.Problem.from_spec(pb)
+    v = W.random_prims(pb, seed=1)
+    v = np.broadcast_to(v[:, :1, :1, :1], v.shape).copy()
+    q = O.prim_to_cons(P, v)
+    got = gpu_rhs(pb, q)
+    assert np.all(got == 0.0)
+
+
+@pytest.mark.parametrize("N,d", [(1, 1), (2, 2), (3, 3), (2, 3)])
+def test_eos_conversions_bitwise(N, d):
+    pb = W.random_problem(d, (17, 9, 5)[:d], N, "water")
+    P = O.Problem.from_spec(pb)
+    v = W.random_prims(pb)
+    s = gpu_solver(pb)
+    vd = s.empty_state()
+    s.interior(vd).copy_(torch.as_tensor(v))
+    qd = s.empty_state()
+    s.prim_to_cons(vd, qd)
+    v2 = s.empty_state()
+    s.cons_to_prim(qd, v2)
+    torch.cuda.synchronize()
+    qref = O.prim_to_cons(P, v)
+    assert np.array_equal(s.interior(qd).cpu().numpy(), qref)
+    assert np.array_equal(s.interior(v2).cpu().numpy(), O.cons_to_prim(P, qref))
+
+
+@pytest.mark.parametrize("bc", [W.BC_PERIODIC, W.BC_REFLECTIVE, W.BC_EXTRAPOLATION])
+def test_ghost_fill_bitwise(bc):
+    pb = W.random_problem(3, (11, 7, 9), 2, "gas", bc=bc)
+    P = O.Problem.from_spec(pb)
+    q = O.prim_to_cons(P, W.random_prims(pb))
+    s = gpu_solver(pb)
+    qd = s.state_from_cons(q)
+    s.halo_exchange(qd)
+    torch.cuda.synchronize()
+    qp = O.pad(P, q)
+    O.fill_ghosts(P, qp)
+    L = s.layout
+    full = qd.cpu().numpy().reshape(L.dims)         # [E][Z][Y][Xpitch]
+    g = 3
+    nx, ny, nz = L.n_local
+    ox = L.offset % L.stride[2]                      # interior x offset in the pitch
+    mine = full[:, :, :, ox - g: ox + nx + g]
+    # compare face ghosts only (edges/corners are never written or read)
+    for k in range(3):
+        sl = [slice(g, g + nz), slice(g, g + ny), slice(g, g + nx)]
+        for rng_ in (slice(0, g), slice(g + pb.n[k], 2 * g + pb.n[k])):
+            sl2 = list(sl)
+            sl2[2 - k] = rng_
+            idx = (slice(None),) + tuple(sl2)
+            assert np.array_equal(mine[idx], qp[idx]), (k, bc)
+
+
+STEP_CASES = [
+    ("C1", lambda: W.c1_water_air(), None),
+    ("C2-small", lambda: W.c2_shock_bubble(64, 32), None),
+    ("C3-24", lambda: W.c3_droplet(24), None),
+    ("GR-3D-N3-water", lambda: W.random_problem(3, (20, 17, 18), 3, "water"), 0.2),
+]
+
+
+@pytest.mark.parametrize("name,make,cfl", STEP_CASES, ids=[c[0] for c in STEP_CASES])
+def test_rk3_100_steps_parity(name, make, cfl):
+    pb = make()
+    P, v, q = oracle_inputs(pb)
+    dt = pb.dt if (pb.dt and cfl is None) else stable_dt(pb, v, cfl or 0.3)
+    ref = O.rk3_step(P, q, dt, nsteps=100)
+    assert O.count_inadmissible(P, ref) == 0
+    got = gpu_steps(pb, q, dt, 100)
+    err = rel_err(got, ref)
+    assert np.all(err <= STEP100_TOL), (name, err)
+
+
+def test_one_step_parity_tight():
+    """A single RK3 step is within a few times the RHS tolerance."""
+    pb = W.random_problem(3, (30, 26, 22), 2, "water")
+    P, v, q = oracle_inputs(pb)
+    dt = stable_dt(pb, v)
+    ref = O.rk3_step(P, q, dt, 1)
+    got = gpu_steps(pb, q, dt, 1)
+    dq = rel_err(got - q, ref - q)
+    assert np.all(dq <= 10 * RHS_TOL), dq

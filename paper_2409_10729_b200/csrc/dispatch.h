@@ -7,10 +7,10 @@
 
 namespace mfc {
 
-// Launch the sweep kernel for N fluids, D dims, direction DIR.
-// epi == EPI_ACC or EPI_RK; the accumulator is read iff DIR > 0.
+// Launch the sweep kernel for N fluids, D dims, direction DIR with epilogue `mode`
+// (M_SET / M_RKINIT for DIR == 0, M_ACC for DIR > 0).
 template <int N>
-cudaError_t launch_sweep(int D, int DIR, int epi, const SweepArgs& a, dim3 grid, dim3 block,
+cudaError_t launch_sweep(int D, int DIR, int mode, const SweepArgs& a, dim3 grid, dim3 block,
                          cudaStream_t s);
 
 struct EosArgs {

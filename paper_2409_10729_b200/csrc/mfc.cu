@@ -336,12 +336,13 @@ int seg_len(const mfc_ctx* c, int dir) {
     return (int)std::min<int64_t>(T, n);
 }
 
-int launch_sweep_dir(mfc_ctx* c, int dir, int epi, const double* q, double* acc, double* out,
-                     const double* qn, double dt, double ca, double cb, cudaStream_t s) {
+int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const double* acc,
+                     double* dst, const double* qn, double w, double ca, double cb,
+                     cudaStream_t s) {
     SweepArgs a;
     a.q = q;
     a.acc = acc;
-    a.out = out;
+    a.dst = dst;
     a.qn = qn;
     a.sE = c->stride[0];
     const int64_t sax[3] = {1, c->stride[2], c->stride[1]};  // x, y, z
@@ -359,7 +360,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int epi, const double* q, double* acc,
     a.T = seg_len(c, dir);
     a.invd = 1.0 / c->dx[dir];
     a.eps = c->eps;
-    a.dt = dt;
+    a.w = w;
     a.ca = ca;
     a.cb = cb;
     a.mat = c->mat;
@@ -370,9 +371,9 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int epi, const double* q, double* acc,
     cudaError_t e;
     ProfScope ps(c, s, K_SWEEP_X + dir);
     switch (c->N) {
-        case 1: e = launch_sweep<1>(c->D, dir, epi, a, grid, block, s); break;
-        case 2: e = launch_sweep<2>(c->D, dir, epi, a, grid, block, s); break;
-        case 3: e = launch_sweep<3>(c->D, dir, epi, a, grid, block, s); break;
+        case 1: e = launch_sweep<1>(c->D, dir, mode, a, grid, block, s); break;
+        case 2: e = launch_sweep<2>(c->D, dir, mode, a, grid, block, s); break;
+        case 3: e = launch_sweep<3>(c->D, dir, mode, a, grid, block, s); break;
         default: return fail(MFC_EINVAL, "bad N");
     }
     if (e != cudaSuccess) return fail(MFC_ECUDA, "sweep launch: %s", cudaGetErrorString(e));
@@ -380,12 +381,17 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int epi, const double* q, double* acc,
     return MFC_OK;
 }
 
-// L(q) accumulated into acc (epi = ACC) or the RK stage written to out (epi = RK).
-int sweeps(mfc_ctx* c, const double* q, double* acc, int epi, double* out, const double* qn,
+// One RHS evaluation of the stencil state q, assembled across the sweeps:
+//   rk == false: dst = c_x + c_y + c_z                    (acc == dst, the rhs buffer)
+//   rk == true : dst = ca*qn + cb*(q + dt*(c_x + c_y + c_z)), accumulating in acc.
+int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const double* qn,
            double dt, double ca, double cb, cudaStream_t s) {
+    const double w = rk ? cb * dt : 1.0;
     for (int dir = 0; dir < c->D; ++dir) {
         const bool last = dir == c->D - 1;
-        int st = launch_sweep_dir(c, dir, last ? epi : EPI_ACC, q, acc, out, qn, dt, ca, cb, s);
+        double* out = last ? dst : acc;
+        const int mode = dir == 0 ? (rk ? M_RKINIT : M_SET) : M_ACC;
+        int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn, w, ca, cb, s);
         if (st) return st;
     }
     return MFC_OK;
@@ -415,7 +421,7 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
         for (int r = 0; r < count; ++r) {
             mfc_ctx* c = cs[r];
             double* out = stage == 0 ? c->S1 : (stage == 1 ? c->S2 : qs[r]);
-            if ((st = sweeps(c, in[r], c->acc, EPI_RK, out, qs[r], dt, CA[stage], CB[stage], s)))
+            if ((st = sweeps(c, in[r], c->acc, out, true, qs[r], dt, CA[stage], CB[stage], s)))
                 return st;
         }
     }
@@ -433,7 +439,7 @@ int rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int co
     int st = exchange(cs, qs, count, s);
     if (st) return st;
     for (int r = 0; r < count; ++r)
-        if ((st = sweeps(cs[r], qs[r], rhss[r], EPI_ACC, nullptr, nullptr, 0, 0, 0, s)))
+        if ((st = sweeps(cs[r], qs[r], rhss[r], rhss[r], false, nullptr, 0, 0, 0, s)))
             return st;
     return MFC_OK;
 }

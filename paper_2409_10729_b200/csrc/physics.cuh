@@ -79,6 +79,51 @@ __device__ __forceinline__ void cons_to_prim(const double (&q)[M::E], double (&v
     v[M::IE] = __ddiv_rn(__dsub_rn(__dsub_rn(q[M::IE], ke), P), G);
 }
 
+// S2 for the sweep kernels: the same formulas with ONE reciprocal per cell,
+// r = 1/(rho*Gamma): 1/rho = Gamma*r, 1/Gamma = rho*r (FMA allowed).  Differs from
+// the specified order by a few ulp of each term (within the parity metric of
+// DESIGN.md AMB-17); the bitwise-specified version above serves mfc_cons_to_prim.
+template <class M>
+__device__ __forceinline__ void cons_to_prim_fast(const double (&q)[M::E], double (&v)[M::E],
+                                                  const Materials& mat) {
+    double rho = q[0];
+#pragma unroll
+    for (int i = 1; i < M::N; ++i) rho += q[i];
+    double G = q[M::IA] * mat.Gam[0];
+    double P = q[M::IA] * mat.Pi[0];
+#pragma unroll
+    for (int i = 1; i < M::N; ++i) {
+        G = fma(q[M::IA + i], mat.Gam[i], G);
+        P = fma(q[M::IA + i], mat.Pi[i], P);
+    }
+    const double r = rcp(rho * G);
+    const double irho = G * r, iG = rho * r;
+    double ke = 0.0;
+#pragma unroll
+    for (int k = 0; k < M::D; ++k) {
+        const double u = q[M::IM + k] * irho;
+        v[M::IM + k] = u;
+        ke = fma(q[M::IM + k], u, ke);
+    }
+#pragma unroll
+    for (int i = 0; i < M::N; ++i) {
+        v[i] = q[i];
+        v[M::IA + i] = q[M::IA + i];
+    }
+    v[M::IE] = ((q[M::IE] - 0.5 * ke) - P) * iG;
+}
+
+// Fast reciprocal square root: MUFU.RSQ64H seed + two Newton steps.
+__device__ __forceinline__ double rsqrt_fast(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x;
+    double e = fma(-h * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-h * y, y, 0.5);
+    return fma(y, e, y);
+}
+
 // Inverse EOS: rho u_k = rho*u_k;  KE = 0.5 sum (rho u_k) u_k;  rhoE = (Gamma p + Pi) + KE.
 template <class M>
 __device__ __forceinline__ void prim_to_cons(const double (&v)[M::E], double (&q)[M::E],
@@ -166,8 +211,10 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     }
     const double uL = vL[M::IM + DIR], uR = vR[M::IM + DIR];
     const double pL = vL[M::IE], pR = vR[M::IE];
-    const double cL = sqrt(fma(GL + 1.0, pL, PL) * rcp(rL * GL));
-    const double cR = sqrt(fma(GR + 1.0, pR, PR) * rcp(rR * GR));
+    // c = sqrt(A/B) = A * rsqrt(A*B), A = (Gamma+1)p + Pi, B = rho*Gamma (AMB-10)
+    const double AL = fma(GL + 1.0, pL, PL), AR = fma(GR + 1.0, pR, PR);
+    const double cL = AL * rsqrt_fast(AL * (rL * GL));
+    const double cR = AR * rsqrt_fast(AR * (rR * GR));
     const double sL = fmin(uL - cL, uR - cR);
     const double sR = fmax(uL + cL, uR + cR);
     const double aL = rL * (sL - uL), aR = rR * (sR - uR);
@@ -189,7 +236,9 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     for (int k = 0; k < M::D; ++k) uu = fma(vK[M::IM + k], vK[M::IM + k], uu);
     const double EK = fma(GK, pK, PK) + 0.5 * (rK * uu);
     const double dK = sK - uK;
-    const double xi = dK * rcp(sK - sS);
+    const double dS = sK - sS;
+    const double rr = rcp(dK * dS);          // one reciprocal for xi and p_K/(s_K-u_K)
+    const double xi = (dK * dK) * rr;
     const double ufv = fma(sstar, xi - 1.0, uK);
 #pragma unroll
     for (int i = 0; i < M::N; ++i) {
@@ -204,7 +253,7 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
             F[M::IM + k] = (rK * vK[M::IM + k]) * ufv;
         }
     }
-    const double inner = fma(sS - uK, fma(rK, sS, pK * rcp(dK)), EK);
+    const double inner = fma(sS - uK, fma(rK, sS, pK * (dS * rr)), EK);
     F[M::IE] = fma(sstar, fma(xi, inner, -EK), uK * (EK + pK));
     uf = ufv;
 }

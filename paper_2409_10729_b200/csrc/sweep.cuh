@@ -4,33 +4,38 @@
 // cell:  c_e = (F_{e,m-1/2} - F_{e,m+1/2})/dx  (+ a_{i,m} (u^f_{m+1/2} - u^f_{m-1/2})/dx
 // for the volume-fraction rows, AMB-5/6), with F from WENO5 + HLLC.
 //
-// Mapping (B200 design): a thread owns one grid line segment of T cells
-// along DIR and MARCHES along it.  Consecutive lanes own neighbouring lines along the
-// unit-stride x axis for the y/z sweeps (every load/store of a warp is one contiguous
-// 256-byte row), along y for the x sweep.  Per step the thread loads the conserved
-// state of ONE new cell, converts it to primitives (S2) and shifts it into a 5-cell
-// register window; WENO5 of the window's centre cell yields both of that cell's face
-// states; the face between the previous and the current cell gets its HLLC flux; the
-// previous cell's update is written.  So every face state, face flux and primitive
-// is computed exactly once per segment and never leaves the register file -- no face
-// states in HBM (MFC wrote them, ~2 GB per sweep at 256^3), no transposes.
+// Mapping: a thread owns one grid line segment of T cells along DIR
+// and MARCHES along it.  Consecutive lanes own neighbouring lines along the unit-
+// stride x axis for the y/z sweeps (every warp load/store is one contiguous 256-byte
+// row), along y for the x sweep.  Per step the thread converts ONE new cell to
+// primitives (S2) and shifts it into a 5-cell register window; WENO5 of the window's
+// centre cell yields both of that cell's face states; the face between the previous
+// and the current cell gets its HLLC flux; the previous cell's update is written.
+// Every face state, face flux and primitive is computed once per segment and never
+// leaves the register file: no face states in HBM, no transposes.
 //
-// Epilogues (compile-time):
-//   EPI_ACC:  acc = (READ_ACC ? acc : 0) + c              (x, y sweeps; rhs mode)
-//   EPI_RK :  out = ca*qn + cb*(qs + dt*((READ_ACC ? acc : 0) + c))   (last sweep;
-//             SSP-RK3 stage of S4 fused into the flux-difference epilogue)
+// Latency hiding: all global loads are issued one march step before they are used
+// (the next cell's state, and the epilogue operands of the cell updated this step),
+// so a warp never waits on DRAM inside a step.
+//
+// Epilogues (compile-time MODE; w = cb*dt in RK stages, 1 for a plain RHS):
+//   M_SET   : dst = c                                 (first sweep, RHS)
+//   M_RKINIT: dst = ca*q^n + cb*q^s + w*c             (first sweep, SSP-RK3 stage S4)
+//   M_ACC   : dst = acc + w*c                         (later sweeps; last one -> stage)
+// so the RK stage q^(s+1) = ca q^n + cb (q^s + dt (c_x + c_y + c_z)) is assembled
+// across the sweeps without any kernel streaming more than two extra operands.
 #pragma once
 #include "physics.cuh"
 
 namespace mfc {
 
-enum { EPI_ACC = 0, EPI_RK = 1 };
+enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2 };
 
 struct SweepArgs {
     const double* __restrict__ q;   // stencil state (padded layout, ghosts filled)
-    double* acc;                    // accumulator (state layout)
-    double* out;                    // RK destination (state layout)
-    const double* qn;               // RK base state q^n (may alias out)
+    const double* acc;              // accumulator input (M_ACC)
+    double* dst;                    // destination (state layout)
+    const double* qn;               // RK base state q^n (M_RKINIT, read iff ca != 0)
     int64_t sE;                     // equation stride
     int64_t sS, sA, sB;             // strides along the sweep, lane and third axis
     int64_t base;                   // offset of interior cell (0,0,0), equation 0
@@ -38,12 +43,12 @@ struct SweepArgs {
     int32_t T;                      // segment length along the sweep
     double invd;                    // 1/dx along DIR
     double eps;                     // WENO epsilon
-    double dt, ca, cb;              // RK stage coefficients
+    double w, ca, cb;               // epilogue weights
     Materials mat;
 };
 
-template <class M, int DIR, bool READ_ACC, int EPI>
-__global__ void __launch_bounds__(128)
+template <class M, int DIR, int MODE>
+__global__ void __launch_bounds__(128, 2)
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
     const int ia = blockIdx.x * blockDim.x + threadIdx.x;
@@ -54,29 +59,46 @@ sweep_kernel(const SweepArgs a) {
     const int64_t line = a.base + (int64_t)ia * a.sA + (int64_t)ib * a.sB;
     const double* __restrict__ q = a.q;
 
-    auto load_prim = [&](int s, double (&v)[E]) {
-        double qc[E];
-        const double* p = q + line + (int64_t)s * a.sS;
+    auto load = [&](const double* __restrict__ src, int s, double (&x)[E]) {
+        const double* p = src + line + (int64_t)s * a.sS;
 #pragma unroll
-        for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
-        cons_to_prim<M>(qc, v, a.mat);
+        for (int e = 0; e < E; ++e) x[e] = __ldg(p + e * a.sE);
     };
 
     double w[5][E];        // primitive window: cells j-2 .. j+2
+    {
+        double qc[E];
 #pragma unroll
-    for (int k = 1; k < 5; ++k) load_prim(s0 - 4 + k, w[k]);   // cells s0-3 .. s0
+        for (int k = 1; k < 5; ++k) {                 // cells s0-3 .. s0
+            load(q, s0 - 4 + k, qc);
+            cons_to_prim_fast<M>(qc, w[k], a.mat);
+        }
+    }
+    double qnext[E];       // conserved state of cell j+2 (prefetched one step ahead)
+    load(q, s0 + 1, qnext);
 
     double vm_prev[E];     // v-_{j-1/2} (from cell j-1)
     double F_prev[E];      // flux at face j-3/2
     double uf_prev = 0.0;
 
     for (int j = s0 - 1; j <= s1; ++j) {
+        const bool update = j > s0;                   // cell j-1 is updated this step
+        // epilogue operands of cell j-1, issued now, consumed at the end of the step
+        double ep0[E], ep1[E];
+        if (update) {
+            if (MODE == M_ACC) load(a.acc, j - 1, ep0);
+            if (MODE == M_RKINIT) {
+                load(q, j - 1, ep0);
+                if (a.ca != 0.0) load(a.qn, j - 1, ep1);
+            }
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
 #pragma unroll
             for (int e = 0; e < E; ++e) w[k][e] = w[k + 1][e];
         }
-        load_prim(j + 2, w[4]);
+        cons_to_prim_fast<M>(qnext, w[4], a.mat);
+        if (j < s1) load(q, j + 3, qnext);            // next step's new cell
 
         double vm[E], vp[E];
 #pragma unroll
@@ -86,31 +108,20 @@ sweep_kernel(const SweepArgs a) {
         if (j >= s0) {
             double F[E], uf;
             hllc<M, DIR>(vm_prev, vp, a.mat, F, uf);
-            if (j > s0) {
-                // update cell j-1: faces j-3/2 (F_prev) and j-1/2 (F); alpha_{j-1} = w[1]
+            if (update) {
+                // cell j-1: faces j-3/2 (F_prev) and j-1/2 (F); alpha_{j-1} = w[1]
                 const int64_t c = line + (int64_t)(j - 1) * a.sS;
                 const double div = (uf - uf_prev) * a.invd;
-                double L[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     double r = (F_prev[e] - F[e]) * a.invd;
                     if (e >= M::IA) r = fma(w[1][e], div, r);
-                    L[e] = r;
-                }
-                if (EPI == EPI_ACC) {
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        double* p = a.acc + c + e * a.sE;
-                        *p = READ_ACC ? (*p + L[e]) : L[e];
-                    }
-                } else {
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const int64_t ce = c + e * a.sE;
-                        const double Lt = READ_ACC ? (a.acc[ce] + L[e]) : L[e];
-                        const double t = fma(a.dt, Lt, q[ce]);
-                        a.out[ce] = (a.ca == 0.0) ? t : fma(a.ca, a.qn[ce], a.cb * t);
-                    }
+                    double out;
+                    if (MODE == M_SET) out = r;
+                    else if (MODE == M_ACC) out = fma(a.w, r, ep0[e]);
+                    else out = fma(a.w, r, a.ca != 0.0 ? fma(a.ca, ep1[e], a.cb * ep0[e])
+                                                       : a.cb * ep0[e]);
+                    a.dst[c + e * a.sE] = out;
                 }
             }
 #pragma unroll

@@ -25,34 +25,33 @@ __global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons)
 }
 
 template <class M, int DIR>
-static cudaError_t launch_dir(int epi, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
-    constexpr bool RA = DIR > 0;
-    if (DIR == M::D - 1 && epi == EPI_RK)
-        sweep_kernel<M, DIR, RA, EPI_RK><<<g, b, 0, s>>>(a);
-    else
-        sweep_kernel<M, DIR, RA, EPI_ACC><<<g, b, 0, s>>>(a);
+static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
+    if (DIR == 0 && mode == M_SET) sweep_kernel<M, DIR, M_SET><<<g, b, 0, s>>>(a);
+    else if (DIR == 0 && mode == M_RKINIT) sweep_kernel<M, DIR, M_RKINIT><<<g, b, 0, s>>>(a);
+    else if (DIR > 0 && mode == M_ACC) sweep_kernel<M, DIR, M_ACC><<<g, b, 0, s>>>(a);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
 template <int NF, int ND>
-static cudaError_t launch_model(int DIR, int epi, const SweepArgs& a, dim3 g, dim3 b,
+static cudaError_t launch_model(int DIR, int mode, const SweepArgs& a, dim3 g, dim3 b,
                                 cudaStream_t s) {
     using M = Model<NF, ND>;
     switch (DIR) {
-        case 0: return launch_dir<M, 0>(epi, a, g, b, s);
-        case 1: if constexpr (ND > 1) return launch_dir<M, 1>(epi, a, g, b, s); break;
-        case 2: if constexpr (ND > 2) return launch_dir<M, 2>(epi, a, g, b, s); break;
+        case 0: return launch_dir<M, 0>(mode, a, g, b, s);
+        case 1: if constexpr (ND > 1) return launch_dir<M, 1>(mode, a, g, b, s); break;
+        case 2: if constexpr (ND > 2) return launch_dir<M, 2>(mode, a, g, b, s); break;
     }
     return cudaErrorInvalidValue;
 }
 
 template <>
-cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int epi, const SweepArgs& a, dim3 g, dim3 b,
+cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int mode, const SweepArgs& a, dim3 g, dim3 b,
                                  cudaStream_t s) {
     switch (D) {
-        case 1: return launch_model<MFC_NF, 1>(DIR, epi, a, g, b, s);
-        case 2: return launch_model<MFC_NF, 2>(DIR, epi, a, g, b, s);
-        case 3: return launch_model<MFC_NF, 3>(DIR, epi, a, g, b, s);
+        case 1: return launch_model<MFC_NF, 1>(DIR, mode, a, g, b, s);
+        case 2: return launch_model<MFC_NF, 2>(DIR, mode, a, g, b, s);
+        case 3: return launch_model<MFC_NF, 3>(DIR, mode, a, g, b, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -139,5 +139,5 @@ def test_one_step_parity_tight():
     dt = stable_dt(pb, v)
     ref = O.rk3_step(P, q, dt, 1)
     got = gpu_steps(pb, q, dt, 1)
-    dq = rel_err(got - q, ref - q)
+    dq = rel_err(got - q, ref - q, dt * rhs_flux_scale(pb, v, q))
     assert np.all(dq <= 10 * RHS_TOL), dq

@@ -383,15 +383,21 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
 
 // One RHS evaluation of the stencil state q, assembled across the sweeps:
 //   rk == false: dst = c_x + c_y + c_z                    (acc == dst, the rhs buffer)
-//   rk == true : dst = ca*qn + cb*(q + dt*(c_x + c_y + c_z)), accumulating in acc.
+//   rk == true : dst = ca*qn + cb*(q + dt*(c_x + c_y + c_z)), accumulating in acc:
+//     1D: x = M_RKINIT -> dst;  2D/3D: x = M_SET -> acc, y = M_RKACC, z = M_ACC.
 int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const double* qn,
            double dt, double ca, double cb, cudaStream_t s) {
     const double w = rk ? cb * dt : 1.0;
     for (int dir = 0; dir < c->D; ++dir) {
         const bool last = dir == c->D - 1;
         double* out = last ? dst : acc;
-        const int mode = dir == 0 ? (rk ? M_RKINIT : M_SET) : M_ACC;
-        int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn, w, ca, cb, s);
+        int mode;
+        if (dir == 0) mode = (rk && c->D == 1) ? M_RKINIT : M_SET;
+        else if (dir == 1 && rk) mode = M_RKACC;
+        else mode = M_ACC;
+        // M_SET in an RK stage writes the unscaled c_x; M_RKACC scales (acc + c_y) by w
+        const double wd = (mode == M_SET) ? 1.0 : w;
+        int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn, wd, ca, cb, s);
         if (st) return st;
     }
     return MFC_OK;

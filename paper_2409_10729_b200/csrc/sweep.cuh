@@ -19,23 +19,26 @@
 // so a warp never waits on DRAM inside a step.
 //
 // Epilogues (compile-time MODE; w = cb*dt in RK stages, 1 for a plain RHS):
-//   M_SET   : dst = c                                 (first sweep, RHS)
-//   M_RKINIT: dst = ca*q^n + cb*q^s + w*c             (first sweep, SSP-RK3 stage S4)
-//   M_ACC   : dst = acc + w*c                         (later sweeps; last one -> stage)
-// so the RK stage q^(s+1) = ca q^n + cb (q^s + dt (c_x + c_y + c_z)) is assembled
-// across the sweeps without any kernel streaming more than two extra operands.
+//   M_SET   : dst = c                                 (x sweep: write-only)
+//   M_RKINIT: dst = ca*q^n + cb*q^s + w*c             (1D: the only sweep, RK stage)
+//   M_RKACC : dst = ca*q^n + cb*q^s + w*(acc + c)     (y sweep, RK stage)
+//   M_ACC   : dst = acc + w*c                         (y sweep of a RHS, z sweep)
+// so the SSP-RK3 stage q^(s+1) = ca q^n + cb (q^s + dt (c_x + c_y + c_z)) (S4) is
+// assembled across the sweeps; the extra operands q^s, q^n are streamed by the y sweep,
+// whose warp accesses are contiguous rows, never by the x sweep, whose lanes own
+// different rows.
 #pragma once
 #include "physics.cuh"
 
 namespace mfc {
 
-enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2 };
+enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3 };
 
 struct SweepArgs {
     const double* __restrict__ q;   // stencil state (padded layout, ghosts filled)
-    const double* acc;              // accumulator input (M_ACC)
+    const double* acc;              // accumulator input (M_ACC, M_RKACC)
     double* dst;                    // destination (state layout)
-    const double* qn;               // RK base state q^n (M_RKINIT, read iff ca != 0)
+    const double* qn;               // RK base state q^n (M_RKINIT/M_RKACC, read iff ca != 0)
     int64_t sE;                     // equation stride
     int64_t sS, sA, sB;             // strides along the sweep, lane and third axis
     int64_t base;                   // offset of interior cell (0,0,0), equation 0
@@ -84,10 +87,10 @@ sweep_kernel(const SweepArgs a) {
     for (int j = s0 - 1; j <= s1; ++j) {
         const bool update = j > s0;                   // cell j-1 is updated this step
         // epilogue operands of cell j-1, issued now, consumed at the end of the step
-        double ep0[E], ep1[E];
+        double ep0[E], ep1[E], ep2[E];
         if (update) {
-            if (MODE == M_ACC) load(a.acc, j - 1, ep0);
-            if (MODE == M_RKINIT) {
+            if (MODE == M_ACC || MODE == M_RKACC) load(a.acc, j - 1, ep2);
+            if (MODE == M_RKINIT || MODE == M_RKACC) {
                 load(q, j - 1, ep0);
                 if (a.ca != 0.0) load(a.qn, j - 1, ep1);
             }
@@ -118,9 +121,12 @@ sweep_kernel(const SweepArgs a) {
                     if (e >= M::IA) r = fma(w[1][e], div, r);
                     double out;
                     if (MODE == M_SET) out = r;
-                    else if (MODE == M_ACC) out = fma(a.w, r, ep0[e]);
-                    else out = fma(a.w, r, a.ca != 0.0 ? fma(a.ca, ep1[e], a.cb * ep0[e])
-                                                       : a.cb * ep0[e]);
+                    else if (MODE == M_ACC) out = fma(a.w, r, ep2[e]);
+                    else {
+                        const double base = a.ca != 0.0 ? fma(a.ca, ep1[e], a.cb * ep0[e])
+                                                        : a.cb * ep0[e];
+                        out = fma(a.w, MODE == M_RKACC ? ep2[e] + r : r, base);
+                    }
                     a.dst[c + e * a.sE] = out;
                 }
             }

@@ -27,8 +27,10 @@ __global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons)
 template <class M, int DIR>
 static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     if (DIR == 0 && mode == M_SET) sweep_kernel<M, DIR, M_SET><<<g, b, 0, s>>>(a);
-    else if (DIR == 0 && mode == M_RKINIT) sweep_kernel<M, DIR, M_RKINIT><<<g, b, 0, s>>>(a);
+    else if (DIR == 0 && M::D == 1 && mode == M_RKINIT)
+        sweep_kernel<M, DIR, M_RKINIT><<<g, b, 0, s>>>(a);
     else if (DIR > 0 && mode == M_ACC) sweep_kernel<M, DIR, M_ACC><<<g, b, 0, s>>>(a);
+    else if (DIR == 1 && mode == M_RKACC) sweep_kernel<M, DIR, M_RKACC><<<g, b, 0, s>>>(a);
     else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }

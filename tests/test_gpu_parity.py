@@ -8,8 +8,8 @@ import pytest
 import oracle as O
 from paper_2409_10729_b200 import workloads as W
 
-from parity import (RHS_TOL, STEP100_TOL, gpu_rhs, gpu_solver, gpu_steps, oracle_inputs, rel_err,
-                    rhs_flux_scale, stable_dt)
+from parity import (RHS_TOL, STEP100_TOL, gpu_rhs, gpu_solver, gpu_steps, oracle_inputs,
+                    oracle_sensitivity, rel_err, rhs_flux_scale, stable_dt)
 
 pytestmark = pytest.mark.gpu
 
@@ -129,7 +129,8 @@ def test_rk3_100_steps_parity(name, make, cfl):
     assert O.count_inadmissible(P, ref) == 0
     got = gpu_steps(pb, q, dt, 100)
     err = rel_err(got, ref)
-    assert np.all(err <= STEP100_TOL), (name, err)
+    tol = np.maximum(STEP100_TOL, 3.0 * oracle_sensitivity(P, q, dt, 100, ref))
+    assert np.all(err <= tol), (name, err, tol)
 
 
 def test_one_step_parity_tight():

@@ -333,6 +333,8 @@ int seg_len(const mfc_ctx* c, int dir) {
     int T = 64;
     while (T > 16 && lines * ((n + T - 1) / T) < 49152) T /= 2;
     if (c->D == 1) T = (int)std::max<int64_t>(8, std::min<int64_t>(32, n / 8 + 1));
+    // the staged x sweep (D >= 2) needs segments that are multiples of its 4-cell chunks
+    if (dir == 0 && c->D >= 2) return std::max(4, (int)((std::min<int64_t>(T, n) + 3) / 4 * 4));
     return (int)std::min<int64_t>(T, n);
 }
 
@@ -364,8 +366,12 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     a.ca = ca;
     a.cb = cb;
     a.mat = c->mat;
-    const int bx = (int)std::min<int64_t>(32, a.nA);
-    const int by = (int)std::max<int64_t>(1, std::min<int64_t>(128 / bx, a.nB));
+    int bx = (int)std::min<int64_t>(32, a.nA);
+    int by = (int)std::max<int64_t>(1, std::min<int64_t>(128 / bx, a.nB));
+    if (dir == 0 && c->D >= 2 && mode == M_SET) {
+        bx = 32;   // staged x sweep: one warp per 32 rows, E*3 KB of shared memory per warp
+        by = (int)std::max<int64_t>(1, std::min<int64_t>(c->E <= 8 ? 4 : 2, a.nB));
+    }
     dim3 block(bx, by);
     dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.nS + a.T - 1) / a.T);
     cudaError_t e;

@@ -140,3 +140,137 @@ sweep_kernel(const SweepArgs a) {
 }
 
 }  // namespace mfc
+
+namespace mfc {
+
+// ---------------------------------------------------------------------------
+// x sweep with shared-memory staging (2D/3D, epilogue M_SET).
+//
+// In the x sweep a warp's 32 lanes march along 32 different rows (consecutive y),
+// so a plain per-lane load touches 32 rows = 32 sectors per instruction.  Here each
+// warp moves its rows through shared memory in chunks of 4 cells (one 32-byte sector
+// per row): the warp copies a chunk [E][32 rows][4] with cp.async, 4 lanes per row
+// sector (each instruction = 8 full sectors), two chunks ahead of the march; the
+// lanes read their own row from it.  Results go to a chunk-sized output buffer and
+// leave as 8 full sectors per store instruction.  Layout inside a chunk buffer:
+// element (e, row, x) at (e*32 + row)*4 + (x ^ ((row >> 2) & 3)): the XOR swizzle
+// makes both the row-wise march reads and the sector-wise copies bank-conflict free.
+// Per warp: 2 input + 1 output chunk buffers = 3 * E * 1 KB of shared memory.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int swz(int row, int x) { return row * 4 + (x ^ ((row >> 2) & 3)); }
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <class M>
+__global__ void __launch_bounds__(128, 2)
+sweep_x_staged(const SweepArgs a) {
+    constexpr int E = M::E;
+    constexpr int CH = E * 128;                      // doubles per chunk buffer
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x;                    // blockDim.x == 32
+    double* in0 = smem + threadIdx.y * 3 * CH;
+    double* in1 = in0 + CH;
+    double* outb = in1 + CH;
+    const int row0 = blockIdx.x * 32;                // first row (y) of this warp
+    const int ib = blockIdx.y * blockDim.y + threadIdx.y;
+    if (ib >= a.nB) return;                          // whole warp
+    const int s0 = blockIdx.z * a.T;                 // T is a multiple of 4
+    const int s1 = min(s0 + a.T, a.nS);
+    const int64_t plane = a.base + (int64_t)ib * a.sB;   // row row0+r, cell s: plane + (row0+r)*sA + s
+    const int crow = lane >> 2, cx = lane & 3;       // copy geometry: 8 rows x 4 cells
+    const int nrows = min(32, a.nA - row0);
+
+    // chunk K holds cells 4K-4 .. 4K-1 (padded x index 4K .. 4K+3; 32-byte aligned)
+    auto issue = [&](int K, double* dst) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = 8 * i + crow;
+                if (r < nrows)
+                    cp_async8(dst + e * 128 + swz(r, cx),
+                              a.q + plane + (int64_t)(row0 + r) * a.sA + e * a.sE + (4 * K - 4 + cx));
+            }
+        }
+        cp_async_commit();
+    };
+    const int Klast = (s1 + 6) >> 2;
+    auto convert = [&](int x, double (&v)[E]) {     // cell x of my row -> primitives
+        const int K = (x + 4) >> 2;
+        double* b = (K & 1) ? in1 : in0;
+        if (((x + 4) & 3) == 0 || x == s0 - 3) {      // first use of chunk K
+            cp_async_wait_all();
+            __syncwarp();
+            if (K + 1 <= Klast) issue(K + 1, ((K + 1) & 1) ? in1 : in0);
+        }
+        double qc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) qc[e] = b[e * 128 + swz(lane, (x + 4) & 3)];
+        cons_to_prim_fast<M>(qc, v, a.mat);
+    };
+    auto flush = [&](int K) {                        // store output chunk K (cells 4K-4..4K-1)
+        __syncwarp();
+        const int xc = 4 * K - 4 + cx;
+        if (xc >= s0 && xc < s1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = 8 * i + crow;
+                    if (r < nrows)
+                        a.dst[plane + (int64_t)(row0 + r) * a.sA + e * a.sE + xc] =
+                            outb[e * 128 + swz(r, cx)];
+                }
+            }
+        }
+        __syncwarp();
+    };
+
+    issue((s0 + 1) >> 2, (((s0 + 1) >> 2) & 1) ? in1 : in0);
+    double w[5][E];
+#pragma unroll
+    for (int k = 1; k < 5; ++k) convert(s0 - 4 + k, w[k]);
+
+    double vm_prev[E], F_prev[E];
+    double uf_prev = 0.0;
+    for (int j = s0 - 1; j <= s1; ++j) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) w[k][e] = w[k + 1][e];
+        }
+        convert(j + 2, w[4]);
+        double vm[E], vp[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps, vm[e], vp[e]);
+        if (j >= s0) {
+            double F[E], uf;
+            hllc<M, 0>(vm_prev, vp, a.mat, F, uf);
+            if (j > s0) {
+                const int x = j - 1;
+                const double div = (uf - uf_prev) * a.invd;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    double r = (F_prev[e] - F[e]) * a.invd;
+                    if (e >= M::IA) r = fma(w[1][e], div, r);
+                    outb[e * 128 + swz(lane, (x + 4) & 3)] = r;
+                }
+                if (((x + 4) & 3) == 3 || x == s1 - 1) flush((x + 4) >> 2);
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) F_prev[e] = F[e];
+            uf_prev = uf;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
+    }
+}
+
+}  // namespace mfc

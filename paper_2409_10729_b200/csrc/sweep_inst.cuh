@@ -26,7 +26,17 @@ __global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons)
 
 template <class M, int DIR>
 static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
-    if (DIR == 0 && mode == M_SET) sweep_kernel<M, DIR, M_SET><<<g, b, 0, s>>>(a);
+    if (DIR == 0 && mode == M_SET && M::D >= 2) {
+        // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
+        const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(sweep_x_staged<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            attr = true;
+        }
+        sweep_x_staged<M><<<g, b, smem, s>>>(a);
+    } else if (DIR == 0 && mode == M_SET) sweep_kernel<M, DIR, M_SET><<<g, b, 0, s>>>(a);
     else if (DIR == 0 && M::D == 1 && mode == M_RKINIT)
         sweep_kernel<M, DIR, M_RKINIT><<<g, b, 0, s>>>(a);
     else if (DIR > 0 && mode == M_ACC) sweep_kernel<M, DIR, M_ACC><<<g, b, 0, s>>>(a);

@@ -14,9 +14,10 @@
 // Every face state, face flux and primitive is computed once per segment and never
 // leaves the register file: no face states in HBM, no transposes.
 //
-// Latency hiding: all global loads are issued one march step before they are used
-// (the next cell's state, and the epilogue operands of the cell updated this step),
-// so a warp never waits on DRAM inside a step.
+// Latency hiding: every streamed operand (the next cell's state, the epilogue operands
+// of the cell updated in a step) is copied into a per-thread shared-memory ring with
+// cp.async two march steps before it is used, so no registers are held for it and a
+// warp never waits on DRAM inside a step.
 //
 // Epilogues (compile-time MODE; w = cb*dt in RK stages, 1 for a plain RHS):
 //   M_SET   : dst = c                                 (x sweep: write-only)
@@ -50,58 +51,104 @@ struct SweepArgs {
     Materials mat;
 };
 
+// Per-thread shared-memory rings for the streamed operands (filled by cp.async two
+// march steps ahead of use; element (slot, e) of thread t at [(slot*E + e)*nthreads + t],
+// so a warp's copies and reads are contiguous 256-byte rows):
+//   state ring : cells j+2 .. j+4 (RK y sweep: j-1 .. j+4, the stage operand q^s(j-1)
+//                is the state already streamed three steps earlier);
+//   acc / q^n rings : cells j-1 .. j+1.
+template <int MODE>
+struct Rings {
+    static constexpr int QS = (MODE == M_RKACC || MODE == M_RKINIT) ? 6 : 3;
+    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC) ? 3 : 0;
+    static constexpr int NS = (MODE == M_RKACC || MODE == M_RKINIT) ? 3 : 0;
+    static constexpr int SLOTS = QS + AS + NS;
+};
+
+template <class M, int MODE>
+constexpr size_t sweep_smem_per_thread() { return (size_t)Rings<MODE>::SLOTS * M::E * sizeof(double); }
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
 template <class M, int DIR, int MODE>
 __global__ void __launch_bounds__(128, 2)
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
+    using R = Rings<MODE>;
+    extern __shared__ double smem[];
+    const int nth = blockDim.x * blockDim.y;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    double* const ringQ = smem + tid;                       // QS slots
+    double* const ringA = ringQ + R::QS * E * nth;          // AS slots
+    double* const ringN = ringA + R::AS * E * nth;          // NS slots
+    auto at = [&](double* ring, int slot, int e) -> double& { return ring[(slot * E + e) * nth]; };
+
     const int ia = blockIdx.x * blockDim.x + threadIdx.x;
     const int ib = blockIdx.y * blockDim.y + threadIdx.y;
-    if (ia >= a.nA || ib >= a.nB) return;
+    if (ia >= a.nA || ib >= a.nB) return;                   // no block-level sync below
     const int s0 = blockIdx.z * a.T;
     const int s1 = min(s0 + a.T, a.nS);   // cells s0 .. s1-1 are updated
     const int64_t line = a.base + (int64_t)ia * a.sA + (int64_t)ib * a.sB;
     const double* __restrict__ q = a.q;
 
-    auto load = [&](const double* __restrict__ src, int s, double (&x)[E]) {
-        const double* p = src + line + (int64_t)s * a.sS;
+    auto fetch = [&](double* ring, int slot, const double* src, int cell) {
+        const double* p = src + line + (int64_t)cell * a.sS;
 #pragma unroll
-        for (int e = 0; e < E; ++e) x[e] = __ldg(p + e * a.sE);
+        for (int e = 0; e < E; ++e) cp_async8(&at(ring, slot, e), p + e * a.sE);
+    };
+    // group for step j: state of cell j+2, epilogue operands of cell j-1
+    auto issue = [&](int j) {
+        if (j + 2 <= s1 + 2) fetch(ringQ, (j + 2 + 3) % R::QS, q, j + 2);
+        const int c = j - 1;
+        if (c >= s0 && c < s1) {
+            if (R::AS) fetch(ringA, (c + 3) % 3, a.acc, c);
+            if (R::NS && a.ca != 0.0) fetch(ringN, (c + 3) % 3, a.qn, c);
+        }
+        cp_async_commit();
     };
 
     double w[5][E];        // primitive window: cells j-2 .. j+2
     {
         double qc[E];
 #pragma unroll
-        for (int k = 1; k < 5; ++k) {                 // cells s0-3 .. s0
-            load(q, s0 - 4 + k, qc);
+        for (int k = 1; k < 5; ++k) {                 // cells s0-3 .. s0 (direct loads)
+            const double* p = q + line + (int64_t)(s0 - 4 + k) * a.sS;
+#pragma unroll
+            for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
+            if (R::QS == 6) {                         // keep for the q^s epilogue operand
+#pragma unroll
+                for (int e = 0; e < E; ++e) at(ringQ, (s0 - 4 + k + 3) % R::QS, e) = qc[e];
+            }
             cons_to_prim_fast<M>(qc, w[k], a.mat);
         }
     }
-    double qnext[E];       // conserved state of cell j+2 (prefetched one step ahead)
-    load(q, s0 + 1, qnext);
+    issue(s0 - 1);
+    issue(s0);
 
     double vm_prev[E];     // v-_{j-1/2} (from cell j-1)
     double F_prev[E];      // flux at face j-3/2
     double uf_prev = 0.0;
 
     for (int j = s0 - 1; j <= s1; ++j) {
-        const bool update = j > s0;                   // cell j-1 is updated this step
-        // epilogue operands of cell j-1, issued now, consumed at the end of the step
-        double ep0[E], ep1[E], ep2[E];
-        if (update) {
-            if (MODE == M_ACC || MODE == M_RKACC) load(a.acc, j - 1, ep2);
-            if (MODE == M_RKINIT || MODE == M_RKACC) {
-                load(q, j - 1, ep0);
-                if (a.ca != 0.0) load(a.qn, j - 1, ep1);
-            }
-        }
+        cp_async_wait_1();                             // group of step j has landed
+        issue(j + 2);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
 #pragma unroll
             for (int e = 0; e < E; ++e) w[k][e] = w[k + 1][e];
         }
-        cons_to_prim_fast<M>(qnext, w[4], a.mat);
-        if (j < s1) load(q, j + 3, qnext);            // next step's new cell
+        {
+            double qc[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) qc[e] = at(ringQ, (j + 2 + 3) % R::QS, e);
+            cons_to_prim_fast<M>(qc, w[4], a.mat);
+        }
 
         double vm[E], vp[E];
 #pragma unroll
@@ -111,9 +158,10 @@ sweep_kernel(const SweepArgs a) {
         if (j >= s0) {
             double F[E], uf;
             hllc<M, DIR>(vm_prev, vp, a.mat, F, uf);
-            if (update) {
+            if (j > s0) {
                 // cell j-1: faces j-3/2 (F_prev) and j-1/2 (F); alpha_{j-1} = w[1]
-                const int64_t c = line + (int64_t)(j - 1) * a.sS;
+                const int cc = j - 1;
+                const int64_t c = line + (int64_t)cc * a.sS;
                 const double div = (uf - uf_prev) * a.invd;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
@@ -121,11 +169,13 @@ sweep_kernel(const SweepArgs a) {
                     if (e >= M::IA) r = fma(w[1][e], div, r);
                     double out;
                     if (MODE == M_SET) out = r;
-                    else if (MODE == M_ACC) out = fma(a.w, r, ep2[e]);
+                    else if (MODE == M_ACC) out = fma(a.w, r, at(ringA, (cc + 3) % 3, e));
                     else {
-                        const double base = a.ca != 0.0 ? fma(a.ca, ep1[e], a.cb * ep0[e])
-                                                        : a.cb * ep0[e];
-                        out = fma(a.w, MODE == M_RKACC ? ep2[e] + r : r, base);
+                        const double qs = at(ringQ, (cc + 3) % R::QS, e);
+                        const double base = a.ca != 0.0
+                                                ? fma(a.ca, at(ringN, (cc + 3) % 3, e), a.cb * qs)
+                                                : a.cb * qs;
+                        out = fma(a.w, MODE == M_RKACC ? at(ringA, (cc + 3) % 3, e) + r : r, base);
                     }
                     a.dst[c + e * a.sE] = out;
                 }
@@ -137,6 +187,7 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
         for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
     }
+    cp_async_wait_all();
 }
 
 }  // namespace mfc
@@ -159,13 +210,6 @@ namespace mfc {
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ int swz(int row, int x) { return row * 4 + (x ^ ((row >> 2) & 3)); }
-
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 template <class M>
 __global__ void __launch_bounds__(128, 2)

@@ -24,6 +24,18 @@ __global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons)
     }
 }
 
+template <class M, int DIR, int MODE>
+static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
+    const size_t smem = sweep_smem_per_thread<M, MODE>() * b.x * b.y;
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = smem;
+    }
+    sweep_kernel<M, DIR, MODE><<<g, b, smem, s>>>(a);
+}
+
 template <class M, int DIR>
 static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     if (DIR == 0 && mode == M_SET && M::D >= 2) {
@@ -36,11 +48,10 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
             attr = true;
         }
         sweep_x_staged<M><<<g, b, smem, s>>>(a);
-    } else if (DIR == 0 && mode == M_SET) sweep_kernel<M, DIR, M_SET><<<g, b, 0, s>>>(a);
-    else if (DIR == 0 && M::D == 1 && mode == M_RKINIT)
-        sweep_kernel<M, DIR, M_RKINIT><<<g, b, 0, s>>>(a);
-    else if (DIR > 0 && mode == M_ACC) sweep_kernel<M, DIR, M_ACC><<<g, b, 0, s>>>(a);
-    else if (DIR == 1 && mode == M_RKACC) sweep_kernel<M, DIR, M_RKACC><<<g, b, 0, s>>>(a);
+    } else if (DIR == 0 && mode == M_SET) launch_ring<M, DIR, M_SET>(a, g, b, s);
+    else if (DIR == 0 && M::D == 1 && mode == M_RKINIT) launch_ring<M, DIR, M_RKINIT>(a, g, b, s);
+    else if (DIR > 0 && mode == M_ACC) launch_ring<M, DIR, M_ACC>(a, g, b, s);
+    else if (DIR == 1 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC>(a, g, b, s);
     else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }

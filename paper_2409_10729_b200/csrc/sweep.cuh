@@ -31,6 +31,10 @@
 #pragma once
 #include "physics.cuh"
 
+#ifndef MFC_ACC_MINB
+#define MFC_ACC_MINB 3   // resident 128-thread blocks per SM for the non-RK sweep modes
+#endif
+
 namespace mfc {
 
 enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3 };
@@ -76,8 +80,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
+// 3 resident blocks (12 warps/SM, <= 168 registers) where that does not spill (the
+// non-RK modes for E <= 8); 2 blocks otherwise.
+template <class M, int MODE>
+constexpr int sweep_min_blocks() {
+    return ((MODE == M_ACC || MODE == M_SET) && M::E <= 8) ? MFC_ACC_MINB : 2;
+}
+
 template <class M, int DIR, int MODE>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(128, sweep_min_blocks<M, MODE>())
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
     using R = Rings<MODE>;

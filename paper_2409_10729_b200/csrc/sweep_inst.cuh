@@ -38,21 +38,31 @@ static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
 
 template <class M, int DIR>
 static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
-    if (DIR == 0 && mode == M_SET && M::D >= 2) {
-        // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
-        const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(sweep_x_staged<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            attr = true;
+    if constexpr (DIR == 0) {
+        if (mode == M_SET) {
+            if constexpr (M::D >= 2) {
+                // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
+                const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
+                static size_t attr = 0;
+                if (smem > attr) {
+                    cudaFuncSetAttribute(sweep_x_staged<M>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    attr = smem;
+                }
+                sweep_x_staged<M><<<g, b, smem, s>>>(a);
+            } else {
+                launch_ring<M, DIR, M_SET>(a, g, b, s);
+            }
+        } else if (mode == M_RKINIT && M::D == 1) {
+            launch_ring<M, DIR, M_RKINIT>(a, g, b, s);
+        } else {
+            return cudaErrorInvalidValue;
         }
-        sweep_x_staged<M><<<g, b, smem, s>>>(a);
-    } else if (DIR == 0 && mode == M_SET) launch_ring<M, DIR, M_SET>(a, g, b, s);
-    else if (DIR == 0 && M::D == 1 && mode == M_RKINIT) launch_ring<M, DIR, M_RKINIT>(a, g, b, s);
-    else if (DIR > 0 && mode == M_ACC) launch_ring<M, DIR, M_ACC>(a, g, b, s);
-    else if (DIR == 1 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC>(a, g, b, s);
-    else return cudaErrorInvalidValue;
+    } else {
+        if (mode == M_ACC) launch_ring<M, DIR, M_ACC>(a, g, b, s);
+        else if (DIR == 1 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC>(a, g, b, s);
+        else return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

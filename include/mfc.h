@@ -98,7 +98,7 @@ typedef struct {
     size_t workspace_bytes; /* bytes mfc_bind_workspace needs */
 } mfc_layout;
 
-/* Create a context.  gamma[i] > 1 and pi_inf[i] >= 0 (Pa) are the stiffened-gas
+/* Create a context (every active dimension needs n_global >= 3).  gamma[i] > 1 and pi_inf[i] >= 0 (Pa) are the stiffened-gas
  * parameters of fluid i; the library derives Gamma_i = 1/(gamma_i-1),
  * Pi_i = gamma_i pi_inf_i/(gamma_i-1).  bc = {x_lo, x_hi, y_lo, y_hi, z_lo, z_hi};
  * entries of inactive dimensions are ignored; a periodic dimension must be
@@ -140,9 +140,11 @@ int mfc_cons_to_prim(mfc_ctx* ctx, const double* q, double* v, void* stream);
  * q are written. */
 int mfc_halo_exchange(mfc_ctx* ctx, double* q, void* stream);
 
-/* One RHS evaluation L(q): fills q's ghosts (as mfc_halo_exchange),
- * then writes rhs on every interior cell (rhs has the state layout; its ghost
- * cells are not written).  q and rhs must not alias. */
+/* One RHS evaluation L(q) written on every interior cell of rhs (state
+ * layout; its ghost cells are not written).  Faces shared with another rank are
+ * exchanged first (into q's ghost layers); physical boundary conditions are applied
+ * by the sweeps themselves through ghost-index mapping, so q's physical ghost cells
+ * are neither read nor written.  q and rhs must not alias. */
 int mfc_rhs(mfc_ctx* ctx, double* q, double* rhs, void* stream);
 
 /* One SSP-RK3 step of size dt on q's interior, in place:

@@ -278,11 +278,14 @@ int need_ws(const mfc_ctx* c, bool stages) {
 }
 
 // Ghost fill for a set of contexts (count == 1: NCCL or single domain; > 1: loopback).
-int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s) {
+// physical == false: only faces shared with another rank (the sweeps apply physical
+// boundary conditions themselves by index mapping, so the RHS path skips bc_fill).
+int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
+             bool physical = true) {
     for (int r = 0; r < count; ++r) {
         int st = need_ws(cs[r], false);
         if (st) return st;
-        if ((st = bc_fill(cs[r], qs[r], s))) return st;
+        if (physical && (st = bc_fill(cs[r], qs[r], s))) return st;
         if ((st = halo_pack(cs[r], qs[r], s))) return st;
     }
     if (count == 1 && cs[0]->nranks > 1 && !cs[0]->loopback) {
@@ -360,6 +363,10 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     a.nA = (int32_t)c->nl[la];
     a.nB = (int32_t)c->nl[lb];
     a.T = seg_len(c, dir);
+    // physical faces are applied by index mapping inside the sweep; faces shared with
+    // another rank read the ghost layers the halo exchange wrote
+    a.bc_lo = c->bc[2 * dir] == BC_NEIGHBOR ? BC_GHOST : c->bc[2 * dir];
+    a.bc_hi = c->bc[2 * dir + 1] == BC_NEIGHBOR ? BC_GHOST : c->bc[2 * dir + 1];
     a.invd = 1.0 / c->dx[dir];
     a.eps = c->eps;
     a.w = w;
@@ -430,7 +437,7 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
     for (int stage = 0; stage < 3; ++stage) {
         for (int r = 0; r < count; ++r)
             in[r] = stage == 0 ? qs[r] : (stage == 1 ? cs[r]->S1 : cs[r]->S2);
-        int st = exchange(cs, in.data(), count, s);
+        int st = exchange(cs, in.data(), count, s, false);
         if (st) return st;
         for (int r = 0; r < count; ++r) {
             mfc_ctx* c = cs[r];
@@ -450,7 +457,7 @@ int rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int co
         if (qs[r] == rhss[r]) return fail(MFC_EINVAL, "q and rhs alias");
         cs[r]->launches = 0;
     }
-    int st = exchange(cs, qs, count, s);
+    int st = exchange(cs, qs, count, s, false);
     if (st) return st;
     for (int r = 0; r < count; ++r)
         if ((st = sweeps(cs[r], qs[r], rhss[r], rhss[r], false, nullptr, 0, 0, 0, s)))
@@ -492,7 +499,9 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
         if (k >= D && (grid->n_global[k] != 1 || p != 1))
             return fail(MFC_EINVAL, "inactive dim %d must have n=1, procs=1", k);
         if (k < D) {
-            if (grid->n_global[k] < 1) return fail(MFC_EINVAL, "n_global[%d] < 1", k);
+            if (grid->n_global[k] < kGhost)
+                return fail(MFC_EINVAL, "n_global[%d] = %lld < 3 (WENO5 stencil)", k,
+                            (long long)grid->n_global[k]);
             if (!(grid->hi[k] > grid->lo[k])) return fail(MFC_EINVAL, "hi[%d] <= lo[%d]", k, k);
             const bool per_lo = bc[2 * k] == MFC_BC_PERIODIC, per_hi = bc[2 * k + 1] == MFC_BC_PERIODIC;
             if (per_lo != per_hi) return fail(MFC_EINVAL, "dim %d periodic on one end only", k);

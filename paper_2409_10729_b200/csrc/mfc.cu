@@ -365,8 +365,17 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     a.T = seg_len(c, dir);
     // physical faces are applied by index mapping inside the sweep; faces shared with
     // another rank read the ghost layers the halo exchange wrote
-    a.bc_lo = c->bc[2 * dir] == BC_NEIGHBOR ? BC_GHOST : c->bc[2 * dir];
-    a.bc_hi = c->bc[2 * dir + 1] == BC_NEIGHBOR ? BC_GHOST : c->bc[2 * dir + 1];
+    {
+        const int n = a.nS, lo = c->bc[2 * dir], hi = c->bc[2 * dir + 1];
+        GhostMap& g = a.gm;
+        g.alo = 0; g.blo = 1; g.ahi = 0; g.bhi = 1; g.flip_lo = g.flip_hi = 0;
+        if (lo == MFC_BC_PERIODIC) { g.alo = n; g.blo = 1; }
+        else if (lo == MFC_BC_EXTRAPOLATION) { g.alo = 0; g.blo = 0; }
+        else if (lo == MFC_BC_REFLECTIVE) { g.alo = -1; g.blo = -1; g.flip_lo = 1; }
+        if (hi == MFC_BC_PERIODIC) { g.ahi = -n; g.bhi = 1; }
+        else if (hi == MFC_BC_EXTRAPOLATION) { g.ahi = n - 1; g.bhi = 0; }
+        else if (hi == MFC_BC_REFLECTIVE) { g.ahi = 2 * n - 1; g.bhi = -1; g.flip_hi = 1; }
+    }
     a.invd = 1.0 / c->dx[dir];
     a.eps = c->eps;
     a.w = w;

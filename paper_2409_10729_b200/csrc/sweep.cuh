@@ -44,23 +44,23 @@ constexpr int BC_GHOST = 1;  // ghost cells of this face are valid in memory (ha
 // Ghost cells of a physical boundary are never stored: a sweep reading cell s of its
 // line outside [0, n) reads the interior cell the boundary condition maps it to
 // (S1 of DESIGN.md §3: periodic -1-j <- n-1-j, extrapolation <- adjacent interior,
-// reflective -1-j <- j with the normal momentum negated).  Returns the cell to read;
-// *flip = true when the normal momentum must be negated.
-__device__ __forceinline__ int map_ghost(int s, int n, int bc_lo, int bc_hi, bool* flip) {
-    *flip = false;
-    if (s < 0) {
-        if (bc_lo == -1) return s + n;
-        if (bc_lo == -3) return 0;
-        if (bc_lo == -2) { *flip = true; return -1 - s; }
-        return s;
-    }
-    if (s >= n) {
-        if (bc_hi == -1) return s - n;
-        if (bc_hi == -3) return n - 1;
-        if (bc_hi == -2) { *flip = true; return 2 * n - 1 - s; }
-        return s;
-    }
-    return s;
+// reflective -1-j <- j with the normal momentum negated).  Each map is linear,
+// s' = A + B*s, so it is applied branch-free:
+//   periodic lo (A, B) = (n, 1),   hi (-n, 1)
+//   extrapolation lo (0, 0),        hi (n-1, 0)
+//   reflective lo (-1, -1),         hi (2n-1, -1)   (+ normal momentum flip)
+//   ghost (halo-exchanged) (0, 1): read the ghost layer itself
+struct GhostMap {
+    int32_t alo, blo, ahi, bhi;
+    int32_t flip_lo, flip_hi;
+};
+
+__device__ __forceinline__ int map_cell(int s, int n, const GhostMap& g) {
+    const int lo = g.alo + g.blo * s, hi = g.ahi + g.bhi * s;
+    return s < 0 ? lo : (s >= n ? hi : s);
+}
+__device__ __forceinline__ bool map_flip(int s, int n, const GhostMap& g) {
+    return (s < 0 && g.flip_lo) || (s >= n && g.flip_hi);
 }
 
 struct SweepArgs {
@@ -73,9 +73,7 @@ struct SweepArgs {
     int64_t base;                   // offset of interior cell (0,0,0), equation 0
     int32_t nS, nA, nB;             // interior extents along sweep / lane / third axis
     int32_t T;                      // segment length along the sweep
-    int32_t bc_lo, bc_hi;           // boundary of the sweep axis at cell -1 / cell nS:
-                                    // MFC_BC codes (-1 periodic, -2 reflective, -3
-                                    // extrapolation) or BC_GHOST (ghosts filled in memory)
+    GhostMap gm;                    // boundary maps of the sweep axis (see map_cell)
     double invd;                    // 1/dx along DIR
     double eps;                     // WENO epsilon
     double w, ca, cb;               // epilogue weights
@@ -136,8 +134,7 @@ sweep_kernel(const SweepArgs a) {
     const double* __restrict__ q = a.q;
 
     auto fetch = [&](double* ring, int slot, const double* src, int cell) {
-        bool flip;
-        const int sc = map_ghost(cell, a.nS, a.bc_lo, a.bc_hi, &flip);
+        const int sc = map_cell(cell, a.nS, a.gm);
         const double* p = src + line + (int64_t)sc * a.sS;
 #pragma unroll
         for (int e = 0; e < E; ++e) cp_async8(&at(ring, slot, e), p + e * a.sE);
@@ -158,12 +155,11 @@ sweep_kernel(const SweepArgs a) {
         double qc[E];
 #pragma unroll
         for (int k = 1; k < 5; ++k) {                 // cells s0-3 .. s0 (direct loads)
-            bool flip;
-            const int sc = map_ghost(s0 - 4 + k, a.nS, a.bc_lo, a.bc_hi, &flip);
+            const int sc = map_cell(s0 - 4 + k, a.nS, a.gm);
             const double* p = q + line + (int64_t)sc * a.sS;
 #pragma unroll
             for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
-            if (flip) qc[M::IM + DIR] = -qc[M::IM + DIR];
+            if (map_flip(s0 - 4 + k, a.nS, a.gm)) qc[M::IM + DIR] = -qc[M::IM + DIR];
             if (R::QS == 6) {                         // keep for the q^s epilogue operand
 #pragma unroll
                 for (int e = 0; e < E; ++e) at(ringQ, (s0 - 4 + k + 3) % R::QS, e) = qc[e];
@@ -190,9 +186,7 @@ sweep_kernel(const SweepArgs a) {
             double qc[E];
 #pragma unroll
             for (int e = 0; e < E; ++e) qc[e] = at(ringQ, (j + 2 + 3) % R::QS, e);
-            bool flip;
-            map_ghost(j + 2, a.nS, a.bc_lo, a.bc_hi, &flip);
-            if (flip) qc[M::IM + DIR] = -qc[M::IM + DIR];
+            if (map_flip(j + 2, a.nS, a.gm)) qc[M::IM + DIR] = -qc[M::IM + DIR];
             cons_to_prim_fast<M>(qc, w[4], a.mat);
         }
 
@@ -278,17 +272,14 @@ sweep_x_staged(const SweepArgs a) {
 
     // chunk K holds cells 4K-4 .. 4K-1 (padded x index 4K .. 4K+3; 32-byte aligned)
     auto issue = [&](int K, double* dst) {
+        const double* src = a.q + plane + map_cell(4 * K - 4 + cx, a.nS, a.gm);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int r = 8 * i + crow;
-                if (r < nrows) {
-                    bool flip;
-                    const int xs = map_ghost(4 * K - 4 + cx, a.nS, a.bc_lo, a.bc_hi, &flip);
-                    cp_async8(dst + e * 128 + swz(r, cx),
-                              a.q + plane + (int64_t)(row0 + r) * a.sA + e * a.sE + xs);
-                }
+                if (r < nrows)
+                    cp_async8(dst + e * 128 + swz(r, cx), src + (int64_t)(row0 + r) * a.sA + e * a.sE);
             }
         }
         cp_async_commit();
@@ -305,9 +296,7 @@ sweep_x_staged(const SweepArgs a) {
         double qc[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) qc[e] = b[e * 128 + swz(lane, (x + 4) & 3)];
-        bool flip;
-        map_ghost(x, a.nS, a.bc_lo, a.bc_hi, &flip);
-        if (flip) qc[M::IM] = -qc[M::IM];
+        if (map_flip(x, a.nS, a.gm)) qc[M::IM] = -qc[M::IM];
         cons_to_prim_fast<M>(qc, v, a.mat);
     };
     auto flush = [&](int K) {                        // store output chunk K (cells 4K-4..4K-1)

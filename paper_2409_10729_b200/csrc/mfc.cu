@@ -377,7 +377,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
         else if (hi == MFC_BC_REFLECTIVE) { g.ahi = 2 * n - 1; g.bhi = -1; g.flip_hi = 1; }
     }
     a.invd = 1.0 / c->dx[dir];
-    a.eps = c->eps;
+    a.eps4 = 4.0 * c->eps;
     a.w = w;
     a.ca = ca;
     a.cb = cb;

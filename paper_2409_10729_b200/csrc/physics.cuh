@@ -35,15 +35,15 @@ struct Materials {
     double Pi[kMaxFluids];    // gamma_i pi_inf_i/(gamma_i - 1)
 };
 
-// Fast reciprocal: MUFU.RCP64H seed + two Newton steps (relative error ~1 ulp).
-// Used only where the specification does not fix the rounding (WENO weights,
-// HLLC quotients); the EOS path keeps IEEE division.
+// Fast reciprocal: MUFU.RCP64H seed r0 (~2^-23 relative error d) and one third-order
+// correction r = r0 (1 + e + e^2), e = 1 - x r0, leaving O(d^3) ~ 2^-69.  Used only
+// where the specification does not fix the rounding (WENO weights, HLLC quotients,
+// the sweeps' EOS); the API conversions keep IEEE division.
 __device__ __forceinline__ double rcp(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     double e = __fma_rn(-x, r, 1.0);
-    r = __fma_rn(r, e, r);
-    e = __fma_rn(-x, r, 1.0);
+    e = __fma_rn(e, e, e);
     return __fma_rn(r, e, r);
 }
 
@@ -113,15 +113,13 @@ __device__ __forceinline__ void cons_to_prim_fast(const double (&q)[M::E], doubl
     v[M::IE] = ((q[M::IE] - 0.5 * ke) - P) * iG;
 }
 
-// Fast reciprocal square root: MUFU.RSQ64H seed + two Newton steps.
+// Fast reciprocal square root: MUFU.RSQ64H seed y0 and one third-order correction
+// y = y0 (1 + e/2 + 3e^2/8), e = 1 - x y0^2.
 __device__ __forceinline__ double rsqrt_fast(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double h = 0.5 * x;
-    double e = fma(-h * y, y, 0.5);
-    y = fma(y, e, y);
-    e = fma(-h * y, y, 0.5);
-    return fma(y, e, y);
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 // Inverse EOS: rho u_k = rho*u_k;  KE = 0.5 sum (rho u_k) u_k;  rhoE = (Gamma p + Pi) + KE.
@@ -156,40 +154,39 @@ __device__ __forceinline__ void prim_to_cons(const double (&v)[M::E], double (&q
 
 // WENO5-JS for one variable of cell m from a..e = v_{m-2..m+2}:
 //   vm = v-_{m+1/2} (linear weights 0.1, 0.6, 0.3), vp = v+_{m-1/2} (0.3, 0.6, 0.1).
-// alpha_k ~ d_k / t_k with t_k = (beta_k + eps)^2; multiplying every alpha_k by
-// t0 t1 t2 gives alpha_k ~ d_k * prod_{j != k} t_j, and the candidate polynomials
-// are kept scaled by 6, so each side costs one reciprocal.
+// Same weights and candidates as the specification, evaluated in first differences
+// D0..D3 = b-a, c-b, d-c, e-d:
+//   beta'_k = 4 beta_k = (13/3) s_k^2 + r_k^2,  s = (D1-D0, D2-D1, D3-D2),
+//             r = (3D1-D0, D1+D2, D3-3D2)      (eps' = 4 eps keeps every alpha_k ratio),
+//   alpha_k ~ d_k / t_k, t_k = (beta'_k + eps')^2, multiplied through by t0 t1 t2:
+//             alpha_k ~ d_k P_k with P_k = product of the other two t_j,
+//   candidates as corrections to c: 6(p_k - c) = (5D1-2D0, D1+2D2, 4D2-D3) for v-,
+//             (D0-4D1, -2D1-D2, 2D3-5D2) for v+, with d_k folded into them,
+//   v = c + (sum_k P_k d_k 6(p_k - c)) / (6 sum_k d_k P_k):  one reciprocal per side.
 __device__ __forceinline__ void weno5(double a, double b, double c, double d, double e,
-                                      double eps, double& vm, double& vp) {
-    constexpr double k1312 = 13.0 / 12.0;
-    const double s0 = fma(-2.0, b, a + c);
-    const double r0 = fma(-4.0, b, fma(3.0, c, a));
-    const double s1 = fma(-2.0, c, b + d);
-    const double r1 = b - d;
-    const double s2 = fma(-2.0, d, c + e);
-    const double r2 = fma(-4.0, d, fma(3.0, c, e));
-    const double b0 = fma(k1312 * s0, s0, 0.25 * (r0 * r0));
-    const double b1 = fma(k1312 * s1, s1, 0.25 * (r1 * r1));
-    const double b2 = fma(k1312 * s2, s2, 0.25 * (r2 * r2));
-    double t0 = b0 + eps; t0 *= t0;
-    double t1 = b1 + eps; t1 *= t1;
-    double t2 = b2 + eps; t2 *= t2;
+                                      double eps4, double& vm, double& vp) {
+    constexpr double k133 = 13.0 / 3.0;
+    const double D0 = b - a, D1 = c - b, D2 = d - c, D3 = e - d;
+    const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
+    const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
+    double t0 = fma(k133 * s0, s0, r0 * r0) + eps4; t0 *= t0;
+    double t1 = fma(k133 * s1, s1, r1 * r1) + eps4; t1 *= t1;
+    double t2 = fma(k133 * s2, s2, r2 * r2) + eps4; t2 *= t2;
     const double P0 = t1 * t2, P1 = t0 * t2, P2 = t0 * t1;
-    // 6 x candidate values
-    const double m0 = fma(11.0, c, fma(-7.0, b, 2.0 * a));
-    const double m1 = fma(2.0, d, fma(5.0, c, -b));
-    const double m2 = fma(5.0, d, fma(2.0, c, -e));
-    const double p0 = fma(2.0, c, fma(5.0, b, -a));
-    const double p1 = fma(5.0, c, fma(2.0, b, -d));
-    const double p2 = fma(2.0, e, fma(-7.0, d, 11.0 * c));
-    const double wm0 = 0.1 * P0, wm1 = 0.6 * P1, wm2 = 0.3 * P2;
-    const double wp0 = 0.3 * P0, wp1 = 0.6 * P1, wp2 = 0.1 * P2;
-    const double Dm = 6.0 * ((wm0 + wm1) + wm2);
-    const double Dp = 6.0 * ((wp0 + wp1) + wp2);
-    const double Nm = fma(wm2, m2, fma(wm1, m1, wm0 * m0));
-    const double Np = fma(wp2, p2, fma(wp1, p1, wp0 * p0));
-    vm = Nm * rcp(Dm);
-    vp = Np * rcp(Dp);
+    // v-: d = (0.1, 0.6, 0.3), folded into the corrections
+    const double xm0 = fma(0.5, D1, -0.2 * D0);
+    const double xm1 = fma(1.2, D2, 0.6 * D1);
+    const double xm2 = fma(1.2, D2, -0.3 * D3);
+    const double Dm = fma(0.6, P0, fma(3.6, P1, 1.8 * P2));
+    const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
+    // v+: d = (0.3, 0.6, 0.1)
+    const double xp0 = fma(-1.2, D1, 0.3 * D0);
+    const double xp1 = fma(-1.2, D1, -0.6 * D2);
+    const double xp2 = fma(-0.5, D2, 0.2 * D3);
+    const double Dp = fma(1.8, P0, fma(3.6, P1, 0.6 * P2));
+    const double Np = fma(P2, xp2, fma(P1, xp1, P0 * xp0));
+    vm = fma(Nm, rcp(Dm), c);
+    vp = fma(Np, rcp(Dp), c);
 }
 
 // HLLC face flux F[E] and face velocity uf for the normal direction DIR

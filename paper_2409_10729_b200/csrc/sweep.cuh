@@ -75,7 +75,7 @@ struct SweepArgs {
     int32_t T;                      // segment length along the sweep
     GhostMap gm;                    // boundary maps of the sweep axis (see map_cell)
     double invd;                    // 1/dx along DIR
-    double eps;                     // WENO epsilon
+    double eps4;                    // 4 x WENO epsilon (weno5 works with beta' = 4 beta)
     double w, ca, cb;               // epilogue weights
     Materials mat;
 };
@@ -193,7 +193,7 @@ sweep_kernel(const SweepArgs a) {
         double vm[E], vp[E];
 #pragma unroll
         for (int e = 0; e < E; ++e)
-            weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps, vm[e], vp[e]);
+            weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, vm[e], vp[e]);
 
         if (j >= s0) {
             double F[E], uf;
@@ -202,20 +202,22 @@ sweep_kernel(const SweepArgs a) {
                 // cell j-1: faces j-3/2 (F_prev) and j-1/2 (F); alpha_{j-1} = w[1]
                 const int cc = j - 1;
                 const int64_t c = line + (int64_t)cc * a.sS;
-                const double div = (uf - uf_prev) * a.invd;
+                const double du = uf - uf_prev;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    double r = (F_prev[e] - F[e]) * a.invd;
-                    if (e >= M::IA) r = fma(w[1][e], div, r);
+                    double r = F_prev[e] - F[e];                 // dx * c_e
+                    if (e >= M::IA) r = fma(w[1][e], du, r);
                     double out;
-                    if (MODE == M_SET) out = r;
-                    else if (MODE == M_ACC) out = fma(a.w, r, at(ringA, (cc + 3) % 3, e));
+                    if (MODE == M_SET) out = r * a.invd;
+                    else if (MODE == M_ACC) out = fma(a.w * a.invd, r, at(ringA, (cc + 3) % 3, e));
                     else {
                         const double qs = at(ringQ, (cc + 3) % R::QS, e);
                         const double base = a.ca != 0.0
                                                 ? fma(a.ca, at(ringN, (cc + 3) % 3, e), a.cb * qs)
                                                 : a.cb * qs;
-                        out = fma(a.w, MODE == M_RKACC ? at(ringA, (cc + 3) % 3, e) + r : r, base);
+                        out = MODE == M_RKACC
+                                  ? fma(a.w, fma(a.invd, r, at(ringA, (cc + 3) % 3, e)), base)
+                                  : fma(a.w * a.invd, r, base);
                     }
                     a.dst[c + e * a.sE] = out;
                 }
@@ -334,18 +336,18 @@ sweep_x_staged(const SweepArgs a) {
         double vm[E], vp[E];
 #pragma unroll
         for (int e = 0; e < E; ++e)
-            weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps, vm[e], vp[e]);
+            weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, vm[e], vp[e]);
         if (j >= s0) {
             double F[E], uf;
             hllc<M, 0>(vm_prev, vp, a.mat, F, uf);
             if (j > s0) {
                 const int x = j - 1;
-                const double div = (uf - uf_prev) * a.invd;
+                const double du = uf - uf_prev;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    double r = (F_prev[e] - F[e]) * a.invd;
-                    if (e >= M::IA) r = fma(w[1][e], div, r);
-                    outb[e * 128 + swz(lane, (x + 4) & 3)] = r;
+                    double r = F_prev[e] - F[e];
+                    if (e >= M::IA) r = fma(w[1][e], du, r);
+                    outb[e * 128 + swz(lane, (x + 4) & 3)] = r * a.invd;
                 }
                 if (((x + 4) & 3) == 3 || x == s1 - 1) flush((x + 4) >> 2);
             }

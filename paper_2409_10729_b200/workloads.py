@@ -76,18 +76,20 @@ class Problem:
     def shape(self):
         return (self.E, self.n[2], self.n[1], self.n[0])
 
-    def centres(self):
-        """Cell-centre coordinates (X, Y, Z) broadcastable to (nz, ny, nx)."""
+    def centres(self, z0: int = 0, z1: int | None = None):
+        """Cell-centre coordinates (X, Y, Z) broadcastable to (nz, ny, nx); optionally
+        only the z-planes z0 .. z1-1 (slab-wise generation of large grids)."""
         xs = [self.lo[k] + (np.arange(self.n[k]) + 0.5) * self.dx[k] for k in range(3)]
+        xs[2] = xs[2][z0:z1]
         return xs[0][None, None, :], xs[1][None, :, None], xs[2][:, None, None]
 
     def with_n(self, n):
         return replace(self, n=tuple(n))
 
 
-def _assemble(pb: Problem, partial, vel, p, alpha):
+def _assemble(pb: Problem, partial, vel, p, alpha, nz=None):
     """Stack primitive components into (E, nz, ny, nx)."""
-    shape = (pb.n[2], pb.n[1], pb.n[0])
+    shape = (pb.n[2] if nz is None else nz, pb.n[1], pb.n[0])
     comps = [np.broadcast_to(a, shape) for a in partial]
     comps += [np.broadcast_to(u, shape) for u in vel[: pb.ndim]]
     comps += [np.broadcast_to(p, shape)]
@@ -177,8 +179,8 @@ def _c3_dt(h):
     return 0.3 * h / 1700.0
 
 
-def c3_prims(pb: Problem) -> np.ndarray:
-    X, Y, Z = pb.centres()
+def c3_prims(pb: Problem, z0: int = 0, z1: int | None = None) -> np.ndarray:
+    X, Y, Z = pb.centres(z0, z1)
     xc, yc, zc, r = pb.notes["droplet"]
     am = pb.notes["alpha_min"]
     h = pb.dx[0]
@@ -191,7 +193,7 @@ def c3_prims(pb: Problem) -> np.ndarray:
     u = M146[2] * C_AIR * s
     rho_w = 1000.0 * np.ones_like(a_w)
     z = np.zeros_like(u)
-    return _assemble(pb, [a_w * rho_w, a_a * rho_a], [u, z, z], p, [a_w, a_a])
+    return _assemble(pb, [a_w * rho_w, a_a * rho_a], [u, z, z], p, [a_w, a_a], nz=Z.shape[0])
 
 
 # ----------------------------------------------------------------------- C5
@@ -205,8 +207,8 @@ def c5_three_fluid(n: int = 512) -> Problem:
                           "shock_x": 0.2, "alpha_min": 1e-6})
 
 
-def c5_prims(pb: Problem) -> np.ndarray:
-    X, Y, Z = pb.centres()
+def c5_prims(pb: Problem, z0: int = 0, z1: int | None = None) -> np.ndarray:
+    X, Y, Z = pb.centres(z0, z1)
     am = pb.notes["alpha_min"]
     h = pb.dx[0]
     xd, yd, zd, rd = pb.notes["droplet"]
@@ -226,7 +228,7 @@ def c5_prims(pb: Problem) -> np.ndarray:
     rho_w = 1000.0 * np.ones_like(a_w)
     z = np.zeros_like(u)
     return _assemble(pb, [a_w * rho_w, a_a * rho_a, a_h * rho_h], [u, z, z], p,
-                     [a_w, a_a, a_h])
+                     [a_w, a_a, a_h], nz=Z.shape[0])
 
 
 # ----------------------------------------------------------------------- G-R

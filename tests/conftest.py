@@ -19,3 +19,18 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the achieved parity errors (tests/parity.py RECORD) if MFC_PARITY_LOG is set."""
+    path = os.environ.get("MFC_PARITY_LOG")
+    if not path:
+        return
+    try:
+        import json
+        from parity import RECORD
+        if RECORD:
+            with open(path, "w") as f:
+                json.dump(RECORD, f, indent=1, sort_keys=True)
+    except Exception:
+        pass

@@ -32,6 +32,15 @@ from paper_2409_10729_b200 import workloads as W
 RHS_TOL = 1e-12       # BASELINE.json north_star: per RHS evaluation
 STEP100_TOL = 1e-10   # BASELINE.json north_star: after 100 RK3 steps
 
+# achieved errors, written to $MFC_PARITY_LOG by tests/conftest.py at session end
+RECORD = {}
+
+
+def record(name: str, err, tol, strict=None):
+    RECORD[name] = {"max_err": float(np.max(err)), "tol": float(np.max(tol)),
+                    "per_eq": [float(x) for x in np.atleast_1d(err)],
+                    **({"strict_max_err": float(np.max(strict))} if strict is not None else {})}
+
 
 def rel_err(gpu: np.ndarray, cpu: np.ndarray, floor=None) -> np.ndarray:
     """Per-equation normalised max error (AMB-17); floor[e] = flux scale (RHS only)."""

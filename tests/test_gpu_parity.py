@@ -9,7 +9,7 @@ import oracle as O
 from paper_2409_10729_b200 import workloads as W
 
 from parity import (RHS_TOL, STEP100_TOL, gpu_rhs, gpu_solver, gpu_steps, oracle_inputs,
-                    oracle_sensitivity, rel_err, rhs_flux_scale, stable_dt)
+                    oracle_sensitivity, record, rel_err, rhs_flux_scale, stable_dt)
 
 pytestmark = pytest.mark.gpu
 
@@ -24,6 +24,8 @@ def _rhs_case(pb, seed=W.SEED):
     assert np.all(np.isfinite(ref))
     got = gpu_rhs(pb, q)
     err = rel_err(got, ref, rhs_flux_scale(pb, v, q))
+    record("rhs " + pb.name + " " + "x".join(str(k) for k in pb.n[:pb.ndim]), err, RHS_TOL,
+           rel_err(got, ref))
     assert np.all(err <= RHS_TOL), (pb.name, err)
     # the strict per-equation max|rhs_e| normalisation, reported for the record
     return err, rel_err(got, ref)
@@ -130,6 +132,7 @@ def test_rk3_100_steps_parity(name, make, cfl):
     got = gpu_steps(pb, q, dt, 100)
     err = rel_err(got, ref)
     tol = np.maximum(STEP100_TOL, 3.0 * oracle_sensitivity(P, q, dt, 100, ref))
+    record("100 RK3 steps " + name, err, tol)
     assert np.all(err <= tol), (name, err, tol)
 
 
@@ -141,4 +144,5 @@ def test_one_step_parity_tight():
     ref = O.rk3_step(P, q, dt, 1)
     got = gpu_steps(pb, q, dt, 1)
     dq = rel_err(got - q, ref - q, dt * rhs_flux_scale(pb, v, q))
+    record("1 RK3 step increment " + pb.name, dq, 10 * RHS_TOL)
     assert np.all(dq <= 10 * RHS_TOL), dq

@@ -171,18 +171,30 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- ours
-def algorithmic_bytes(kind: str, E: int, stage_mix=True) -> float:
-    """Algorithmic HBM bytes per interior cell for one launch of each sweep kind
-    (DESIGN.md §6): x: read q, write acc (16E); y: read q, acc, write acc (24E);
-    z + RK epilogue: read q, acc, write q_out (24E) + read q^n in stages 2, 3
-    (+8E for 2 of 3 launches)."""
+def algorithmic_bytes(kind: str, E: int) -> float:
+    """Algorithmic HBM bytes per interior cell for one launch of each sweep kind in an
+    RK3 step: x: read q, write acc (16E); y: read q, acc, q^s (the
+    stencil state, counted once), q^n (stages 2, 3 only), write acc (32E + 8E*2/3);
+    z: read q, acc, write q_out (24E)."""
     if kind == "sweep_x":
         return 16.0 * E
     if kind == "sweep_y":
-        return 24.0 * E
+        return 32.0 * E + 8.0 * E * 2.0 / 3.0
     if kind == "sweep_z":
-        return 24.0 * E + (8.0 * E * 2.0 / 3.0 if stage_mix else 0.0)
+        return 24.0 * E
     return 0.0
+
+
+def algorithmic_flops(kind: str, N: int, d: int) -> float:
+    """Algorithmic fp64 flops per interior cell for one sweep launch:
+    WENO5 98 per variable, HLLC 104 per face (N = 2, d = 3), differencing + source 30,
+    cons->prim 20 once per RHS (a third per sweep); every +, -, *, /, sqrt, min, max
+    of the specification counts as one flop."""
+    E = 2 * N + d + 1
+    return 98.0 * E + 104.0 + 30.0 + 20.0 / 3.0
+
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: unit counts x max clock (DESIGN.md)
 
 
 def run_ours(args):
@@ -209,9 +221,7 @@ def run_ours(args):
     else:
         pb = W.c3_droplet(n, nz=n * world)       # global domain: blocks stacked along z
         procs = (1, 1, world)
-        obj = [mfc.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid, ng = obj[0], None
+        nid, ng = mfc.broadcast_unique_id(), None
         workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
     s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local)
     L = s.layout
@@ -264,15 +274,25 @@ def run_ours(args):
     # dominant kernel roofline (CUDA events on the launch stream, over the timed region)
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    sweeps = {k: v for k, v in prof.items() if k.startswith("sweep")}
+    sweeps = {k: v for k, v in prof.items() if k.startswith("sweep") and v[1]}
     dom = max(sweeps, key=lambda k: sweeps[k][0])
     dom_ms, dom_n = sweeps[dom]
     per_launch_ms = dom_ms / max(dom_n, 1)
+    flops = algorithmic_flops(dom, pb.n_fluids, pb.ndim) * cells_local
+    achieved_tf = flops / (per_launch_ms * 1e-3) / 1e12
     alg_bytes = algorithmic_bytes(dom, E) * cells_local
-    achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    achieved_gbs = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    try:   # DRAM bytes of this kernel from the last committed ncu --set full capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(dom)
+    except Exception:
+        pass
     # per step: 3 x (16E + 24E + 24E) + q^n reads in stages 2 and 3 (2 x 8E) = 208E B/cell
     step_alg_bytes = (16 + 24 + 24) * E * cells_local * RHS_PER_STEP + 2 * 8 * E * cells_local
     hbm_step = step_alg_bytes / (ms_max / args.steps * 1e-3) / 1e9
+    step_flops = (RHS_PER_STEP * sum(algorithmic_flops(k, pb.n_fluids, pb.ndim)
+                                     for k in ("sweep_x", "sweep_y", "sweep_z")) + 96.0) * cells_local
 
     line = {
         "metric": METRIC, "value": grind, "unit": UNIT, "n_gpus": world,
@@ -285,12 +305,20 @@ def run_ours(args):
                    "l2": f"inputs > L2: each state buffer {8 * L.n_elems / 1e9:.2f} GB >> 126 MB, no flush",
                    "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU"},
         "hbm_gbs_step": hbm_step,
+        "fp64_tflops_step": step_flops / (ms_max / args.steps * 1e-3) / 1e12,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+        "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved_tf,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "per_launch_ms": per_launch_ms,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
-                     else "fallback 6650 GB/s (B200_PROFILING.md)"},
+                     "algorithmic_flops_per_cell": algorithmic_flops(dom, pb.n_fluids, pb.ndim),
+                     "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz "
+                                    "(B200_PROFILING.md unit counts/clock; MEASURED_PEAKS.json "
+                                    "has no FP64 entry; tools/fp64_peak.cu measured 34.1)",
+                     "hbm_view": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": achieved_gbs / hbm_peak,
+                                  "algorithmic_bytes_per_cell": algorithmic_bytes(dom, E),
+                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}},
         "clocks": clocks,
         "gpu_launches": launches,
         "state_finite": finite,

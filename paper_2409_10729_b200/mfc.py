@@ -116,6 +116,16 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def broadcast_unique_id(src: int = 0, group=None) -> bytes:
+    """Rank `src` generates the NCCL unique id; every rank of the torch.distributed
+    group receives the same 128 bytes (plumbing for mfc_init with nranks > 1)."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if dist.get_rank(group) == src else None]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    assert isinstance(obj[0], (bytes, bytearray)) and len(obj[0]) == 128
+    return bytes(obj[0])
+
+
 def _stream(stream=None):
     if stream is None:
         stream = torch.cuda.current_stream()

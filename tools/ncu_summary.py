@@ -9,20 +9,20 @@ import sys
 from collections import defaultdict
 
 KEYS = [
-    ("gpu__time_duration.sum", "duration (ns)"),
-    ("dram__bytes_read.sum", "DRAM read (bytes)"),
-    ("dram__bytes_write.sum", "DRAM write (bytes)"),
-    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput (% peak)"),
-    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe inst (% peak, active)"),
-    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe cycles active (%)"),
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe instructions (of peak, active)"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe cycles active"),
     ("smsp__inst_executed.sum", "warp instructions executed"),
-    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy (%)"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy"),
     ("launch__registers_per_thread", "registers / thread"),
-    ("launch__shared_mem_per_block_dynamic", "dynamic smem / block (bytes)"),
-    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy (%)"),
-    ("lts__t_sector_hit_rate.pct", "L2 hit rate (%)"),
+    ("launch__shared_mem_per_block_dynamic", "dynamic smem / block"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
-    ("sm__cycles_elapsed.avg.per_second", "SM clock (Hz)"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
 ]
 STALLS = ["long_scoreboard", "short_scoreboard", "wait", "math_pipe_throttle", "mio_throttle",
           "lg_throttle", "barrier", "branch_resolving", "no_instructions", "not_selected",
@@ -34,12 +34,12 @@ def raw(rep):
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, data = rows[0], rows[1], rows[2:]
-    return hdr, data
+    return hdr, units, data
 
 
 def main():
     rep = sys.argv[1]
-    hdr, data = raw(rep)
+    hdr, units, data = raw(rep)
     idx = {h: i for i, h in enumerate(hdr)}
     name_i = idx.get("Kernel Name")
     print(f"# ncu summary: `{rep.split('/')[-1]}`\n")
@@ -51,7 +51,7 @@ def main():
         print("| metric | value |\n|---|---|")
         for k, label in KEYS:
             if k in idx:
-                print(f"| {label} (`{k}`) | {row[idx[k]]} |")
+                print(f"| {label} (`{k}`) | {row[idx[k]]} {units[idx[k]]} |")
         samples = {}
         for s in STALLS:
             k = f"smsp__pcsamp_warps_issue_stalled_{s}"

@@ -385,8 +385,8 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     int bx = (int)std::min<int64_t>(32, a.nA);
     int by = (int)std::max<int64_t>(1, std::min<int64_t>(128 / bx, a.nB));
     if (dir == 0 && c->D >= 2 && mode == M_SET) {
-        bx = 32;   // staged x sweep: one warp per 32 rows, 2*E KB of shared memory per warp
-        by = (int)std::max<int64_t>(1, std::min<int64_t>(4, a.nB));
+        bx = 32;   // staged x sweep: one warp per 32 rows, E*3 KB of shared memory per warp
+        by = (int)std::max<int64_t>(1, std::min<int64_t>(c->E <= 8 ? 4 : 2, a.nB));
     } else if ((mode == M_RKACC || mode == M_RKINIT) && c->E > 9 && bx * by > 64) {
         by = std::max(1, 64 / bx);   // 12 ring slots x E doubles per thread: keep 2 blocks/SM
     }

@@ -242,27 +242,27 @@ namespace mfc {
 // In the x sweep a warp's 32 lanes march along 32 different rows (consecutive y),
 // so a plain per-lane load touches 32 rows = 32 sectors per instruction.  Here each
 // warp moves its rows through shared memory in chunks of 4 cells (one 32-byte sector
-// per row): the warp copies a chunk [E][32 rows][4] with cp.async (8 full sectors per
-// instruction) and the lanes read their own row from it.  The chunk buffer is reused
-// IN PLACE for the chunk's results (cell x is converted at step x-2, before its result
-// is written at step x+1), which leave as full sectors when the chunk is complete;
-// right after that flush the buffer receives chunk K+2 (two march steps of lead).
-// Layout: element (e, row, x) at (e*32 + row)*4 + (x ^ ((row >> 2) & 3)): the XOR
-// swizzle makes the row-wise march accesses and the sector-wise copies bank-conflict
-// free.  Two buffers per warp = 2 * E KB of shared memory, so three 4-warp blocks fit
-// per SM for E <= 8.
+// per row): the warp copies a chunk [E][32 rows][4] with cp.async, 4 lanes per row
+// sector (each instruction = 8 full sectors), two chunks ahead of the march; the
+// lanes read their own row from it.  Results go to a chunk-sized output buffer and
+// leave as 8 full sectors per store instruction.  Layout inside a chunk buffer:
+// element (e, row, x) at (e*32 + row)*4 + (x ^ ((row >> 2) & 3)): the XOR swizzle
+// makes both the row-wise march reads and the sector-wise copies bank-conflict free.
+// Per warp: 2 input + 1 output chunk buffers = 3 * E * 1 KB of shared memory.
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ int swz(int row, int x) { return row * 4 + (x ^ ((row >> 2) & 3)); }
 
 template <class M>
-__global__ void __launch_bounds__(128, M::E <= 8 ? 3 : 2)
+__global__ void __launch_bounds__(128, 2)
 sweep_x_staged(const SweepArgs a) {
     constexpr int E = M::E;
     constexpr int CH = E * 128;                      // doubles per chunk buffer
     extern __shared__ double smem[];
     const int lane = threadIdx.x;                    // blockDim.x == 32
-    double* const buf0 = smem + threadIdx.y * 2 * CH;
+    double* in0 = smem + threadIdx.y * 3 * CH;
+    double* in1 = in0 + CH;
+    double* outb = in1 + CH;
     const int row0 = blockIdx.x * 32;                // first row (y) of this warp
     const int ib = blockIdx.y * blockDim.y + threadIdx.y;
     if (ib >= a.nB) return;                          // whole warp
@@ -271,14 +271,9 @@ sweep_x_staged(const SweepArgs a) {
     const int64_t plane = a.base + (int64_t)ib * a.sB;   // row row0+r, cell s: plane + (row0+r)*sA + s
     const int crow = lane >> 2, cx = lane & 3;       // copy geometry: 8 rows x 4 cells
     const int nrows = min(32, a.nA - row0);
-    auto bufK = [&](int K) { return buf0 + (K & 1) * CH; };
 
     // chunk K holds cells 4K-4 .. 4K-1 (padded x index 4K .. 4K+3; 32-byte aligned)
-    const int K0 = (s0 + 1) >> 2;                    // chunk of the first cell (s0-3)
-    const int Klast = (s1 + 6) >> 2;                 // chunk of the last cell (s1+2)
-    auto issue = [&](int K) {
-        if (K > Klast) return;
-        double* dst = bufK(K);
+    auto issue = [&](int K, double* dst) {
         const double* src = a.q + plane + map_cell(4 * K - 4 + cx, a.nS, a.gm);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -291,22 +286,23 @@ sweep_x_staged(const SweepArgs a) {
         }
         cp_async_commit();
     };
+    const int Klast = (s1 + 6) >> 2;
     auto convert = [&](int x, double (&v)[E]) {     // cell x of my row -> primitives
         const int K = (x + 4) >> 2;
+        double* b = (K & 1) ? in1 : in0;
         if (((x + 4) & 3) == 0 || x == s0 - 3) {      // first use of chunk K
             cp_async_wait_all();
             __syncwarp();
+            if (K + 1 <= Klast) issue(K + 1, ((K + 1) & 1) ? in1 : in0);
         }
-        const double* b = bufK(K);
         double qc[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) qc[e] = b[e * 128 + swz(lane, (x + 4) & 3)];
         if (map_flip(x, a.nS, a.gm)) qc[M::IM] = -qc[M::IM];
         cons_to_prim_fast<M>(qc, v, a.mat);
     };
-    auto flush = [&](int K) {                        // store results of chunk K, refill
+    auto flush = [&](int K) {                        // store output chunk K (cells 4K-4..4K-1)
         __syncwarp();
-        const double* b = bufK(K);
         const int xc = 4 * K - 4 + cx;
         if (xc >= s0 && xc < s1) {
 #pragma unroll
@@ -316,22 +312,17 @@ sweep_x_staged(const SweepArgs a) {
                     const int r = 8 * i + crow;
                     if (r < nrows)
                         a.dst[plane + (int64_t)(row0 + r) * a.sA + e * a.sE + xc] =
-                            b[e * 128 + swz(r, cx)];
+                            outb[e * 128 + swz(r, cx)];
                 }
             }
         }
         __syncwarp();
-        issue(K + 2);
     };
 
-    issue(K0);
-    issue(K0 + 1);
+    issue((s0 + 1) >> 2, (((s0 + 1) >> 2) & 1) ? in1 : in0);
     double w[5][E];
 #pragma unroll
-    for (int k = 1; k < 5; ++k) convert(s0 - 4 + k, w[k]);   // cells s0-3 .. s0
-    // chunk K0 (cells s0-4 .. s0-1) produces no results: free it now
-    __syncwarp();
-    issue(K0 + 2);
+    for (int k = 1; k < 5; ++k) convert(s0 - 4 + k, w[k]);
 
     double vm_prev[E], F_prev[E];
     double uf_prev = 0.0;
@@ -352,12 +343,11 @@ sweep_x_staged(const SweepArgs a) {
             if (j > s0) {
                 const int x = j - 1;
                 const double du = uf - uf_prev;
-                double* b = bufK((x + 4) >> 2);
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     double r = F_prev[e] - F[e];
                     if (e >= M::IA) r = fma(w[1][e], du, r);
-                    b[e * 128 + swz(lane, (x + 4) & 3)] = r * a.invd;   // in place
+                    outb[e * 128 + swz(lane, (x + 4) & 3)] = r * a.invd;
                 }
                 if (((x + 4) & 3) == 3 || x == s1 - 1) flush((x + 4) >> 2);
             }
@@ -368,7 +358,6 @@ sweep_x_staged(const SweepArgs a) {
 #pragma unroll
         for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
     }
-    cp_async_wait_all();
 }
 
 }  // namespace mfc

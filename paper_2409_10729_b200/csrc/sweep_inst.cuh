@@ -41,8 +41,8 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
     if constexpr (DIR == 0) {
         if (mode == M_SET) {
             if constexpr (M::D >= 2) {
-                // shared-memory staged x sweep: 2 chunk buffers of E*128 doubles per warp
-                const size_t smem = (size_t)b.y * 2 * M::E * 128 * sizeof(double);
+                // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
+                const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
                 static size_t attr = 0;
                 if (smem > attr) {
                     cudaFuncSetAttribute(sweep_x_staged<M>,

@@ -34,7 +34,7 @@
 #include "physics.cuh"
 
 #ifndef MFC_MARCH_UNROLL
-#define MFC_MARCH_UNROLL 2   // unroll factor of the steady-state march loop
+#define MFC_MARCH_UNROLL 1   // unroll factor of the steady-state march loop
 #endif
 #define MFC_PRAGMA_(x) _Pragma(#x)
 #define MFC_UNROLL_(n) MFC_PRAGMA_(unroll n)

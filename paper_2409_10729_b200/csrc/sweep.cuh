@@ -29,15 +29,7 @@
 // whose warp accesses are contiguous rows, never by the x sweep, whose lanes own
 // different rows.
 #pragma once
-#include <type_traits>
-
 #include "physics.cuh"
-
-#ifndef MFC_MARCH_UNROLL
-#define MFC_MARCH_UNROLL 1   // unroll factor of the steady-state march loop
-#endif
-#define MFC_PRAGMA_(x) _Pragma(#x)
-#define MFC_UNROLL_(n) MFC_PRAGMA_(unroll n)
 
 #ifndef MFC_ACC_MINB
 #define MFC_ACC_MINB 3   // resident 128-thread blocks per SM for the non-RK sweep modes
@@ -182,12 +174,7 @@ sweep_kernel(const SweepArgs a) {
     double F_prev[E];      // flux at face j-3/2
     double uf_prev = 0.0;
 
-    // One march step j: convert cell j+2, WENO of cell j, HLLC of face j-1/2 (DO_FACE),
-    // update of cell j-1 (DO_UPDATE).  The first two steps of a segment are peeled so
-    // the steady-state step has no branches.
-    auto step = [&](const int j, auto do_face, auto do_update) {
-        constexpr bool DO_FACE = decltype(do_face)::value;
-        constexpr bool DO_UPDATE = decltype(do_update)::value;
+    for (int j = s0 - 1; j <= s1; ++j) {
         cp_async_wait_1();                             // group of step j has landed
         issue(j + 2);
 #pragma unroll
@@ -202,14 +189,16 @@ sweep_kernel(const SweepArgs a) {
             if (map_flip(j + 2, a.nS, a.gm)) qc[M::IM + DIR] = -qc[M::IM + DIR];
             cons_to_prim_fast<M>(qc, w[4], a.mat);
         }
+
         double vm[E], vp[E];
 #pragma unroll
         for (int e = 0; e < E; ++e)
             weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, vm[e], vp[e]);
-        if constexpr (DO_FACE) {
+
+        if (j >= s0) {
             double F[E], uf;
             hllc<M, DIR>(vm_prev, vp, a.mat, F, uf);
-            if constexpr (DO_UPDATE) {
+            if (j > s0) {
                 // cell j-1: faces j-3/2 (F_prev) and j-1/2 (F); alpha_{j-1} = w[1]
                 const int cc = j - 1;
                 const int64_t c = line + (int64_t)cc * a.sS;
@@ -239,13 +228,7 @@ sweep_kernel(const SweepArgs a) {
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
-    };
-    using T_ = std::true_type;
-    using F_ = std::false_type;
-    step(s0 - 1, F_{}, F_{});
-    step(s0, T_{}, F_{});
-    MFC_UNROLL_(MFC_MARCH_UNROLL)
-    for (int j = s0 + 1; j <= s1; ++j) step(j, T_{}, T_{});
+    }
     cp_async_wait_all();
 }
 

@@ -291,12 +291,22 @@ int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
     if (count == 1 && cs[0]->nranks > 1 && !cs[0]->loopback) {
         mfc_ctx* c = cs[0];
         if (has_neighbors(c)) {
+            // NCCL pairs the k-th send A->B with the k-th receive on B from A.  The
+            // message of my face f lands in the neighbour's face f^1, and every rank
+            // posts its receives in ascending face order, so sends are posted in
+            // ascending order of the DESTINATION face f^1 (1,0,3,2,5,4).  This matters
+            // when both faces of an axis have the same peer (2 ranks, periodic).
             NCCL_TRY(ncclGroupStart());
+            for (int g = 0; g < 2 * c->D; ++g) {
+                const int f = g ^ 1;
+                if (c->bc[f] != BC_NEIGHBOR) continue;
+                NCCL_TRY(ncclSend(c->sendb[f], (size_t)c->face_elems[f / 2], ncclFloat64,
+                                  c->nbr[f], c->comm, s));
+            }
             for (int f = 0; f < 2 * c->D; ++f) {
                 if (c->bc[f] != BC_NEIGHBOR) continue;
-                const size_t n = (size_t)c->face_elems[f / 2];
-                NCCL_TRY(ncclSend(c->sendb[f], n, ncclFloat64, c->nbr[f], c->comm, s));
-                NCCL_TRY(ncclRecv(c->recvb[f], n, ncclFloat64, c->nbr[f], c->comm, s));
+                NCCL_TRY(ncclRecv(c->recvb[f], (size_t)c->face_elems[f / 2], ncclFloat64,
+                                  c->nbr[f], c->comm, s));
             }
             NCCL_TRY(ncclGroupEnd());
         }

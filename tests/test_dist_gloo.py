@@ -61,8 +61,10 @@ def _worker(rank, world, port, out_dir):
     send_hi = torch.from_numpy(np.ascontiguousarray(qs[:, nz:nz + g][:, :, inner[2], inner[3]]))
     recv_lo = torch.empty_like(send_lo)
     recv_hi = torch.empty_like(send_hi)
-    ops = [dist.P2POp(dist.isend, send_lo, lo_nb), dist.P2POp(dist.irecv, recv_hi, hi_nb),
-           dist.P2POp(dist.isend, send_hi, hi_nb), dist.P2POp(dist.irecv, recv_lo, lo_nb)]
+    # libmfc's NCCL ordering: sends in ascending DESTINATION face (my hi face lands in
+    # the neighbour's lo face, so it goes first), receives in ascending own face
+    ops = [dist.P2POp(dist.isend, send_hi, hi_nb), dist.P2POp(dist.isend, send_lo, lo_nb),
+           dist.P2POp(dist.irecv, recv_lo, lo_nb), dist.P2POp(dist.irecv, recv_hi, hi_nb)]
     for r in dist.batch_isend_irecv(ops):
         r.wait()
     qs[:, 0:g, inner[2], inner[3]] = recv_lo.numpy()

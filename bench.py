@@ -214,20 +214,42 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
 
     n = args.n
-    block = W.c3_droplet(n)                      # the per-GPU block (C3 / C4)
-    if world == 1:
-        pb, procs, nid, ng = block, (1, 1, 1), None, None
-        workload = f"C3 3D two-fluid shock-droplet {n}^3 (BASELINE configs[2])"
-    else:
-        pb = W.c3_droplet(n, nz=n * world)       # global domain: blocks stacked along z
-        procs = (1, 1, world)
-        nid, ng = mfc.broadcast_unique_id(), None
-        workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
-    s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local)
+    nid = mfc.broadcast_unique_id() if world > 1 else None
+    procs = (1, 1, world)
+    if args.config == "C3":
+        block = W.c3_droplet(n)                  # the per-GPU block (C3 / C4)
+        if world == 1:
+            pb = block
+            workload = f"C3 3D two-fluid shock-droplet {n}^3 (BASELINE configs[2])"
+        else:
+            pb = W.c3_droplet(n, nz=n * world)   # global domain: blocks stacked along z
+            workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
+        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local)
+        # every rank holds the same C3 block (its local prims), converted on the GPU
+        q = s.state_from_prims(W.c3_prims(block))
+        dt = block.dt
+    elif args.config == "C5":
+        nn = args.n if args.n != 256 else 512
+        pb = W.c5_three_fluid(nn)                # strong scaling: fixed 512^3 split in z-slabs
+        workload = f"C5 3D three-fluid shock-droplet {nn}^3 total, z-slabs x{world} (BASELINE configs[4])"
+        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local)
+        L0 = s.layout
+        v = s.empty_state()
+        vi = s.interior(v)
+        z0, nzl = L0.lo_global[2], L0.n_local[2]
+        for zz in range(0, nzl, 64):             # slab-wise host generation
+            vi[:, zz:zz + 64].copy_(torch.as_tensor(W.c5_prims(pb, z0 + zz, z0 + min(zz + 64, nzl))))
+        q = s.empty_state()
+        s.prim_to_cons(v, q)
+        del v, vi
+        dt = pb.dt
+    else:                                        # C2, single GPU
+        pb = W.c2_shock_bubble()
+        workload = "C2 2D air-helium shock-bubble 1024x512 (BASELINE configs[1])"
+        s = mfc.Solver(pb, procs=(1, 1, 1), device=local)
+        q = s.state_from_prims(W.c2_prims(pb))
+        dt = pb.dt
     L = s.layout
-    # every rank holds the same C3 block (its local prims), converted on the GPU
-    q = s.state_from_prims(W.c3_prims(block))
-    dt = block.dt
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -297,8 +319,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": grind, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
+        "higher_is_better": False, "scaling": "strong" if args.config == "C5" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload, "cells_per_gpu": cells_local, "cells_total": cells_total,
                    "E": E, "n_fluids": pb.n_fluids, "decomposition": f"procs={list(procs)}",
                    "rhs_per_step": RHS_PER_STEP, "dt": dt,
@@ -364,6 +386,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=256, help="cells per dimension of the per-GPU block")
+    ap.add_argument("--config", default="C3", choices=["C3", "C5", "C2"],
+                    help="C3/C4 (default; weak scaling for N > 1), C5 (strong scaling), C2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -45,18 +45,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def run(job):
         src, cmd = job
+        obj = cmd[-1]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log = os.path.join(BUILD, src + ".log")
         with open(log, "w") as f:
             f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
-        return src
+            if os.path.exists(obj):
+                os.remove(obj)          # never link a stale object after a failed compile
+            return src, r.stderr[-4000:]
+        return src, None
 
+    errors = []
     with ThreadPoolExecutor(max_workers=min(4, max(1, len(jobs)))) as ex:
-        for src in ex.map(run, jobs):
-            if verbose:
+        for src, err in ex.map(run, jobs):
+            if err:
+                errors.append(f"nvcc failed for {src}:\n{err}")
+            elif verbose:
                 print("compiled", src, file=sys.stderr)
+    if errors:
+        if os.path.exists(SO):
+            os.remove(SO)               # a failed build leaves no library behind
+        raise RuntimeError("\n".join(errors))
     if force or jobs or _stale(SO, objs):
         tmp = SO + f".tmp{os.getpid()}"
         cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lnccl", "-lcuda"]

@@ -397,9 +397,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     if (dir == 0 && c->D >= 2 && mode == M_SET) {
         bx = 32;   // staged x sweep: one warp per 32 rows, E*3 KB of shared memory per warp
         by = (int)std::max<int64_t>(1, std::min<int64_t>(c->E <= 8 ? 4 : 2, a.nB));
-    } else if ((mode == M_RKACC || mode == M_RKINIT) && c->E > 9 && bx * by > 64) {
-        by = std::max(1, 64 / bx);   // 12 ring slots x E doubles per thread: keep 2 blocks/SM
-    }
+    }   // (ring sweeps fix their own block shape: 32 x NTH/32, see sweep_nth)
     dim3 block(bx, by);
     dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.nS + a.T - 1) / a.T);
     cudaError_t e;

@@ -97,6 +97,12 @@ struct Rings {
 template <class M, int MODE>
 constexpr size_t sweep_smem_per_thread() { return (size_t)Rings<MODE>::SLOTS * M::E * sizeof(double); }
 
+// Threads per block of the ring sweeps (a compile-time constant so that ring offsets
+// fold into instruction immediates): 128, or 64 where 12 ring slots of E > 9 doubles
+// would not leave room for two blocks per SM.
+template <class M, int MODE>
+__host__ __device__ constexpr int sweep_nth() { return ((MODE == M_RKACC || MODE == M_RKINIT) && M::E > 9) ? 64 : 128; }
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
@@ -108,18 +114,18 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 // 3 resident blocks (12 warps/SM, <= 168 registers) where that does not spill (the
 // non-RK modes for E <= 8); 2 blocks otherwise.
 template <class M, int MODE>
-constexpr int sweep_min_blocks() {
+__host__ __device__ constexpr int sweep_min_blocks() {
     return ((MODE == M_ACC || MODE == M_SET) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
 template <class M, int DIR, int MODE>
-__global__ void __launch_bounds__(128, sweep_min_blocks<M, MODE>())
+__global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, MODE>())
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
     using R = Rings<MODE>;
     extern __shared__ double smem[];
-    const int nth = blockDim.x * blockDim.y;
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    constexpr int nth = sweep_nth<M, MODE>();            // == blockDim.x * blockDim.y
+    const int tid = threadIdx.y * 32 + threadIdx.x;      // blockDim.x == 32
     double* const ringQ = smem + tid;                       // QS slots
     double* const ringA = ringQ + R::QS * E * nth;          // AS slots
     double* const ringN = ringA + R::AS * E * nth;          // NS slots
@@ -139,16 +145,18 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
         for (int e = 0; e < E; ++e) cp_async8(&at(ring, slot, e), p + e * a.sE);
     };
-    // group for step j: state of cell j+2, epilogue operands of cell j-1
-    auto issue = [&](int j) {
-        if (j + 2 <= s1 + 2) fetch(ringQ, (j + 2 + 3) % R::QS, q, j + 2);
+    // group for step j: state of cell j+2 -> state slot sq, epilogue operands of cell
+    // j-1 -> operand slot sa.  Slots: state cell c at (c+3) % QS, operands at (c+3) % 3.
+    auto issue = [&](int j, int sq, int sa) {
+        if (j + 2 <= s1 + 2) fetch(ringQ, sq, q, j + 2);
         const int c = j - 1;
         if (c >= s0 && c < s1) {
-            if (R::AS) fetch(ringA, (c + 3) % 3, a.acc, c);
-            if (R::NS && a.ca != 0.0) fetch(ringN, (c + 3) % 3, a.qn, c);
+            if (R::AS) fetch(ringA, sa, a.acc, c);
+            if (R::NS && a.ca != 0.0) fetch(ringN, sa, a.qn, c);
         }
         cp_async_commit();
     };
+    auto inc = [](int k, int n) { return k + 1 == n ? 0 : k + 1; };
 
     double w[5][E];        // primitive window: cells j-2 .. j+2
     {
@@ -167,8 +175,15 @@ sweep_kernel(const SweepArgs a) {
             cons_to_prim_fast<M>(qc, w[k], a.mat);
         }
     }
-    issue(s0 - 1);
-    issue(s0);
+    issue(s0 - 1, (s0 + 4) % R::QS, (s0 + 1) % 3);
+    issue(s0, (s0 + 5) % R::QS, (s0 + 2) % 3);
+    // rotating slots at step j: conversion (cell j+2), fetch (cell j+4), q^s (cell j-1),
+    // operands of cell j-1, operand fetch (cell j+1)
+    int kq = (s0 + 4) % R::QS;
+    int kqf = (s0 + 6) % R::QS;
+    int kqs = (s0 + 1) % R::QS;
+    int ka = (s0 + 1) % 3;
+    int kaf = (s0 + 3) % 3;
 
     double vm_prev[E];     // v-_{j-1/2} (from cell j-1)
     double F_prev[E];      // flux at face j-3/2
@@ -176,7 +191,7 @@ sweep_kernel(const SweepArgs a) {
 
     for (int j = s0 - 1; j <= s1; ++j) {
         cp_async_wait_1();                             // group of step j has landed
-        issue(j + 2);
+        issue(j + 2, kqf, kaf);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
 #pragma unroll
@@ -185,7 +200,7 @@ sweep_kernel(const SweepArgs a) {
         {
             double qc[E];
 #pragma unroll
-            for (int e = 0; e < E; ++e) qc[e] = at(ringQ, (j + 2 + 3) % R::QS, e);
+            for (int e = 0; e < E; ++e) qc[e] = at(ringQ, kq, e);
             if (map_flip(j + 2, a.nS, a.gm)) qc[M::IM + DIR] = -qc[M::IM + DIR];
             cons_to_prim_fast<M>(qc, w[4], a.mat);
         }
@@ -209,14 +224,14 @@ sweep_kernel(const SweepArgs a) {
                     if (e >= M::IA) r = fma(w[1][e], du, r);
                     double out;
                     if (MODE == M_SET) out = r * a.invd;
-                    else if (MODE == M_ACC) out = fma(a.w * a.invd, r, at(ringA, (cc + 3) % 3, e));
+                    else if (MODE == M_ACC) out = fma(a.w * a.invd, r, at(ringA, ka, e));
                     else {
-                        const double qs = at(ringQ, (cc + 3) % R::QS, e);
+                        const double qs = at(ringQ, kqs, e);
                         const double base = a.ca != 0.0
-                                                ? fma(a.ca, at(ringN, (cc + 3) % 3, e), a.cb * qs)
+                                                ? fma(a.ca, at(ringN, ka, e), a.cb * qs)
                                                 : a.cb * qs;
                         out = MODE == M_RKACC
-                                  ? fma(a.w, fma(a.invd, r, at(ringA, (cc + 3) % 3, e)), base)
+                                  ? fma(a.w, fma(a.invd, r, at(ringA, ka, e)), base)
                                   : fma(a.w * a.invd, r, base);
                     }
                     a.dst[c + e * a.sE] = out;
@@ -228,6 +243,11 @@ sweep_kernel(const SweepArgs a) {
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
+        kq = inc(kq, R::QS);
+        kqf = inc(kqf, R::QS);
+        kqs = inc(kqs, R::QS);
+        ka = inc(ka, 3);
+        kaf = inc(kaf, 3);
     }
     cp_async_wait_all();
 }

@@ -26,7 +26,10 @@ __global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons)
 
 template <class M, int DIR, int MODE>
 static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
-    const size_t smem = sweep_smem_per_thread<M, MODE>() * b.x * b.y;
+    constexpr int NTH = sweep_nth<M, MODE>();
+    b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
+    g = dim3((a.nA + 31) / 32, (a.nB + b.y - 1) / b.y, g.z);
+    const size_t smem = sweep_smem_per_thread<M, MODE>() * NTH;
     static size_t attr = 0;
     if (smem > attr) {
         cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -273,8 +273,10 @@ namespace mfc {
 
 __device__ __forceinline__ int swz(int row, int x) { return row * 4 + (x ^ ((row >> 2) & 3)); }
 
+// One warp per block (3*E KB of shared memory): 9 resident warps per SM for E = 8
+// (the register budget allows 227 per thread) instead of 2 x 4-warp blocks.
 template <class M>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(32, M::E <= 8 ? 9 : 6)
 sweep_x_staged(const SweepArgs a) {
     constexpr int E = M::E;
     constexpr int CH = E * 128;                      // doubles per chunk buffer

@@ -395,8 +395,8 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     int bx = (int)std::min<int64_t>(32, a.nA);
     int by = (int)std::max<int64_t>(1, std::min<int64_t>(128 / bx, a.nB));
     if (dir == 0 && c->D >= 2 && mode == M_SET) {
-        bx = 32;   // staged x sweep: one warp (32 rows) per block, E*3 KB of shared memory
-        by = 1;
+        bx = 32;   // staged x sweep: one warp per 32 rows, E*3 KB of shared memory per warp
+        by = (int)std::max<int64_t>(1, std::min<int64_t>(c->E <= 8 ? 4 : 2, a.nB));
     }   // (ring sweeps fix their own block shape: 32 x NTH/32, see sweep_nth)
     dim3 block(bx, by);
     dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.nS + a.T - 1) / a.T);

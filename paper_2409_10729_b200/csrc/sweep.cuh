@@ -273,10 +273,8 @@ namespace mfc {
 
 __device__ __forceinline__ int swz(int row, int x) { return row * 4 + (x ^ ((row >> 2) & 3)); }
 
-// One warp per block (3*E KB of shared memory): 9 resident warps per SM for E = 8
-// (the register budget allows 227 per thread) instead of 2 x 4-warp blocks.
 template <class M>
-__global__ void __launch_bounds__(32, M::E <= 8 ? 9 : 6)
+__global__ void __launch_bounds__(128, 2)
 sweep_x_staged(const SweepArgs a) {
     constexpr int E = M::E;
     constexpr int CH = E * 128;                      // doubles per chunk buffer
@@ -296,15 +294,15 @@ sweep_x_staged(const SweepArgs a) {
 
     // chunk K holds cells 4K-4 .. 4K-1 (padded x index 4K .. 4K+3; 32-byte aligned)
     auto issue = [&](int K, double* dst) {
-        const double* src = a.q + plane + map_cell(4 * K - 4 + cx, a.nS, a.gm);
-#pragma unroll
+        const double* src = a.q + plane + (int64_t)(row0 + crow) * a.sA + map_cell(4 * K - 4 + cx, a.nS, a.gm);
+#pragma unroll 1
         for (int e = 0; e < E; ++e) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int r = 8 * i + crow;
-                if (r < nrows)
-                    cp_async8(dst + e * 128 + swz(r, cx), src + (int64_t)(row0 + r) * a.sA + e * a.sE);
+                if (8 * i + crow < nrows)
+                    cp_async8(dst + e * 128 + swz(8 * i + crow, cx), src + (int64_t)(8 * i) * a.sA);
             }
+            src += a.sE;
         }
         cp_async_commit();
     };
@@ -327,15 +325,15 @@ sweep_x_staged(const SweepArgs a) {
         __syncwarp();
         const int xc = 4 * K - 4 + cx;
         if (xc >= s0 && xc < s1) {
-#pragma unroll
+            double* dst = a.dst + plane + (int64_t)(row0 + crow) * a.sA + xc;
+#pragma unroll 1
             for (int e = 0; e < E; ++e) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int r = 8 * i + crow;
-                    if (r < nrows)
-                        a.dst[plane + (int64_t)(row0 + r) * a.sA + e * a.sE + xc] =
-                            outb[e * 128 + swz(r, cx)];
+                    if (8 * i + crow < nrows)
+                        dst[(int64_t)(8 * i) * a.sA] = outb[e * 128 + swz(8 * i + crow, cx)];
                 }
+                dst += a.sE;
             }
         }
         __syncwarp();

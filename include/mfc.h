@@ -152,6 +152,13 @@ int mfc_rhs(mfc_ctx* ctx, double* q, double* rhs, void* stream);
  * Needs a bound workspace (ESTATE otherwise). */
 int mfc_rk3_step(mfc_ctx* ctx, double* q, double dt, void* stream);
 
+/* nsteps SSP-RK3 steps of size dt on q (as nsteps calls of mfc_rk3_step), replayed
+ * from a CUDA graph of one step that the library captures on first use and keeps
+ * while q and dt stay the same (NCCL halo calls are captured too).  Removes the
+ * per-kernel launch latency that dominates small grids.  With profiling enabled
+ * the steps are launched individually. */
+int mfc_rk3_steps(mfc_ctx* ctx, double* q, double dt, int64_t nsteps, void* stream);
+
 /* End-to-end call with HOST buffers: copy the dense interior q_in[E][nz][ny][nx]
  * (host, pinned or pageable) into the padded device buffer q_dev, run nsteps RK3
  * steps of size dt, copy the interior back to q_out (host; may equal q_in), and

@@ -93,6 +93,12 @@ struct mfc_ctx {
     struct Rec { int kind; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     size_t ev_used = 0;
+    // CUDA graph of one RK3 step (mfc_rk3_steps), keyed on the state pointer and dt
+    cudaGraphExec_t graph = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    const double* graph_q = nullptr;
+    double graph_dt = 0.0;
+    int64_t graph_launches = 0;
 };
 
 namespace {
@@ -740,6 +746,46 @@ int mfc_rk3_step(mfc_ctx* c, double* q, double dt, void* stream) {
     return rk3_group(&c, &q, 1, dt, (cudaStream_t)stream);
 }
 
+int mfc_rk3_steps(mfc_ctx* c, double* q, double dt, int64_t nsteps, void* stream) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (!std::isfinite(dt)) return fail(MFC_EINVAL, "dt not finite");
+    if (nsteps < 0) return fail(MFC_EINVAL, "nsteps < 0");
+    int st = set_device(c);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (c->prof) {   // per-launch event timing needs the plain launches
+        for (int64_t i = 0; i < nsteps; ++i)
+            if ((st = rk3_group(&c, &q, 1, dt, s))) return st;
+        return MFC_OK;
+    }
+    if (nsteps == 0) return MFC_OK;
+    if (!c->graph || c->graph_q != q || c->graph_dt != dt) {
+        if (c->graph) {
+            cudaGraphExecDestroy(c->graph);
+            c->graph = nullptr;
+        }
+        if (!c->cap_stream) CU_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        CU_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+        st = rk3_group(&c, &q, 1, dt, c->cap_stream);
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+        if (st) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        if (e != cudaSuccess) return fail(MFC_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        const cudaError_t ei = cudaGraphInstantiate(&c->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) return fail(MFC_ECUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+        c->graph_q = q;
+        c->graph_dt = dt;
+        c->graph_launches = c->launches;
+    }
+    for (int64_t i = 0; i < nsteps; ++i) CU_TRY(cudaGraphLaunch(c->graph, s));
+    c->launches = c->graph_launches * nsteps;
+    return MFC_OK;
+}
+
 int mfc_advance_host(mfc_ctx* c, const double* q_in, double* q_out, double* q_dev,
                      int64_t nsteps, double dt, void* stream) {
     if (!c || !q_in || !q_out) return fail(MFC_EINVAL, "NULL argument");
@@ -765,8 +811,7 @@ int mfc_advance_host(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
         return MFC_OK;
     };
     if ((st = copy(true))) return st;
-    for (int64_t i = 0; i < nsteps; ++i)
-        if ((st = rk3_group(&c, &q_dev, 1, dt, s))) return st;
+    if ((st = mfc_rk3_steps(c, q_dev, dt, nsteps, stream))) return st;
     if ((st = copy(false))) return st;
     CU_TRY(cudaStreamSynchronize(s));
     return MFC_OK;
@@ -831,6 +876,8 @@ int mfc_profile_read(mfc_ctx* c, double* ms, int64_t* count, int32_t nkinds) {
 
 int mfc_finalize(mfc_ctx* c) {
     if (!c) return MFC_OK;
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;

@@ -27,6 +27,7 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ES
 EXPORTED = [
     "mfc_init", "mfc_get_layout", "mfc_get_neighbors", "mfc_bind_workspace", "mfc_set_weno_eps",
     "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
+    "mfc_rk3_steps",
     "mfc_advance_host", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
     "mfc_nccl_get_unique_id", "mfc_last_launch_count", "mfc_profile_enable", "mfc_profile_read", "mfc_finalize", "mfc_last_error",
     "mfc_version",
@@ -75,6 +76,7 @@ def _load():
         "mfc_halo_exchange": [vp, vp, vp],
         "mfc_rhs": [vp, vp, vp, vp],
         "mfc_rk3_step": [vp, vp, dbl, vp],
+        "mfc_rk3_steps": [vp, vp, dbl, i64, vp],
         "mfc_advance_host": [vp, vp, vp, vp, i64, dbl, vp],
         "mfc_halo_exchange_group": [pp, pp, i32, vp],
         "mfc_rhs_group": [pp, pp, pp, i32, vp],
@@ -238,6 +240,11 @@ class Solver:
 
     def rk3_step(self, q, dt: float, stream=None):
         _check(lib.mfc_rk3_step(self._h, _ptr(q), float(dt), _stream(stream)), "mfc_rk3_step")
+
+    def rk3_steps(self, q, dt: float, nsteps: int, stream=None):
+        """nsteps RK3 steps replayed from a CUDA graph of one step."""
+        _check(lib.mfc_rk3_steps(self._h, _ptr(q), float(dt), int(nsteps), _stream(stream)),
+               "mfc_rk3_steps")
 
     def advance_host(self, q_in: torch.Tensor, q_out: torch.Tensor, q_dev: torch.Tensor,
                      nsteps: int, dt: float, stream=None):

@@ -146,3 +146,25 @@ def test_one_step_parity_tight():
     dq = rel_err(got - q, ref - q, dt * rhs_flux_scale(pb, v, q))
     record("1 RK3 step increment " + pb.name, dq, 10 * RHS_TOL)
     assert np.all(dq <= 10 * RHS_TOL), dq
+
+
+@pytest.mark.parametrize("make", [lambda: W.c1_water_air(), lambda: W.random_problem(3, (20, 18, 16), 2, "water")])
+def test_graph_steps_bitwise_equal_to_single_steps(make):
+    """mfc_rk3_steps (CUDA graph replay) == the same number of mfc_rk3_step calls."""
+    pb = make()
+    P, v, q = oracle_inputs(pb)
+    dt = pb.dt if pb.dt else stable_dt(pb, v)
+    s = gpu_solver(pb)
+    a = s.state_from_cons(q)
+    b = s.state_from_cons(q)
+    for _ in range(7):
+        s.rk3_step(a, dt)
+    s.rk3_steps(b, dt, 4)
+    s.rk3_steps(b, dt, 3)            # graph reused
+    torch.cuda.synchronize()
+    assert torch.equal(s.interior(a), s.interior(b))
+    c = s.state_from_cons(q)
+    s.rk3_steps(c, dt * 0.5, 2)      # new key (q, dt): re-captured
+    s.rk3_step(b, dt * 0.5)
+    torch.cuda.synchronize()
+    assert torch.isfinite(s.interior(c)).all()

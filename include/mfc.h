@@ -134,6 +134,16 @@ int mfc_set_weno_eps(mfc_ctx* ctx, double eps);
 int mfc_prim_to_cons(mfc_ctx* ctx, const double* v, double* q, void* stream);
 int mfc_cons_to_prim(mfc_ctx* ctx, const double* q, double* v, void* stream);
 
+/* Adaptive time step (DESIGN.md AMB-25).  mfc_max_wave_rate writes
+ * to the device double *d_out the maximum over all interior cells (all ranks: NCCL
+ * max-allreduce) of max_k (|u_k| + c)/dx_k, c^2 = ((Gamma+1)p + Pi)/(rho Gamma);
+ * enqueued on `stream`, no host sync.  mfc_cfl_dt computes it into the device
+ * scratch double d_scratch, synchronises `stream` and returns *dt_out = cfl/rate on
+ * the host (ESTATE if the rate is not positive and finite). */
+int mfc_max_wave_rate(mfc_ctx* ctx, const double* q, double* d_out, void* stream);
+int mfc_cfl_dt(mfc_ctx* ctx, const double* q, double cfl, double* dt_out, double* d_scratch,
+               void* stream);
+
 /* Fill the 3 ghost layers of every active dimension of q: physical faces by the
  * boundary condition, faces shared with another rank by the halo exchange
  * (P:94).  Face ghosts only (edges/corners are never read).  Only ghost cells of

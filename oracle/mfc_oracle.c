@@ -540,6 +540,41 @@ int64_t orc_count_inadmissible(const orc_problem* P, const double* q) {
     return bad;
 }
 
+double orc_max_wave_rate(const orc_problem* P, const double* q) {
+    const int N = P->N, d = P->d, E = orc_num_eq(N, d);
+    const int ia = N + d + 1;
+    double Gam[ORC_MAXF], Pi[ORC_MAXF];
+    orc_constants(P, Gam, Pi);
+    int64_t pd[3];
+    orc_padded_dims(P, pd);
+    const int64_t ncell = pd[0] * pd[1] * pd[2];
+    const int64_t o[3] = {ORC_G, d >= 2 ? ORC_G : 0, d >= 3 ? ORC_G : 0};
+    double rate = 0.0;
+    for (int64_t k = 0; k < P->n[2]; ++k) {
+        for (int64_t j = 0; j < P->n[1]; ++j) {
+            for (int64_t i = 0; i < P->n[0]; ++i) {
+                const int64_t cc = cell_index(pd, o[0] + i, o[1] + j, o[2] + k);
+                double qc[ORC_MAXE], v[ORC_MAXE];
+                for (int e = 0; e < E; ++e) qc[e] = q[e * ncell + cc];
+                orc_cons_to_prim_cell(P, Gam, Pi, qc, v);
+                double rho = v[0];
+                for (int i2 = 1; i2 < N; ++i2) rho = rho + v[i2];
+                double G = v[ia] * Gam[0], PI = v[ia] * Pi[0];
+                for (int i2 = 1; i2 < N; ++i2) {
+                    G = G + v[ia + i2] * Gam[i2];
+                    PI = PI + v[ia + i2] * Pi[i2];
+                }
+                const double c = sqrt(((G + 1.0) * v[N + d] + PI) / (rho * G));
+                for (int dir = 0; dir < d; ++dir) {
+                    const double r = (fabs(v[N + dir]) + c) / P->dx[dir];
+                    if (r > rate) rate = r;
+                }
+            }
+        }
+    }
+    return rate;
+}
+
 int32_t orc_num_threads(void) {
 #ifdef _OPENMP
     return (int32_t)omp_get_max_threads();

@@ -103,6 +103,11 @@ void orc_rk3_combine(int32_t stage, int64_t n, const double* qn, const double* q
 /* One SSP-RK3 step on the padded state q (in place), ghost fill before each L. */
 void orc_rk3_step(const orc_problem* P, double* q, double dt);
 
+/* CFL wave rate (DESIGN.md AMB-25): max over interior cells of
+ * max_k (|u_k| + c)/dx_k with c^2 = ((Gamma+1)p + Pi)/(rho Gamma) (AMB-10).
+ * dt = CFL / rate. */
+double orc_max_wave_rate(const orc_problem* P, const double* q);
+
 /* Admissibility check (AMB-14): returns number of interior cells with
  * non-finite values, rho <= 0 or c^2 <= 0. */
 int64_t orc_count_inadmissible(const orc_problem* P, const double* q);

@@ -21,7 +21,7 @@ __all__ = [
     "build", "lib", "Problem", "num_eq", "pad", "unpad", "constants", "cons_to_prim",
     "prim_to_cons", "weno5_minus", "weno5_plus", "hllc", "fill_ghosts", "rhs",
     "rhs_padded", "rhs_cells", "rk3_combine", "rk3_step", "count_inadmissible",
-    "num_threads", "BC_EXTERNAL", "BC_PERIODIC", "BC_REFLECTIVE", "BC_EXTRAPOLATION",
+    "num_threads", "max_wave_rate", "BC_EXTERNAL", "BC_PERIODIC", "BC_REFLECTIVE", "BC_EXTRAPOLATION",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -91,6 +91,7 @@ def lib():
                                            ctypes.c_double, _dp]),
                 "orc_rk3_step": (None, [P, _dp, ctypes.c_double]),
                 "orc_count_inadmissible": (ctypes.c_int64, [P, _dp]),
+                "orc_max_wave_rate": (ctypes.c_double, [P, _dp]),
                 "orc_num_threads": (ctypes.c_int32, []),
             }
             for name, (res, args) in sig.items():
@@ -279,6 +280,12 @@ def rk3_step(P: Problem, q: np.ndarray, dt: float, nsteps: int = 1) -> np.ndarra
 def count_inadmissible(P: Problem, q: np.ndarray) -> int:
     qp = pad(P, np.asarray(q, dtype=np.float64))
     return int(lib().orc_count_inadmissible(P.ptr(), _p(qp)))
+
+
+def max_wave_rate(P: Problem, q: np.ndarray) -> float:
+    """max over interior cells of max_k (|u_k| + c)/dx_k (dt = CFL / rate)."""
+    qp = pad(P, np.asarray(q, dtype=np.float64))
+    return float(lib().orc_max_wave_rate(P.ptr(), _p(qp)))
 
 
 def num_threads() -> int:

@@ -715,6 +715,52 @@ static int eos(mfc_ctx* c, const double* in, double* out, bool to_cons, void* st
     return MFC_OK;
 }
 
+int mfc_max_wave_rate(mfc_ctx* c, const double* q, double* d_out, void* stream) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    int st;
+    if ((st = check_ptr(q, "q")) || (st = set_device(c))) return st;
+    if (!d_out || ((uintptr_t)d_out) % 8) return fail(MFC_EINVAL, "d_out NULL or misaligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    EosArgs a;
+    a.in = q;
+    a.out = nullptr;
+    a.sE = c->stride[0];
+    a.sZ = c->stride[1];
+    a.sY = c->stride[2];
+    a.base = c->offset;
+    a.nx = (int32_t)c->nl[0];
+    a.ny = (int32_t)c->nl[1];
+    a.nz = (int32_t)c->nl[2];
+    a.mat = c->mat;
+    const double3 inv = make_double3(1.0 / c->dx[0], 1.0 / c->dx[1], 1.0 / c->dx[2]);
+    CU_TRY(cudaMemsetAsync(d_out, 0, sizeof(double), s));
+    cudaError_t e;
+    switch (c->N) {
+        case 1: e = launch_wave_rate<1>(c->D, a, inv, d_out, s); break;
+        case 2: e = launch_wave_rate<2>(c->D, a, inv, d_out, s); break;
+        default: e = launch_wave_rate<3>(c->D, a, inv, d_out, s); break;
+    }
+    if (e != cudaSuccess) return fail(MFC_ECUDA, "wave rate launch: %s", cudaGetErrorString(e));
+    if (c->comm) NCCL_TRY(ncclAllReduce(d_out, d_out, 1, ncclFloat64, ncclMax, c->comm, s));
+    return MFC_OK;
+}
+
+int mfc_cfl_dt(mfc_ctx* c, const double* q, double cfl, double* dt_out, double* d_scratch,
+               void* stream) {
+    if (!c || !dt_out || !d_scratch) return fail(MFC_EINVAL, "NULL argument");
+    if (!(cfl > 0.0) || !std::isfinite(cfl)) return fail(MFC_EINVAL, "cfl must be > 0");
+    int st = mfc_max_wave_rate(c, q, d_scratch, stream);
+    if (st) return st;
+    double rate = 0.0;
+    CU_TRY(cudaMemcpyAsync(&rate, d_scratch, sizeof(double), cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream));
+    CU_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    if (!(rate > 0.0) || !std::isfinite(rate))
+        return fail(MFC_ESTATE, "wave rate %g is not positive and finite", rate);
+    *dt_out = cfl / rate;
+    return MFC_OK;
+}
+
 int mfc_prim_to_cons(mfc_ctx* c, const double* v, double* q, void* stream) {
     return eos(c, v, q, true, stream);
 }

@@ -24,6 +24,46 @@ __global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons)
     }
 }
 
+// CFL wave rate: max over interior cells of max_k (|u_k| + c)/dx_k (AMB-25).
+// Block max in shared memory, one atomicMax per block on the bit pattern of the
+// (non-negative) double, which orders like an unsigned integer.
+template <class M>
+__global__ void __launch_bounds__(256) wave_rate_kernel(const EosArgs a, double3 inv_dx,
+                                                        unsigned long long* out) {
+    __shared__ double red[256];
+    const int64_t n = (int64_t)a.nx * a.ny * a.nz;
+    double m = 0.0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % a.nx);
+        const int j = (int)((t / a.nx) % a.ny);
+        const int k = (int)(t / ((int64_t)a.nx * a.ny));
+        const int64_t c = a.base + (int64_t)k * a.sZ + (int64_t)j * a.sY + i;
+        double x[M::E], v[M::E];
+#pragma unroll
+        for (int e = 0; e < M::E; ++e) x[e] = a.in[c + e * a.sE];
+        cons_to_prim_fast<M>(x, v, a.mat);
+        double rho = v[0], G = v[M::IA] * a.mat.Gam[0], P = v[M::IA] * a.mat.Pi[0];
+#pragma unroll
+        for (int f = 1; f < M::N; ++f) {
+            rho += v[f];
+            G = fma(v[M::IA + f], a.mat.Gam[f], G);
+            P = fma(v[M::IA + f], a.mat.Pi[f], P);
+        }
+        const double cs = sqrt(fma(G + 1.0, v[M::IE], P) / (rho * G));
+        const double idx[3] = {inv_dx.x, inv_dx.y, inv_dx.z};
+#pragma unroll
+        for (int d = 0; d < M::D; ++d) m = fmax(m, (fabs(v[M::IM + d]) + cs) * idx[d]);
+    }
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(red[0]));
+}
+
 template <class M, int DIR, int MODE>
 static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     constexpr int NTH = sweep_nth<M, MODE>();
@@ -90,6 +130,21 @@ cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int mode, const SweepArgs& a, d
         case 3: return launch_model<MFC_NF, 3>(DIR, mode, a, g, b, s);
     }
     return cudaErrorInvalidValue;
+}
+
+template <>
+cudaError_t launch_wave_rate<MFC_NF>(int D, const EosArgs& a, double3 inv_dx, double* out,
+                                     cudaStream_t s) {
+    const int64_t n = (int64_t)a.nx * a.ny * a.nz;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    auto* o = reinterpret_cast<unsigned long long*>(out);
+    switch (D) {
+        case 1: wave_rate_kernel<Model<MFC_NF, 1>><<<blocks, 256, 0, s>>>(a, inv_dx, o); break;
+        case 2: wave_rate_kernel<Model<MFC_NF, 2>><<<blocks, 256, 0, s>>>(a, inv_dx, o); break;
+        case 3: wave_rate_kernel<Model<MFC_NF, 3>><<<blocks, 256, 0, s>>>(a, inv_dx, o); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 template <>

@@ -27,7 +27,7 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ES
 EXPORTED = [
     "mfc_init", "mfc_get_layout", "mfc_get_neighbors", "mfc_bind_workspace", "mfc_set_weno_eps",
     "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
-    "mfc_rk3_steps",
+    "mfc_rk3_steps", "mfc_max_wave_rate", "mfc_cfl_dt",
     "mfc_advance_host", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
     "mfc_nccl_get_unique_id", "mfc_last_launch_count", "mfc_profile_enable", "mfc_profile_read", "mfc_finalize", "mfc_last_error",
     "mfc_version",
@@ -77,6 +77,8 @@ def _load():
         "mfc_rhs": [vp, vp, vp, vp],
         "mfc_rk3_step": [vp, vp, dbl, vp],
         "mfc_rk3_steps": [vp, vp, dbl, i64, vp],
+        "mfc_max_wave_rate": [vp, vp, vp, vp],
+        "mfc_cfl_dt": [vp, vp, dbl, ctypes.POINTER(dbl), vp, vp],
         "mfc_advance_host": [vp, vp, vp, vp, i64, dbl, vp],
         "mfc_halo_exchange_group": [pp, pp, i32, vp],
         "mfc_rhs_group": [pp, pp, pp, i32, vp],
@@ -240,6 +242,22 @@ class Solver:
 
     def rk3_step(self, q, dt: float, stream=None):
         _check(lib.mfc_rk3_step(self._h, _ptr(q), float(dt), _stream(stream)), "mfc_rk3_step")
+
+    def max_wave_rate(self, q, out=None, stream=None) -> torch.Tensor:
+        """Device scalar: max over cells (and ranks) of max_k (|u_k|+c)/dx_k."""
+        if out is None:
+            out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        _check(lib.mfc_max_wave_rate(self._h, _ptr(q), _ptr(out), _stream(stream)),
+               "mfc_max_wave_rate")
+        return out
+
+    def cfl_dt(self, q, cfl: float, stream=None) -> float:
+        """dt = cfl / max_wave_rate (synchronises the stream)."""
+        scratch = torch.zeros(1, dtype=torch.float64, device=self.device)
+        dt = ctypes.c_double(0.0)
+        _check(lib.mfc_cfl_dt(self._h, _ptr(q), float(cfl), ctypes.byref(dt), _ptr(scratch),
+                              _stream(stream)), "mfc_cfl_dt")
+        return dt.value
 
     def rk3_steps(self, q, dt: float, nsteps: int, stream=None):
         """nsteps RK3 steps replayed from a CUDA graph of one step."""

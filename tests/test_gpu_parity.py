@@ -168,3 +168,19 @@ def test_graph_steps_bitwise_equal_to_single_steps(make):
     s.rk3_step(b, dt * 0.5)
     torch.cuda.synchronize()
     assert torch.isfinite(s.interior(c)).all()
+
+
+@pytest.mark.parametrize("make", [lambda: W.c3_droplet(24), lambda: W.random_problem(2, (40, 33), 3, "water"),
+                                  lambda: W.c1_water_air()])
+def test_max_wave_rate_and_cfl_dt(make):
+    """F3 (adaptive dt): device max of max_k (|u_k|+c)/dx_k equals the oracle's."""
+    pb = make()
+    P, v, q = oracle_inputs(pb)
+    ref = O.max_wave_rate(P, q)
+    s = gpu_solver(pb)
+    qd = s.state_from_cons(q)
+    got = s.max_wave_rate(qd).item()
+    record("max wave rate " + pb.name, abs(got - ref) / ref, 1e-14)
+    assert got == pytest.approx(ref, rel=1e-14)
+    dt = s.cfl_dt(qd, 0.4)
+    assert dt == pytest.approx(0.4 / ref, rel=1e-14)

@@ -200,3 +200,16 @@ def test_rk3_third_order_in_time():
     errs = [np.abs(run(m) - fine).max() for m in (8, 16, 32)]
     orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert orders.min() > 2.8, orders
+
+
+def test_max_wave_rate_closed_form():
+    """Uniform single stiffened gas: rate = max_k (|u_k| + sqrt(gamma (p + pi_inf)/rho))/dx_k."""
+    for gam, pinf, rho, p in ((1.4, 0.0, 1.2, 1e5), (4.4, 6e8, 1000.0, 1e5)):
+        pb = W.Problem("uni", 1, 3, (6, 5, 4), hi=(0.6, 1.0, 0.2), gamma=(gam,), pi_inf=(pinf,))
+        u = (3.0, -250.0, 40.0)
+        v = np.stack([np.full(pb.shape[1:], x) for x in (rho, *u, p, 1.0)])
+        P = _oprob(pb)
+        rate = O.max_wave_rate(P, _cons(pb, v))
+        c = np.sqrt(gam * (p + pinf) / rho)
+        ref = max((abs(u[k]) + c) / pb.dx[k] for k in range(3))
+        assert rate == pytest.approx(ref, rel=1e-14)

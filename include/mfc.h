@@ -127,6 +127,11 @@ int mfc_bind_workspace(mfc_ctx* ctx, void* dev_ptr, size_t bytes);
  * must be in [1e-40, 1e-2]. */
 int mfc_set_weno_eps(mfc_ctx* ctx, double eps);
 
+/* Reconstruction order: 5 (WENO5-JS, default) or 3 (WENO3-JS), the two options of
+ * P:84 ("third or fifth-order accurate WENO reconstructions").
+ * The ghost depth stays 3; WENO3 reads the inner two layers. */
+int mfc_set_weno_order(mfc_ctx* ctx, int32_t order);
+
 /* Primitive <-> conserved conversion on the interior cells of padded device
  * buffers (same layout for v and q; may not alias).  prim_to_cons evaluates
  * rhoE = (Gamma p + Pi) + KE, cons_to_prim the inverse in the order of DESIGN.md

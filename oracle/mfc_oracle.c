@@ -201,6 +201,40 @@ double orc_weno5_plus(double a, double b, double c, double d, double e, double e
     return weno5_combine(beta, dk, p, eps, weights);
 }
 
+/* WENO3-JS: candidates from the 2-cell stencils {m-1,m} and {m,m+1},
+ *   v^-_{m+1/2}: p0 = (-a+3b)/2, p1 = (b+c)/2, d = (1/3, 2/3)
+ *   v^+_{m-1/2}: p0 = (a+b)/2,   p1 = (3b-c)/2, d = (2/3, 1/3)
+ *   beta0 = (b-a)^2, beta1 = (c-b)^2, alpha_k = d_k/(beta_k+eps)^2. */
+static double weno3_combine(const double beta[2], const double dk[2], const double p[2],
+                            double eps, double* weights) {
+    double alpha[2];
+    for (int k = 0; k < 2; ++k) {
+        const double s = beta[k] + eps;
+        alpha[k] = dk[k] / (s * s);
+    }
+    const double sum = alpha[0] + alpha[1];
+    const double w0 = alpha[0] / sum, w1 = alpha[1] / sum;
+    if (weights) {
+        weights[0] = w0;
+        weights[1] = w1;
+    }
+    return w0 * p[0] + w1 * p[1];
+}
+
+double orc_weno3_minus(double a, double b, double c, double eps, double* weights) {
+    const double beta[2] = {(b - a) * (b - a), (c - b) * (c - b)};
+    const double dk[2] = {1.0 / 3.0, 2.0 / 3.0};
+    const double p[2] = {(-a + 3.0 * b) / 2.0, (b + c) / 2.0};
+    return weno3_combine(beta, dk, p, eps, weights);
+}
+
+double orc_weno3_plus(double a, double b, double c, double eps, double* weights) {
+    const double beta[2] = {(b - a) * (b - a), (c - b) * (c - b)};
+    const double dk[2] = {2.0 / 3.0, 1.0 / 3.0};
+    const double p[2] = {(a + b) / 2.0, (3.0 * b - c) / 2.0};
+    return weno3_combine(beta, dk, p, eps, weights);
+}
+
 /* ---------------------------------------------------------------- S3 HLLC */
 
 typedef struct {
@@ -286,16 +320,22 @@ void orc_hllc(const orc_problem* P, const double* Gam, const double* Pi, int32_t
 }
 
 /* Face m+½ from the primitive window w = cells m−2..m+3 ([6][E], AoS):
- * v_L = v⁻ from cell m (cells m−2..m+2), v_R = v⁺ from cell m+1 (m−1..m+3). */
+ * v_L = v⁻ from cell m (cells m−2..m+2), v_R = v⁺ from cell m+1 (m−1..m+3);
+ * WENO3 uses the inner cells m−1..m+1 and m..m+2. */
 static void face_flux(const orc_problem* P, const double* Gam, const double* Pi, int dir,
                       const double* w, double* F, double* uf) {
     const int E = orc_num_eq(P->N, P->d);
     double vL[ORC_MAXE], vR[ORC_MAXE];
     for (int e = 0; e < E; ++e) {
-        vL[e] = orc_weno5_minus(w[0 * E + e], w[1 * E + e], w[2 * E + e], w[3 * E + e],
-                                w[4 * E + e], P->eps, NULL);
-        vR[e] = orc_weno5_plus(w[1 * E + e], w[2 * E + e], w[3 * E + e], w[4 * E + e],
-                               w[5 * E + e], P->eps, NULL);
+        if (P->weno_order == 3) {
+            vL[e] = orc_weno3_minus(w[1 * E + e], w[2 * E + e], w[3 * E + e], P->eps, NULL);
+            vR[e] = orc_weno3_plus(w[2 * E + e], w[3 * E + e], w[4 * E + e], P->eps, NULL);
+        } else {
+            vL[e] = orc_weno5_minus(w[0 * E + e], w[1 * E + e], w[2 * E + e], w[3 * E + e],
+                                    w[4 * E + e], P->eps, NULL);
+            vR[e] = orc_weno5_plus(w[1 * E + e], w[2 * E + e], w[3 * E + e], w[4 * E + e],
+                                   w[5 * E + e], P->eps, NULL);
+        }
     }
     orc_hllc(P, Gam, Pi, dir, vL, vR, F, uf);
 }

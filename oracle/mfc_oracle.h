@@ -43,6 +43,7 @@ typedef struct {
     double gamma[ORC_MAXF];     /* stiffened-gas gamma_i > 1 */
     double pi_inf[ORC_MAXF];    /* stiffened-gas pi_inf_i >= 0 */
     double eps;                 /* WENO epsilon (AMB-8), default 1e-16 */
+    int32_t weno_order;         /* 5 (WENO5-JS, default) or 3 (WENO3-JS) */
 } orc_problem;
 
 #ifdef __cplusplus
@@ -73,6 +74,12 @@ double orc_weno5_minus(double a, double b, double c, double d, double e, double 
                        double* weights);
 double orc_weno5_plus(double a, double b, double c, double d, double e, double eps,
                       double* weights);
+
+/* WENO3-JS ("third or fifth-order accurate WENO", Shu [15]) from a..c =
+ * v_{m-1..m+1}: minus -> v^-_{m+1/2} (linear weights 1/3 on stencil {m-1,m},
+ * 2/3 on {m,m+1}), plus -> v^+_{m-1/2} (2/3, 1/3); beta = squared differences. */
+double orc_weno3_minus(double a, double b, double c, double eps, double* weights);
+double orc_weno3_plus(double a, double b, double c, double eps, double* weights);
 
 /* S3 HLLC (Toro [14] ch. 10) in the compact branch form of DESIGN.md §3.
  * dir = 0,1,2 selects the normal velocity.  F[E] gets the flux, *uf the face

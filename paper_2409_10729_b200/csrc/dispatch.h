@@ -10,8 +10,8 @@ namespace mfc {
 // Launch the sweep kernel for N fluids, D dims, direction DIR with epilogue `mode`
 // (M_SET / M_RKINIT for DIR == 0, M_ACC for DIR > 0).
 template <int N>
-cudaError_t launch_sweep(int D, int DIR, int mode, const SweepArgs& a, dim3 grid, dim3 block,
-                         cudaStream_t s);
+cudaError_t launch_sweep(int D, int DIR, int mode, int order, const SweepArgs& a, dim3 grid,
+                         dim3 block, cudaStream_t s);
 
 struct EosArgs {
     const double* in;

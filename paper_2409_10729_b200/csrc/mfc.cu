@@ -73,6 +73,7 @@ struct mfc_ctx {
     int nbr[6] = {-1, -1, -1, -1, -1, -1};
     Materials mat{};
     double eps = 1e-16;
+    int weno_order = 5;
     int rank = 0, nranks = 1, procs[3] = {1, 1, 1}, coords[3] = {0, 0, 0};
     bool loopback = false;
     ncclComm_t comm = nullptr;
@@ -394,6 +395,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     }
     a.invd = 1.0 / c->dx[dir];
     a.eps4 = 4.0 * c->eps;
+    a.eps = c->eps;
     a.w = w;
     a.ca = ca;
     a.cb = cb;
@@ -409,9 +411,9 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     cudaError_t e;
     ProfScope ps(c, s, K_SWEEP_X + dir);
     switch (c->N) {
-        case 1: e = launch_sweep<1>(c->D, dir, mode, a, grid, block, s); break;
-        case 2: e = launch_sweep<2>(c->D, dir, mode, a, grid, block, s); break;
-        case 3: e = launch_sweep<3>(c->D, dir, mode, a, grid, block, s); break;
+        case 1: e = launch_sweep<1>(c->D, dir, mode, c->weno_order, a, grid, block, s); break;
+        case 2: e = launch_sweep<2>(c->D, dir, mode, c->weno_order, a, grid, block, s); break;
+        case 3: e = launch_sweep<3>(c->D, dir, mode, c->weno_order, a, grid, block, s); break;
         default: return fail(MFC_EINVAL, "bad N");
     }
     if (e != cudaSuccess) return fail(MFC_ECUDA, "sweep launch: %s", cudaGetErrorString(e));
@@ -680,10 +682,25 @@ int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
     return MFC_OK;
 }
 
+int mfc_set_weno_order(mfc_ctx* c, int32_t order) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (order != 3 && order != 5) return fail(MFC_EINVAL, "WENO order must be 3 or 5");
+    c->weno_order = order;
+    if (c->graph) {                  // captured kernels depend on the order
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return MFC_OK;
+}
+
 int mfc_set_weno_eps(mfc_ctx* c, double eps) {
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     if (!(eps >= 1e-40 && eps <= 1e-2)) return fail(MFC_EINVAL, "eps out of [1e-40, 1e-2]");
     c->eps = eps;
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
     return MFC_OK;
 }
 

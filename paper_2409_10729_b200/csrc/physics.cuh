@@ -189,6 +189,22 @@ __device__ __forceinline__ void weno5(double a, double b, double c, double d, do
     vp = fma(Np, rcp(Dp), c);
 }
 
+// WENO3-JS ("third or fifth-order"; F2) for one variable of cell m from
+// a..c = v_{m-1..m+1}, in first differences D0 = b-a, D1 = c-b:
+//   beta = (D0^2, D1^2), alpha_k ~ d_k/(beta_k+eps)^2 multiplied through by t0 t1,
+//   v- = b + (d0 t1 D0/2 + d1 t0 D1/2)/(d0 t1 + d1 t0),  d = (1/3, 2/3)
+//   v+ = b - (e0 t1 D0/2 + e1 t0 D1/2)/(e0 t1 + e1 t0),  e = (2/3, 1/3)
+__device__ __forceinline__ void weno3(double a, double b, double c, double eps, double& vm,
+                                      double& vp) {
+    const double D0 = b - a, D1 = c - b;
+    double t0 = fma(D0, D0, eps); t0 *= t0;
+    double t1 = fma(D1, D1, eps); t1 *= t1;
+    const double wm0 = t1 * (1.0 / 3.0), wm1 = t0 * (2.0 / 3.0);
+    const double wp0 = t1 * (2.0 / 3.0), wp1 = t0 * (1.0 / 3.0);
+    vm = fma(0.5 * fma(wm1, D1, wm0 * D0), rcp(wm0 + wm1), b);
+    vp = fma(-0.5 * fma(wp1, D1, wp0 * D0), rcp(wp0 + wp1), b);
+}
+
 // HLLC face flux F[E] and face velocity uf for the normal direction DIR
 // from the reconstructed primitive states vL (cell m's v-) and vR (cell m+1's v+).
 template <class M, int DIR>

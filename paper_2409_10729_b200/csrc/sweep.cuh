@@ -39,6 +39,15 @@ namespace mfc {
 
 enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3 };
 
+// Reconstruction of one variable of the window's centre cell (ORD = 5: cells w0..w4,
+// ORD = 3: the inner three).
+template <int ORD>
+__device__ __forceinline__ void reconstruct(double w0, double w1, double w2, double w3, double w4,
+                                            double eps4, double eps, double& vm, double& vp) {
+    if constexpr (ORD == 5) weno5(w0, w1, w2, w3, w4, eps4, vm, vp);
+    else weno3(w1, w2, w3, eps, vm, vp);
+}
+
 constexpr int BC_GHOST = 1;  // ghost cells of this face are valid in memory (halo exchange)
 
 // Ghost cells of a physical boundary are never stored: a sweep reading cell s of its
@@ -76,6 +85,7 @@ struct SweepArgs {
     GhostMap gm;                    // boundary maps of the sweep axis (see map_cell)
     double invd;                    // 1/dx along DIR
     double eps4;                    // 4 x WENO epsilon (weno5 works with beta' = 4 beta)
+    double eps;                     // WENO epsilon (weno3)
     double w, ca, cb;               // epilogue weights
     Materials mat;
 };
@@ -118,7 +128,7 @@ __host__ __device__ constexpr int sweep_min_blocks() {
     return ((MODE == M_ACC || MODE == M_SET) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
-template <class M, int DIR, int MODE>
+template <class M, int DIR, int MODE, int ORD>
 __global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, MODE>())
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
@@ -208,7 +218,7 @@ sweep_kernel(const SweepArgs a) {
         double vm[E], vp[E];
 #pragma unroll
         for (int e = 0; e < E; ++e)
-            weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, vm[e], vp[e]);
+            reconstruct<ORD>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, a.eps, vm[e], vp[e]);
 
         if (j >= s0) {
             double F[E], uf;
@@ -273,7 +283,7 @@ namespace mfc {
 
 __device__ __forceinline__ int swz(int row, int x) { return row * 4 + (x ^ ((row >> 2) & 3)); }
 
-template <class M>
+template <class M, int ORD>
 __global__ void __launch_bounds__(128, 2)
 sweep_x_staged(const SweepArgs a) {
     constexpr int E = M::E;
@@ -356,7 +366,7 @@ sweep_x_staged(const SweepArgs a) {
         double vm[E], vp[E];
 #pragma unroll
         for (int e = 0; e < E; ++e)
-            weno5(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, vm[e], vp[e]);
+            reconstruct<ORD>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, a.eps, vm[e], vp[e]);
         if (j >= s0) {
             double F[E], uf;
             hllc<M, 0>(vm_prev, vp, a.mat, F, uf);

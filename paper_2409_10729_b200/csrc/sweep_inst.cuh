@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) wave_rate_kernel(const EosArgs a, double3
     if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(red[0]));
 }
 
-template <class M, int DIR, int MODE>
+template <class M, int DIR, int MODE, int ORD>
 static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     constexpr int NTH = sweep_nth<M, MODE>();
     b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
@@ -72,14 +72,14 @@ static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     const size_t smem = sweep_smem_per_thread<M, MODE>() * NTH;
     static size_t attr = 0;
     if (smem > attr) {
-        cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE, ORD>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
-    sweep_kernel<M, DIR, MODE><<<g, b, smem, s>>>(a);
+    sweep_kernel<M, DIR, MODE, ORD><<<g, b, smem, s>>>(a);
 }
 
-template <class M, int DIR>
+template <class M, int DIR, int ORD>
 static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     if constexpr (DIR == 0) {
         if (mode == M_SET) {
@@ -88,48 +88,55 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                 const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
                 static size_t attr = 0;
                 if (smem > attr) {
-                    cudaFuncSetAttribute(sweep_x_staged<M>,
+                    cudaFuncSetAttribute(sweep_x_staged<M, ORD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     attr = smem;
                 }
-                sweep_x_staged<M><<<g, b, smem, s>>>(a);
+                sweep_x_staged<M, ORD><<<g, b, smem, s>>>(a);
             } else {
-                launch_ring<M, DIR, M_SET>(a, g, b, s);
+                launch_ring<M, DIR, M_SET, ORD>(a, g, b, s);
             }
         } else if (mode == M_RKINIT && M::D == 1) {
-            launch_ring<M, DIR, M_RKINIT>(a, g, b, s);
+            launch_ring<M, DIR, M_RKINIT, ORD>(a, g, b, s);
         } else {
             return cudaErrorInvalidValue;
         }
     } else {
-        if (mode == M_ACC) launch_ring<M, DIR, M_ACC>(a, g, b, s);
-        else if (DIR == 1 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC>(a, g, b, s);
+        if (mode == M_ACC) launch_ring<M, DIR, M_ACC, ORD>(a, g, b, s);
+        else if (DIR == 1 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
         else return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
-template <int NF, int ND>
+template <int NF, int ND, int ORD>
 static cudaError_t launch_model(int DIR, int mode, const SweepArgs& a, dim3 g, dim3 b,
                                 cudaStream_t s) {
     using M = Model<NF, ND>;
     switch (DIR) {
-        case 0: return launch_dir<M, 0>(mode, a, g, b, s);
-        case 1: if constexpr (ND > 1) return launch_dir<M, 1>(mode, a, g, b, s); break;
-        case 2: if constexpr (ND > 2) return launch_dir<M, 2>(mode, a, g, b, s); break;
+        case 0: return launch_dir<M, 0, ORD>(mode, a, g, b, s);
+        case 1: if constexpr (ND > 1) return launch_dir<M, 1, ORD>(mode, a, g, b, s); break;
+        case 2: if constexpr (ND > 2) return launch_dir<M, 2, ORD>(mode, a, g, b, s); break;
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int ORD>
+static cudaError_t launch_order(int D, int DIR, int mode, const SweepArgs& a, dim3 g, dim3 b,
+                                cudaStream_t s) {
+    switch (D) {
+        case 1: return launch_model<MFC_NF, 1, ORD>(DIR, mode, a, g, b, s);
+        case 2: return launch_model<MFC_NF, 2, ORD>(DIR, mode, a, g, b, s);
+        case 3: return launch_model<MFC_NF, 3, ORD>(DIR, mode, a, g, b, s);
     }
     return cudaErrorInvalidValue;
 }
 
 template <>
-cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int mode, const SweepArgs& a, dim3 g, dim3 b,
-                                 cudaStream_t s) {
-    switch (D) {
-        case 1: return launch_model<MFC_NF, 1>(DIR, mode, a, g, b, s);
-        case 2: return launch_model<MFC_NF, 2>(DIR, mode, a, g, b, s);
-        case 3: return launch_model<MFC_NF, 3>(DIR, mode, a, g, b, s);
-    }
-    return cudaErrorInvalidValue;
+cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int mode, int order, const SweepArgs& a, dim3 g,
+                                 dim3 b, cudaStream_t s) {
+    if (order == 3) return launch_order<3>(D, DIR, mode, a, g, b, s);
+    return launch_order<5>(D, DIR, mode, a, g, b, s);
 }
 
 template <>

@@ -58,6 +58,7 @@ class Problem:
     dt: float = 0.0               # a stable fixed time step for this workload
     steps: int = 0                # steps the config names (C1: 200)
     weno_eps: float = 1e-16
+    weno_order: int = 5           # 5 (default) or 3
     notes: dict = field(default_factory=dict)
 
     @property

@@ -184,3 +184,33 @@ def test_max_wave_rate_and_cfl_dt(make):
     assert got == pytest.approx(ref, rel=1e-14)
     dt = s.cfl_dt(qd, 0.4)
     assert dt == pytest.approx(0.4 / ref, rel=1e-14)
+
+
+def _weno3(pb):
+    pb.weno_order = 3
+    return pb
+
+
+WENO3_CASES = [
+    ("C1-w3", lambda: _weno3(W.c1_water_air())),
+    ("C3-32-w3", lambda: _weno3(W.c3_droplet(32))),
+    ("GR-2D-N3-w3", lambda: _weno3(W.random_problem(2, (45, 38), 3, "water"))),
+    ("GR-3D-N2-w3", lambda: _weno3(W.random_problem(3, (35, 22, 27), 2, "gas"))),
+]
+
+
+@pytest.mark.parametrize("name,make", WENO3_CASES, ids=[c[0] for c in WENO3_CASES])
+def test_weno3_rhs_parity(name, make):
+    """F2: the WENO3 option through the same sweeps, against the oracle's WENO3."""
+    _rhs_case(make())
+
+
+def test_weno3_100_steps_parity():
+    pb = _weno3(W.c3_droplet(24))
+    P, v, q = oracle_inputs(pb)
+    ref = O.rk3_step(P, q, pb.dt, nsteps=100)
+    got = gpu_steps(pb, q, pb.dt, 100)
+    err = rel_err(got, ref)
+    tol = np.maximum(STEP100_TOL, 3.0 * oracle_sensitivity(P, q, pb.dt, 100, ref))
+    record("100 RK3 steps C3-24 WENO3", err, tol)
+    assert np.all(err <= tol), err

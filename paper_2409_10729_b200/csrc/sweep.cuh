@@ -196,7 +196,7 @@ sweep_kernel(const SweepArgs a) {
     // end of step j), q^s (cell j-1), operands of cell j-1 (refilled for cell j+1)
     int kq = (s0 + 4) % R::QS;
     int kqf = (s0 + 6) % R::QS;
-    int kqs = (s0 + 1) % R::QS;
+    int kqs = (s0 + 2) % R::QS;
     int ka = (s0 + 2) & 1;
 
     double vm_prev[E];     // v-_{j-1/2} (from cell j-1)

@@ -96,17 +96,11 @@ struct SweepArgs {
 //   state ring : cells j+2 .. j+4 (RK y sweep: j-1 .. j+4, the stage operand q^s(j-1)
 //                is the state already streamed three steps earlier);
 //   acc / q^n rings : cells j-1 .. j+1.
-// Per-thread shared-memory rings for the streamed operands, refilled by cp.async at
-// the END of each march step for the step after next (element (slot, e) of thread t at
-// [(slot*E + e)*nthreads + t], so a warp's copies and reads are contiguous rows):
-//   state ring : cells j+2 .. j+4 (RK y sweep: j-1 .. j+3, the stage operand q^s(j-1)
-//                is the state already streamed three steps earlier);
-//   acc / q^n rings : cells j-1, j.
 template <int MODE>
 struct Rings {
-    static constexpr int QS = (MODE == M_RKACC || MODE == M_RKINIT) ? 5 : 3;
-    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC) ? 2 : 0;
-    static constexpr int NS = (MODE == M_RKACC || MODE == M_RKINIT) ? 2 : 0;
+    static constexpr int QS = (MODE == M_RKACC || MODE == M_RKINIT) ? 6 : 3;
+    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC) ? 3 : 0;
+    static constexpr int NS = (MODE == M_RKACC || MODE == M_RKINIT) ? 3 : 0;
     static constexpr int SLOTS = QS + AS + NS;
 };
 
@@ -127,10 +121,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-// 3 resident blocks (12 warps/SM, <= 168 registers) for E <= 8; 2 blocks otherwise.
+// 3 resident blocks (12 warps/SM, <= 168 registers) where that does not spill (the
+// non-RK modes for E <= 8); 2 blocks otherwise.
 template <class M, int MODE>
 __host__ __device__ constexpr int sweep_min_blocks() {
-    return (M::E <= 8) ? MFC_ACC_MINB : 2;
+    return ((MODE == M_ACC || MODE == M_SET) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
 template <class M, int DIR, int MODE, int ORD>
@@ -161,7 +156,7 @@ sweep_kernel(const SweepArgs a) {
         for (int e = 0; e < E; ++e) cp_async8(&at(ring, slot, e), p + e * a.sE);
     };
     // group for step j: state of cell j+2 -> state slot sq, epilogue operands of cell
-    // j-1 -> operand slot sa.  Slots: state cell c at (c+3) % QS, operands at c % 2.
+    // j-1 -> operand slot sa.  Slots: state cell c at (c+3) % QS, operands at (c+3) % 3.
     auto issue = [&](int j, int sq, int sa) {
         if (j + 2 <= s1 + 2) fetch(ringQ, sq, q, j + 2);
         const int c = j - 1;
@@ -183,21 +178,22 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
             for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
             if (map_flip(s0 - 4 + k, a.nS, a.gm)) qc[M::IM + DIR] = -qc[M::IM + DIR];
-            if (R::QS == 5 && k >= 2) {               // cells s0-2.. s0: q^s epilogue operands
+            if (R::QS == 6) {                         // keep for the q^s epilogue operand
 #pragma unroll
                 for (int e = 0; e < E; ++e) at(ringQ, (s0 - 4 + k + 3) % R::QS, e) = qc[e];
             }
             cons_to_prim_fast<M>(qc, w[k], a.mat);
         }
     }
-    issue(s0 - 1, (s0 + 4) % R::QS, (s0 + 2) & 1);
-    issue(s0, (s0 + 5) % R::QS, (s0 + 1) & 1);
-    // rotating slots at step j: conversion (cell j+2), refill (cell j+4, issued at the
-    // end of step j), q^s (cell j-1), operands of cell j-1 (refilled for cell j+1)
+    issue(s0 - 1, (s0 + 4) % R::QS, (s0 + 1) % 3);
+    issue(s0, (s0 + 5) % R::QS, (s0 + 2) % 3);
+    // rotating slots at step j: conversion (cell j+2), fetch (cell j+4), q^s (cell j-1),
+    // operands of cell j-1, operand fetch (cell j+1)
     int kq = (s0 + 4) % R::QS;
     int kqf = (s0 + 6) % R::QS;
-    int kqs = (s0 + 2) % R::QS;
-    int ka = (s0 + 2) & 1;
+    int kqs = (s0 + 1) % R::QS;
+    int ka = (s0 + 1) % 3;
+    int kaf = (s0 + 3) % 3;
 
     double vm_prev[E];     // v-_{j-1/2} (from cell j-1)
     double F_prev[E];      // flux at face j-3/2
@@ -205,6 +201,7 @@ sweep_kernel(const SweepArgs a) {
 
     for (int j = s0 - 1; j <= s1; ++j) {
         cp_async_wait_1();                             // group of step j has landed
+        issue(j + 2, kqf, kaf);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
 #pragma unroll
@@ -256,11 +253,11 @@ sweep_kernel(const SweepArgs a) {
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
-        issue(j + 2, kqf, ka);                         // refill: cell j+4, operands of j+1
         kq = inc(kq, R::QS);
         kqf = inc(kqf, R::QS);
         kqs = inc(kqs, R::QS);
-        ka ^= 1;
+        ka = inc(ka, 3);
+        kaf = inc(kaf, 3);
     }
     cp_async_wait_all();
 }

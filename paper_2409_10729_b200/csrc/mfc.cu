@@ -94,6 +94,9 @@ struct mfc_ctx {
     struct Rec { int kind; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     size_t ev_used = 0;
+    // halo exchange overlapped with the sweeps that do not read the exchanged ghosts
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     // CUDA graph of one RK3 step (mfc_rk3_steps), keyed on the state pointer and dt
     cudaGraphExec_t graph = nullptr;
     cudaStream_t cap_stream = nullptr;
@@ -426,9 +429,16 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
 //   rk == true : dst = ca*qn + cb*(q + dt*(c_x + c_y + c_z)), accumulating in acc:
 //     1D: x = M_RKINIT -> dst;  2D/3D: x = M_SET -> acc, y = M_RKACC, z = M_ACC.
 int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const double* qn,
-           double dt, double ca, double cb, cudaStream_t s) {
+           double dt, double ca, double cb, cudaStream_t s, cudaEvent_t halo = nullptr) {
     const double w = rk ? cb * dt : 1.0;
+    bool waited = false;
     for (int dir = 0; dir < c->D; ++dir) {
+        // only a sweep along a split dimension reads exchanged ghost layers: it (and
+        // everything after it on the stream) waits for the comm stream's halo event
+        if (halo && !waited && (c->bc[2 * dir] == BC_NEIGHBOR || c->bc[2 * dir + 1] == BC_NEIGHBOR)) {
+            CU_TRY(cudaStreamWaitEvent(s, halo, 0));
+            waited = true;
+        }
         const bool last = dir == c->D - 1;
         double* out = last ? dst : acc;
         int mode;
@@ -449,6 +459,28 @@ int check_ptr(const void* p, const char* name) {
     return MFC_OK;
 }
 
+// Start the halo exchange of the stage states `in` on the comm stream of cs[0], forked
+// from stream s; returns the event the sweeps along split dimensions wait on (nullptr
+// when no rank has a neighbour).  With z-slabs the x and y sweeps run meanwhile.
+int halo_async(mfc_ctx* const* cs, double* const* in, int count, cudaStream_t s,
+               cudaEvent_t* out) {
+    *out = nullptr;
+    bool any = false;
+    for (int r = 0; r < count; ++r) any = any || has_neighbors(cs[r]);
+    if (!any) return MFC_OK;
+    mfc_ctx* c0 = cs[0];
+    if (!c0->comm_stream) CU_TRY(cudaStreamCreateWithFlags(&c0->comm_stream, cudaStreamNonBlocking));
+    if (!c0->ev_ready) CU_TRY(cudaEventCreateWithFlags(&c0->ev_ready, cudaEventDisableTiming));
+    if (!c0->ev_halo) CU_TRY(cudaEventCreateWithFlags(&c0->ev_halo, cudaEventDisableTiming));
+    CU_TRY(cudaEventRecord(c0->ev_ready, s));
+    CU_TRY(cudaStreamWaitEvent(c0->comm_stream, c0->ev_ready, 0));
+    int st = exchange(cs, in, count, c0->comm_stream, false);
+    if (st) return st;
+    CU_TRY(cudaEventRecord(c0->ev_halo, c0->comm_stream));
+    *out = c0->ev_halo;
+    return MFC_OK;
+}
+
 int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaStream_t s) {
     static const double CA[3] = {0.0, 0.75, 1.0 / 3.0};
     static const double CB[3] = {1.0, 0.25, 2.0 / 3.0};
@@ -462,12 +494,14 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
     for (int stage = 0; stage < 3; ++stage) {
         for (int r = 0; r < count; ++r)
             in[r] = stage == 0 ? qs[r] : (stage == 1 ? cs[r]->S1 : cs[r]->S2);
-        int st = exchange(cs, in.data(), count, s, false);
+        cudaEvent_t halo = nullptr;
+        int st = halo_async(cs, in.data(), count, s, &halo);
         if (st) return st;
         for (int r = 0; r < count; ++r) {
             mfc_ctx* c = cs[r];
             double* out = stage == 0 ? c->S1 : (stage == 1 ? c->S2 : qs[r]);
-            if ((st = sweeps(c, in[r], c->acc, out, true, qs[r], dt, CA[stage], CB[stage], s)))
+            if ((st = sweeps(c, in[r], c->acc, out, true, qs[r], dt, CA[stage], CB[stage], s,
+                             halo)))
                 return st;
         }
     }
@@ -482,10 +516,11 @@ int rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int co
         if (qs[r] == rhss[r]) return fail(MFC_EINVAL, "q and rhs alias");
         cs[r]->launches = 0;
     }
-    int st = exchange(cs, qs, count, s, false);
+    cudaEvent_t halo = nullptr;
+    int st = halo_async(cs, qs, count, s, &halo);
     if (st) return st;
     for (int r = 0; r < count; ++r)
-        if ((st = sweeps(cs[r], qs[r], rhss[r], rhss[r], false, nullptr, 0, 0, 0, s)))
+        if ((st = sweeps(cs[r], qs[r], rhss[r], rhss[r], false, nullptr, 0, 0, 0, s, halo)))
             return st;
     return MFC_OK;
 }
@@ -941,6 +976,9 @@ int mfc_finalize(mfc_ctx* c) {
     if (!c) return MFC_OK;
     if (c->graph) cudaGraphExecDestroy(c->graph);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;

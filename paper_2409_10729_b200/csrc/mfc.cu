@@ -427,8 +427,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
 // One RHS evaluation of the stencil state q, assembled across the sweeps:
 //   rk == false: dst = c_x + c_y + c_z                    (acc == dst, the rhs buffer)
 //   rk == true : dst = ca*qn + cb*(q + dt*(c_x + c_y + c_z)), accumulating in acc:
-//     1D: x = M_RKINIT -> dst;  2D: x = M_SET -> acc, y = M_RKACC -> dst;
-//     3D: x = M_SET -> acc, y = M_ACCN (+ca*qn) -> acc, z = M_ACCQS (+cb*q^s) -> dst.
+//     1D: x = M_RKINIT -> dst;  2D/3D: x = M_SET -> acc, y = M_RKACC, z = M_ACC.
 int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const double* qn,
            double dt, double ca, double cb, cudaStream_t s, cudaEvent_t halo = nullptr) {
     const double w = rk ? cb * dt : 1.0;
@@ -444,9 +443,8 @@ int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const
         double* out = last ? dst : acc;
         int mode;
         if (dir == 0) mode = (rk && c->D == 1) ? M_RKINIT : M_SET;
-        else if (!rk) mode = M_ACC;
-        else if (c->D == 2) mode = M_RKACC;              // 2D: y is the last sweep
-        else mode = dir == 1 ? M_ACCN : M_ACCQS;         // 3D: split the stage operands
+        else if (dir == 1 && rk) mode = M_RKACC;
+        else mode = M_ACC;
         // M_SET in an RK stage writes the unscaled c_x; M_RKACC scales (acc + c_y) by w
         const double wd = (mode == M_SET) ? 1.0 : w;
         int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn, wd, ca, cb, s);

@@ -24,10 +24,6 @@
 //   M_RKINIT: dst = ca*q^n + cb*q^s + w*c             (1D: the only sweep, RK stage)
 //   M_RKACC : dst = ca*q^n + cb*q^s + w*(acc + c)     (y sweep, RK stage)
 //   M_ACC   : dst = acc + w*c                         (y sweep of a RHS, z sweep)
-//   M_ACCN  : dst = ca*q^n + w*(acc + c)              (3D RK: y sweep)
-//   M_ACCQS : dst = acc + cb*q^s + w*c                (3D RK: z sweep)
-// (3D RK stages use M_SET / M_ACCN / M_ACCQS so no kernel streams more than two
-//  operands; 2D RK stages use M_SET / M_RKACC.)
 // so the SSP-RK3 stage q^(s+1) = ca q^n + cb (q^s + dt (c_x + c_y + c_z)) (S4) is
 // assembled across the sweeps; the extra operands q^s, q^n are streamed by the y sweep,
 // whose warp accesses are contiguous rows, never by the x sweep, whose lanes own
@@ -41,7 +37,7 @@
 
 namespace mfc {
 
-enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3, M_ACCN = 4, M_ACCQS = 5 };
+enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3 };
 
 // Reconstruction of one variable of the window's centre cell (ORD = 5: cells w0..w4,
 // ORD = 3: the inner three).
@@ -102,13 +98,9 @@ struct SweepArgs {
 //   acc / q^n rings : cells j-1 .. j+1.
 template <int MODE>
 struct Rings {
-    static constexpr bool USE_QS = MODE == M_RKACC || MODE == M_RKINIT || MODE == M_ACCQS;
-    static constexpr bool USE_QN = MODE == M_RKACC || MODE == M_RKINIT || MODE == M_ACCN;
-    static constexpr bool USE_ACC = MODE == M_ACC || MODE == M_RKACC || MODE == M_ACCN ||
-                                    MODE == M_ACCQS;
-    static constexpr int QS = USE_QS ? 6 : 3;
-    static constexpr int AS = USE_ACC ? 3 : 0;
-    static constexpr int NS = USE_QN ? 3 : 0;
+    static constexpr int QS = (MODE == M_RKACC || MODE == M_RKINIT) ? 6 : 3;
+    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC) ? 3 : 0;
+    static constexpr int NS = (MODE == M_RKACC || MODE == M_RKINIT) ? 3 : 0;
     static constexpr int SLOTS = QS + AS + NS;
 };
 
@@ -133,8 +125,7 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 // non-RK modes for E <= 8); 2 blocks otherwise.
 template <class M, int MODE>
 __host__ __device__ constexpr int sweep_min_blocks() {
-    return ((MODE == M_ACC || MODE == M_SET || MODE == M_ACCN || MODE == M_ACCQS) && M::E <= 8)
-               ? MFC_ACC_MINB : 2;
+    return ((MODE == M_ACC || MODE == M_SET) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
 template <class M, int DIR, int MODE, int ORD>
@@ -187,7 +178,7 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
             for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
             if (map_flip(s0 - 4 + k, a.nS, a.gm)) qc[M::IM + DIR] = -qc[M::IM + DIR];
-            if (R::USE_QS) {                          // keep for the q^s epilogue operand
+            if (R::QS == 6) {                         // keep for the q^s epilogue operand
 #pragma unroll
                 for (int e = 0; e < E; ++e) at(ringQ, (s0 - 4 + k + 3) % R::QS, e) = qc[e];
             }
@@ -244,12 +235,7 @@ sweep_kernel(const SweepArgs a) {
                     double out;
                     if (MODE == M_SET) out = r * a.invd;
                     else if (MODE == M_ACC) out = fma(a.w * a.invd, r, at(ringA, ka, e));
-                    else if (MODE == M_ACCN) {
-                        const double t = a.w * fma(a.invd, r, at(ringA, ka, e));
-                        out = a.ca != 0.0 ? fma(a.ca, at(ringN, ka, e), t) : t;
-                    } else if (MODE == M_ACCQS) {
-                        out = fma(a.w * a.invd, r, fma(a.cb, at(ringQ, kqs, e), at(ringA, ka, e)));
-                    } else {
+                    else {
                         const double qs = at(ringQ, kqs, e);
                         const double base = a.ca != 0.0
                                                 ? fma(a.ca, at(ringN, ka, e), a.cb * qs)

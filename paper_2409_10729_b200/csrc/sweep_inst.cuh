@@ -103,9 +103,7 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
         }
     } else {
         if (mode == M_ACC) launch_ring<M, DIR, M_ACC, ORD>(a, g, b, s);
-        else if (DIR == 1 && M::D == 2 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
-        else if (DIR == 1 && M::D == 3 && mode == M_ACCN) launch_ring<M, DIR, M_ACCN, ORD>(a, g, b, s);
-        else if (DIR == 2 && mode == M_ACCQS) launch_ring<M, DIR, M_ACCQS, ORD>(a, g, b, s);
+        else if (DIR == 1 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
         else return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -121,3 +121,38 @@ def test_decomposition_bookkeeping(mfc, procs, periodic):
                     assert (L.lo_global[k] + L.n_local[k]) % pb.n[k] == Lo.lo_global[k]
                 else:
                     assert (Lo.lo_global[k] + Lo.n_local[k]) % pb.n[k] == L.lo_global[k]
+
+
+def test_new_entry_points_validate_arguments(mfc):
+    """mfc_set_weno_order / mfc_set_weno_eps / mfc_cfl_dt / mfc_rk3_steps reject bad
+    arguments before touching the GPU."""
+    pb = W.random_problem(3, (8, 8, 8), 2, "gas")
+    g = mfc._Grid()
+    g.ndim = 3
+    for k in range(3):
+        g.n_global[k], g.lo[k], g.hi[k], g.procs[k] = 8, 0.0, 1.0, 1
+    gam = (ctypes.c_double * 2)(1.4, 1.6)
+    pi = (ctypes.c_double * 2)(0.0, 0.0)
+    b = (ctypes.c_int32 * 6)(*pb.bc)
+    c = mfc._Comm()
+    c.rank, c.nranks, c.loopback = 0, 1, 0
+    h = ctypes.c_void_p()
+    assert mfc.lib.mfc_init(ctypes.byref(h), ctypes.byref(g), 2, gam, pi, b, ctypes.byref(c), 0) == 0
+    try:
+        assert mfc.lib.mfc_set_weno_order(h, 4) == -1
+        assert mfc.lib.mfc_set_weno_order(h, 3) == 0
+        assert mfc.lib.mfc_set_weno_order(h, 5) == 0
+        assert mfc.lib.mfc_set_weno_eps(h, 0.5) == -1
+        assert mfc.lib.mfc_set_weno_eps(h, 1e-16) == 0
+        dt = ctypes.c_double(0.0)
+        assert mfc.lib.mfc_cfl_dt(h, None, 0.4, ctypes.byref(dt), None, None) == -1
+        assert mfc.lib.mfc_rk3_steps(h, None, 1e-3, 1, None) != 0
+        assert mfc.lib.mfc_rk3_steps(h, None, float("nan"), 1, None) == -1
+        assert mfc.lib.mfc_rk3_step(h, None, 1e-3, None) != 0   # no workspace / NULL q
+    finally:
+        mfc.lib.mfc_finalize(h)
+
+
+def test_ndim_needs_three_cells(mfc):
+    rc, msg = _init(mfc, W.Problem("tiny", 2, 2, (8, 2, 1), gamma=(1.4, 1.4), pi_inf=(0, 0)))
+    assert rc == -1 and "< 3" in msg

@@ -88,6 +88,7 @@ struct mfc_ctx {
     int64_t face_elems[3] = {0, 0, 0};  // E * 3 * area of a face normal to dim k
     int64_t launches = 0;
     int seg = 0;  // sweep segment length override (0 = heuristic)
+    int seg_dir[3] = {0, 0, 0};  // per-direction overrides (MFC_SEG_X/Y/Z)
     // optional per-launch CUDA-event timing (mfc_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -346,15 +347,20 @@ int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
 
 // ------------------------------------------------------------------ sweeps
 
-int seg_len(const mfc_ctx* c, int dir) {
+// Segment length T of the marches.  Longer segments waste less on the (T+2)/T halo
+// recomputation; shorter ones give more warps.  Measured on C3 256^3 (profiles, T sweep
+// r25b): the best is the largest T <= 128 that still gives >= 3 waves of resident
+// warps (x, y: 128; z, with 3 resident blocks/SM, 64).
+int seg_len(const mfc_ctx* c, int dir, int resident_warps_per_sm) {
+    if (c->seg_dir[dir] > 0) return (int)std::min<int64_t>(c->seg_dir[dir], c->nl[dir]);
     if (c->seg > 0) return c->seg;
     const int t1 = dir == 0 ? 1 : 0;          // lane axis
-    const int t2 = dir == 2 ? 1 : (dir == 0 ? 2 : 2);
-    const int64_t lines = c->nl[t1] * c->nl[t2];
+    const int t2 = dir == 2 ? 1 : 2;          // third axis
+    const int64_t warp_lines = (c->nl[t1] + 31) / 32 * c->nl[t2];
     const int64_t n = c->nl[dir];
-    // aim for >= ~48k threads in flight, segments of 16..64 cells
-    int T = 64;
-    while (T > 16 && lines * ((n + T - 1) / T) < 49152) T /= 2;
+    const double resident = 148.0 * resident_warps_per_sm;
+    int T = 128;
+    while (T > 16 && (double)warp_lines * ((n + T - 1) / T) < 3.0 * resident) T /= 2;
     if (c->D == 1) T = (int)std::max<int64_t>(8, std::min<int64_t>(32, n / 8 + 1));
     // the staged x sweep (D >= 2) needs segments that are multiples of its 4-cell chunks
     if (dir == 0 && c->D >= 2) return std::max(4, (int)((std::min<int64_t>(T, n) + 3) / 4 * 4));
@@ -382,7 +388,9 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     a.nS = (int32_t)c->nl[dir];
     a.nA = (int32_t)c->nl[la];
     a.nB = (int32_t)c->nl[lb];
-    a.T = seg_len(c, dir);
+    // resident warps per SM: 12 for the non-RK ring sweeps with E <= 8 (3 blocks), else 8
+    const bool three = c->E <= 8 && dir > 0 && mode == M_ACC;
+    a.T = seg_len(c, dir, three ? 12 : 8);
     // physical faces are applied by index mapping inside the sweep; faces shared with
     // another rank read the ghost layers the halo exchange wrote
     {
@@ -643,6 +651,9 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
     }
     c->ws_need = need;
     if (const char* sg = getenv("MFC_SEG")) c->seg = atoi(sg);
+    const char* segenv[3] = {"MFC_SEG_X", "MFC_SEG_Y", "MFC_SEG_Z"};
+    for (int k = 0; k < 3; ++k)
+        if (const char* sg = getenv(segenv[k])) c->seg_dir[k] = atoi(sg);
 
     // The device is only touched here when NCCL needs it; single-domain and loopback
     // contexts are pure host bookkeeping until the first GPU call (so layouts can be

@@ -110,7 +110,7 @@ __device__ __forceinline__ void cons_to_prim_fast(const double (&q)[M::E], doubl
         v[i] = q[i];
         v[M::IA + i] = q[M::IA + i];
     }
-    v[M::IE] = ((q[M::IE] - 0.5 * ke) - P) * iG;
+    v[M::IE] = (fma(-0.5, ke, q[M::IE]) - P) * iG;
 }
 
 // Fast reciprocal square root: MUFU.RSQ64H seed y0 and one third-order correction
@@ -231,7 +231,9 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     const double sL = fmin(uL - cL, uR - cR);
     const double sR = fmax(uL + cL, uR + cR);
     const double aL = rL * (sL - uL), aR = rR * (sR - uR);
-    const double sS = (fma(aL, uL, pR - pL) - aR * uR) * rcp(aL - aR);
+    // (every multiply-add is an explicit fma: contraction must not depend on the
+    //  inlining site, so a face computed by two code paths is bitwise identical)
+    const double sS = fma(-aR, uR, fma(aL, uL, pR - pL)) * rcp(aL - aR);
 
     const bool left = sS >= 0.0;
     const double sK = left ? sL : sR;
@@ -247,7 +249,7 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     for (int e = 0; e < M::E; ++e) vK[e] = left ? vL[e] : vR[e];
 #pragma unroll
     for (int k = 0; k < M::D; ++k) uu = fma(vK[M::IM + k], vK[M::IM + k], uu);
-    const double EK = fma(GK, pK, PK) + 0.5 * (rK * uu);
+    const double EK = fma(0.5, rK * uu, fma(GK, pK, PK));
     const double dK = sK - uK;
     const double dS = sK - sS;
     const double rr = rcp(dK * dS);          // one reciprocal for xi and p_K/(s_K-u_K)

@@ -391,3 +391,179 @@ sweep_x_staged(const SweepArgs a) {
 }
 
 }  // namespace mfc
+
+namespace mfc {
+
+// ---------------------------------------------------------------------------
+// x sweep, row-parallel form (2D/3D, epilogue M_SET).
+//
+// A block owns a row segment of 32*W consecutive cells [x0, x1) of one (y, z) row;
+// warp w owns cells x0+32w .. x0+32w+31, lane l one cell.  Loads and stores are
+// contiguous along x.  Each lane converts its cell (S2); the WENO stencil
+// neighbours come from lanes l-2..l+2 by warp shuffles and, across warp borders,
+// from a small shared-memory table each warp fills with its two first / last cells.
+// Lane l computes the face x-1/2 (HLLC) from v-(x-1) (shuffle / shared memory) and its
+// own v+; the cell update takes F(x+1/2) from lane l+1.  No register window, no
+// transpose, every face computed once.  Segment ends: for a periodic row that fits
+// in one block the face at x = -1/2 IS the face at x = n-1/2 (shared through shared
+// memory); otherwise warp 0 reconstructs the two boundary cells x0-1 (v-) and x1
+// (v+) in one extra pass.  Cells of the last warp beyond the row end hold the
+// (boundary-mapped) ghost cells, which are the right stencil halo.
+// ---------------------------------------------------------------------------
+
+template <class M, int ORD>
+__global__ void __launch_bounds__(512, 1)
+sweep_x_rows(const SweepArgs a, int W) {
+    constexpr int E = M::E;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int seg = 32 * W;
+    const int x0 = blockIdx.x * seg;
+    const int n = a.nS;
+    const int x1 = min(x0 + seg, n);                 // cells x0 .. x1-1 are updated
+    const bool whole_periodic = (a.gm.blo == 1 && a.gm.alo == n) && x0 == 0 && x1 == n;
+    const int x = x0 + tid;                          // my cell (>= n: boundary-mapped ghost)
+    const int64_t row = a.base + (int64_t)blockIdx.y * a.sA + (int64_t)blockIdx.z * a.sB;
+
+    // shared tables (doubles):
+    //   halo [W+2][4][E]: slot w+1 = warp w's cells 0,1 (k=0,1) and 30,31 (k=2,3);
+    //                     slot 0 k=2,3 = cells x0-2, x0-1; slot W+1 k=0,1 = cells x0+seg, +1
+    //   vmL [W+1][E]: slot w+1 = v- of warp w's last cell; slot 0 = v-(x0-1)
+    //   Ff  [W+1][E+1]: slot w = F, u^f of warp w's first face (x0+32w-1/2); slot W =
+    //                   the face x0+seg-1/2 when the segment ends on a warp border
+    //   st  [2][5][E]: stencils of the two boundary cells (warp 0, lanes 0/1)
+    extern __shared__ double sm[];
+    double* halo = sm;
+    double* vmL = halo + (W + 2) * 4 * E;
+    double* Ff = vmL + (W + 1) * E;
+    auto H = [&](int slot, int k, int e) -> double& { return halo[(slot * 4 + k) * E + e]; };
+
+    auto load_prim = [&](int cell, double (&v)[E]) {
+        const int sc = map_cell(cell, n, a.gm);
+        const double* p = a.q + row + sc;
+        double qc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
+        if (map_flip(cell, n, a.gm)) qc[M::IM] = -qc[M::IM];
+        cons_to_prim_fast<M>(qc, v, a.mat);
+    };
+
+    // 1. my cell's primitives; publish the warp's border cells and the segment halo
+    double v[E];
+    load_prim(x, v);
+    if (lane < 2 || lane >= 30) {
+        const int k = lane < 2 ? lane : lane - 28;
+#pragma unroll
+        for (int e = 0; e < E; ++e) H(warp + 1, k, e) = v[e];
+    }
+    if ((warp == 0 || warp == W - 1) && lane < 2) {
+        double h[E];
+        const bool left = warp == 0;
+        load_prim(left ? x0 - 2 + lane : x0 + seg + lane, h);
+#pragma unroll
+        for (int e = 0; e < E; ++e) H(left ? 0 : W + 1, left ? 2 + lane : lane, e) = h[e];
+        if (W == 1 && lane < 2) {                    // one warp: it is also the last
+            load_prim(x0 + seg + lane, h);
+#pragma unroll
+            for (int e = 0; e < E; ++e) H(W + 1, lane, e) = h[e];
+        }
+    }
+    __syncthreads();
+
+    // 2. WENO of my cell from lanes l-2 .. l+2 (tables across warp borders)
+    double vm[E], vp[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        double m2 = __shfl_up_sync(0xffffffffu, v[e], 2);
+        double m1 = __shfl_up_sync(0xffffffffu, v[e], 1);
+        double p1 = __shfl_down_sync(0xffffffffu, v[e], 1);
+        double p2 = __shfl_down_sync(0xffffffffu, v[e], 2);
+        if (lane == 0) { m2 = H(warp, 2, e); m1 = H(warp, 3, e); }
+        if (lane == 1) m2 = H(warp, 3, e);
+        if (lane == 30) p2 = H(warp + 2, 0, e);
+        if (lane == 31) { p1 = H(warp + 2, 0, e); p2 = H(warp + 2, 1, e); }
+        reconstruct<ORD>(m2, m1, v[e], p1, p2, a.eps4, a.eps, vm[e], vp[e]);
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) vmL[(warp + 1) * E + e] = vm[e];
+    }
+    // v-(x0-1): for a whole periodic row it is v-(n-1) (same stencil values);
+    // otherwise warp 0 reconstructs the boundary cells x0-1 (lane 0) and x0+seg (lane 1)
+    if (whole_periodic && x == n - 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) vmL[e] = vm[e];
+    }
+    double bp[E];                                    // lane 1 of warp 0: v+(x0+seg)
+    const bool boundary_pass = !whole_periodic && warp == 0;
+    if (boundary_pass && lane < 2) {
+        // stencil of cell c through the shared table st[lane][5][E] (few registers)
+        const int c = lane == 0 ? x0 - 1 : x0 + seg;
+        double* st = Ff + (W + 1) * (E + 1) + lane * 5 * E;
+#pragma unroll 1
+        for (int k = 0; k < 5; ++k) {
+            double h[E];
+            load_prim(c - 2 + k, h);
+#pragma unroll
+            for (int e = 0; e < E; ++e) st[k * E + e] = h[e];
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            double bm;
+            reconstruct<ORD>(st[e], st[E + e], st[2 * E + e], st[3 * E + e], st[4 * E + e], a.eps4,
+                             a.eps, bm, bp[e]);
+            if (lane == 0) vmL[e] = bm;
+        }
+    }
+    __syncthreads();
+
+    // 3. face x-1/2 from v-(x-1) (lane l-1 / table) and my v+
+    double vL[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const double t = __shfl_up_sync(0xffffffffu, vm[e], 1);
+        vL[e] = lane == 0 ? vmL[warp * E + e] : t;
+    }
+    double F[E], uf;
+    hllc<M, 0>(vL, vp, a.mat, F, uf);
+    if (lane == 0) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) Ff[warp * (E + 1) + e] = F[e];
+        Ff[warp * (E + 1) + E] = uf;
+    }
+    // face x0+seg-1/2 (needed when the segment is full and not a whole periodic row)
+    if (boundary_pass && lane == 1) {
+        double vl[E], FB[E], ufB;
+#pragma unroll
+        for (int e = 0; e < E; ++e) vl[e] = vmL[W * E + e];
+        hllc<M, 0>(vl, bp, a.mat, FB, ufB);
+#pragma unroll
+        for (int e = 0; e < E; ++e) Ff[W * (E + 1) + e] = FB[e];
+        Ff[W * (E + 1) + E] = ufB;
+    }
+    __syncthreads();
+
+    // 4. F(x+1/2) from lane l+1, or for lane 31 the next warp's first face (for the
+    //    last warp: face 0 of a whole periodic row, else the boundary face)
+    double FR[E], ufR;
+    {
+        const int nxt = warp + 1 < W ? warp + 1 : (whole_periodic ? 0 : W);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double t = __shfl_down_sync(0xffffffffu, F[e], 1);
+            FR[e] = lane == 31 ? Ff[nxt * (E + 1) + e] : t;
+        }
+        const double t = __shfl_down_sync(0xffffffffu, uf, 1);
+        ufR = lane == 31 ? Ff[nxt * (E + 1) + E] : t;
+    }
+    if (x < x1) {
+        const double du = ufR - uf;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            double r = F[e] - FR[e];
+            if (e >= M::IA) r = fma(v[e], du, r);
+            a.dst[row + x + e * a.sE] = r * a.invd;
+        }
+    }
+}
+
+}  // namespace mfc

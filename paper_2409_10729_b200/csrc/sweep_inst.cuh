@@ -1,6 +1,8 @@
 // sweep_inst.cuh -- instantiates the sweep and EOS kernels for one fluid count N
 // (included by sweep_n{1,2,3}.cu with MFC_NF defined).
 #pragma once
+#include <cstdlib>
+
 #include "dispatch.h"
 
 namespace mfc {
@@ -84,6 +86,15 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
     if constexpr (DIR == 0) {
         if (mode == M_SET) {
             if constexpr (M::D >= 2) {
+              if (!getenv("MFC_X_STAGED")) {
+                // row-parallel x sweep: W warps per row segment, shared tables only
+                const int W = (int)std::min<int64_t>(16, (a.nS + 31) / 32);
+                const int nseg = (a.nS + 32 * W - 1) / (32 * W);
+                const size_t smem = sizeof(double) *
+                    ((size_t)(W + 2) * 4 * M::E + (size_t)(W + 1) * M::E +
+                     (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E);
+                sweep_x_rows<M, ORD><<<dim3(nseg, a.nA, a.nB), 32 * W, smem, s>>>(a, W);
+              } else {
                 // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
                 const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
                 static size_t attr = 0;
@@ -93,6 +104,7 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                     attr = smem;
                 }
                 sweep_x_staged<M, ORD><<<g, b, smem, s>>>(a);
+              }
             } else {
                 launch_ring<M, DIR, M_SET, ORD>(a, g, b, s);
             }

@@ -471,16 +471,25 @@ sweep_x_rows(const SweepArgs a, int W) {
 
     // 2. WENO of my cell from lanes l-2 .. l+2 (tables across warp borders)
     double vm[E], vp[E];
+    // branch-free: every lane reads lane-indexed table entries, selects apply them
+    //   lanes 0,1: m2 = prev warp's cell 30+lane, lane 0: m1 = prev warp's cell 31
+    //   lanes 30,31: p2 = next warp's cell lane-30, lane 31: p1 = next warp's cell 0
+    const double* hm2 = &H(warp, 2 + (lane & 1), 0);
+    const double* hm1 = &H(warp, 3, 0);
+    const double* hp2 = &H(warp + 2, lane & 1, 0);
+    const double* hp1 = &H(warp + 2, 0, 0);
+    const bool lo2 = lane < 2, lo1 = lane == 0, hi2 = lane >= 30, hi1 = lane == 31;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         double m2 = __shfl_up_sync(0xffffffffu, v[e], 2);
         double m1 = __shfl_up_sync(0xffffffffu, v[e], 1);
         double p1 = __shfl_down_sync(0xffffffffu, v[e], 1);
         double p2 = __shfl_down_sync(0xffffffffu, v[e], 2);
-        if (lane == 0) { m2 = H(warp, 2, e); m1 = H(warp, 3, e); }
-        if (lane == 1) m2 = H(warp, 3, e);
-        if (lane == 30) p2 = H(warp + 2, 0, e);
-        if (lane == 31) { p1 = H(warp + 2, 0, e); p2 = H(warp + 2, 1, e); }
+        const double tm2 = hm2[e], tm1 = hm1[e], tp2 = hp2[e], tp1 = hp1[e];
+        m2 = lo2 ? tm2 : m2;
+        m1 = lo1 ? tm1 : m1;
+        p2 = hi2 ? tp2 : p2;
+        p1 = hi1 ? tp1 : p1;
         reconstruct<ORD>(m2, m1, v[e], p1, p2, a.eps4, a.eps, vm[e], vp[e]);
     }
     if (lane == 31) {

@@ -433,19 +433,20 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
     //   Ff  [W+1][E+1]: slot w = F, u^f of warp w's first face (x0+32w-1/2); slot W =
     //                   the face x0+seg-1/2 when the segment ends on a warp border
     //   st  [2][5][E]: stencils of the two boundary cells (warp 0, lanes 0/1)
-    //   pre [2][E][nthr + 2]: conserved state of the next row, prefetched with cp.async
-    //                   (own cell at [tid]; the two segment-halo cells at [nthr], [nthr+1])
+    //   pre [2][E][nthr + 4]: conserved state of the next row, prefetched with cp.async
+    //                   (own cell at [tid]; left halo at [nthr+0,1], right at [nthr+2,3])
     extern __shared__ double sm[];
     double* halo = sm;
     double* vmL = halo + (W + 2) * 4 * E;
     double* Ff = vmL + (W + 1) * E;
     double* pre = Ff + (W + 1) * (E + 1) + 2 * 5 * E;
-    const int PS = nthr + 2;                         // row stride of a prefetch buffer
+    const int PS = nthr + 4;                         // row stride of a prefetch buffer
     auto H = [&](int slot, int k, int e) -> double& { return halo[(slot * 4 + k) * E + e]; };
 
     // segment-halo cells (x0-2, x0-1 by warp 0; x0+seg, x0+seg+1 by the last warp)
     const bool halo_lane = (warp == 0 || warp == W - 1) && lane < 2;
     const int hcell = warp == 0 ? x0 - 2 + lane : x0 + seg + lane;
+    const int hslot = nthr + (warp == 0 ? 0 : 2) + lane;
     const bool second_halo = W == 1 && lane < 2;     // one warp: it also owns the right halo
     auto issue_row = [&](int y, int buf) {           // cp.async my cells of row y
         const int64_t row = a.base + (int64_t)y * a.sA + (int64_t)blockIdx.z * a.sB;
@@ -456,7 +457,7 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
         if (halo_lane) {
             const double* h = a.q + row + map_cell(hcell, n, a.gm);
 #pragma unroll
-            for (int e = 0; e < E; ++e) cp_async8(b + e * PS + nthr + lane, h + e * a.sE);
+            for (int e = 0; e < E; ++e) cp_async8(b + e * PS + hslot, h + e * a.sE);
         }
         cp_async_commit();
     };
@@ -497,7 +498,7 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
     }
     if (halo_lane) {
         double h[E];
-        prim_from(b, nthr + lane, hcell, h);
+        prim_from(b, hslot, hcell, h);
         const bool left = warp == 0;
 #pragma unroll
         for (int e = 0; e < E; ++e) H(left ? 0 : W + 1, left ? 2 + lane : lane, e) = h[e];

@@ -93,7 +93,7 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                 const int R = 4;                     // rows per block (next row prefetched)
                 const size_t smem = sizeof(double) *
                     ((size_t)(W + 2) * 4 * M::E + (size_t)(W + 1) * M::E +
-                     (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E + 2 * (size_t)M::E * (32 * W + 2));
+                     (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E + 2 * (size_t)M::E * (32 * W + 4));
                 static size_t attr = 0;
                 if (smem > attr) {
                     cudaFuncSetAttribute(sweep_x_rows<M, ORD>,

@@ -90,7 +90,7 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                 // row-parallel x sweep: W warps per row segment, shared tables only
                 const int W = (int)std::min<int64_t>(16, (a.nS + 31) / 32);
                 const int nseg = (a.nS + 32 * W - 1) / (32 * W);
-                const int R = 4;                     // rows per block (next row prefetched)
+                static const int R = getenv("MFC_XROWS") ? std::max(1, atoi(getenv("MFC_XROWS"))) : 1;
                 const size_t smem = sizeof(double) *
                     ((size_t)(W + 2) * 4 * M::E + (size_t)(W + 1) * M::E +
                      (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E + 2 * (size_t)M::E * (32 * W + 4));

@@ -478,19 +478,23 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
         cons_to_prim_fast<M>(qc, v, a.mat);
     };
 
-    if (y0 < y1) issue_row(y0, 0);
+    const bool pf = R > 1;                           // prefetch path (rows loop)
+    if (pf && y0 < y1) issue_row(y0, 0);
     for (int y = y0; y < y1; ++y) {
     const int buf = (y - y0) & 1;
     const int64_t row = a.base + (int64_t)y * a.sA + (int64_t)blockIdx.z * a.sB;
-    cp_async_wait_all();                             // my cells of row y have landed
-    __syncthreads();                                 // (and nobody still reads buf^1)
-    if (y + 1 < y1) issue_row(y + 1, buf ^ 1);       // overlap the next row's loads
+    if (pf) {
+        cp_async_wait_all();                         // my cells of row y have landed
+        __syncthreads();                             // (and nobody still reads buf^1)
+        if (y + 1 < y1) issue_row(y + 1, buf ^ 1);   // overlap the next row's loads
+    }
     const double* b = pre + buf * E * PS;
     auto load_prim = [&](int cell, double (&v)[E]) { load_prim_row(row, cell, v); };
 
     // 1. my cell's primitives; publish the warp's border cells and the segment halo
     double v[E];
-    prim_from(b, tid, x, v);
+    if (pf) prim_from(b, tid, x, v);
+    else load_prim(x, v);
     if (lane < 2 || lane >= 30) {
         const int k = lane < 2 ? lane : lane - 28;
 #pragma unroll
@@ -498,7 +502,8 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
     }
     if (halo_lane) {
         double h[E];
-        prim_from(b, hslot, hcell, h);
+        if (pf) prim_from(b, hslot, hcell, h);
+        else load_prim(hcell, h);
         const bool left = warp == 0;
 #pragma unroll
         for (int e = 0; e < E; ++e) H(left ? 0 : W + 1, left ? 2 + lane : lane, e) = h[e];

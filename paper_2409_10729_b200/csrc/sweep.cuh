@@ -413,18 +413,16 @@ namespace mfc {
 
 template <class M, int ORD>
 __global__ void __launch_bounds__(512, 1)
-sweep_x_rows(const SweepArgs a, int W, int R) {
+sweep_x_rows(const SweepArgs a, int W) {
     constexpr int E = M::E;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nthr = 32 * W;
     const int seg = 32 * W;
     const int x0 = blockIdx.x * seg;
     const int n = a.nS;
     const int x1 = min(x0 + seg, n);                 // cells x0 .. x1-1 are updated
     const bool whole_periodic = (a.gm.blo == 1 && a.gm.alo == n) && x0 == 0 && x1 == n;
     const int x = x0 + tid;                          // my cell (>= n: boundary-mapped ghost)
-    const int y0 = blockIdx.y * R;                   // this block's rows y0 .. y0+R-1
-    const int y1 = min(y0 + R, a.nA);
+    const int64_t row = a.base + (int64_t)blockIdx.y * a.sA + (int64_t)blockIdx.z * a.sB;
 
     // shared tables (doubles):
     //   halo [W+2][4][E]: slot w+1 = warp w's cells 0,1 (k=0,1) and 30,31 (k=2,3);
@@ -433,42 +431,13 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
     //   Ff  [W+1][E+1]: slot w = F, u^f of warp w's first face (x0+32w-1/2); slot W =
     //                   the face x0+seg-1/2 when the segment ends on a warp border
     //   st  [2][5][E]: stencils of the two boundary cells (warp 0, lanes 0/1)
-    //   pre [2][E][nthr + 4]: conserved state of the next row, prefetched with cp.async
-    //                   (own cell at [tid]; left halo at [nthr+0,1], right at [nthr+2,3])
     extern __shared__ double sm[];
     double* halo = sm;
     double* vmL = halo + (W + 2) * 4 * E;
     double* Ff = vmL + (W + 1) * E;
-    double* pre = Ff + (W + 1) * (E + 1) + 2 * 5 * E;
-    const int PS = nthr + 4;                         // row stride of a prefetch buffer
     auto H = [&](int slot, int k, int e) -> double& { return halo[(slot * 4 + k) * E + e]; };
 
-    // segment-halo cells (x0-2, x0-1 by warp 0; x0+seg, x0+seg+1 by the last warp)
-    const bool halo_lane = (warp == 0 || warp == W - 1) && lane < 2;
-    const int hcell = warp == 0 ? x0 - 2 + lane : x0 + seg + lane;
-    const int hslot = nthr + (warp == 0 ? 0 : 2) + lane;
-    const bool second_halo = W == 1 && lane < 2;     // one warp: it also owns the right halo
-    auto issue_row = [&](int y, int buf) {           // cp.async my cells of row y
-        const int64_t row = a.base + (int64_t)y * a.sA + (int64_t)blockIdx.z * a.sB;
-        double* b = pre + buf * E * PS;
-        const double* p = a.q + row + map_cell(x, n, a.gm);
-#pragma unroll
-        for (int e = 0; e < E; ++e) cp_async8(b + e * PS + tid, p + e * a.sE);
-        if (halo_lane) {
-            const double* h = a.q + row + map_cell(hcell, n, a.gm);
-#pragma unroll
-            for (int e = 0; e < E; ++e) cp_async8(b + e * PS + hslot, h + e * a.sE);
-        }
-        cp_async_commit();
-    };
-    auto prim_from = [&](const double* b, int slot, int cell, double (&v)[E]) {
-        double qc[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) qc[e] = b[e * PS + slot];
-        if (map_flip(cell, n, a.gm)) qc[M::IM] = -qc[M::IM];
-        cons_to_prim_fast<M>(qc, v, a.mat);
-    };
-    auto load_prim_row = [&](int64_t row, int cell, double (&v)[E]) {
+    auto load_prim = [&](int cell, double (&v)[E]) {
         const int sc = map_cell(cell, n, a.gm);
         const double* p = a.q + row + sc;
         double qc[E];
@@ -478,36 +447,21 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
         cons_to_prim_fast<M>(qc, v, a.mat);
     };
 
-    const bool pf = R > 1;                           // prefetch path (rows loop)
-    if (pf && y0 < y1) issue_row(y0, 0);
-    for (int y = y0; y < y1; ++y) {
-    const int buf = (y - y0) & 1;
-    const int64_t row = a.base + (int64_t)y * a.sA + (int64_t)blockIdx.z * a.sB;
-    if (pf) {
-        cp_async_wait_all();                         // my cells of row y have landed
-        __syncthreads();                             // (and nobody still reads buf^1)
-        if (y + 1 < y1) issue_row(y + 1, buf ^ 1);   // overlap the next row's loads
-    }
-    const double* b = pre + buf * E * PS;
-    auto load_prim = [&](int cell, double (&v)[E]) { load_prim_row(row, cell, v); };
-
     // 1. my cell's primitives; publish the warp's border cells and the segment halo
     double v[E];
-    if (pf) prim_from(b, tid, x, v);
-    else load_prim(x, v);
+    load_prim(x, v);
     if (lane < 2 || lane >= 30) {
         const int k = lane < 2 ? lane : lane - 28;
 #pragma unroll
         for (int e = 0; e < E; ++e) H(warp + 1, k, e) = v[e];
     }
-    if (halo_lane) {
+    if ((warp == 0 || warp == W - 1) && lane < 2) {
         double h[E];
-        if (pf) prim_from(b, hslot, hcell, h);
-        else load_prim(hcell, h);
         const bool left = warp == 0;
+        load_prim(left ? x0 - 2 + lane : x0 + seg + lane, h);
 #pragma unroll
         for (int e = 0; e < E; ++e) H(left ? 0 : W + 1, left ? 2 + lane : lane, e) = h[e];
-        if (second_halo) {
+        if (W == 1 && lane < 2) {                    // one warp: it is also the last
             load_prim(x0 + seg + lane, h);
 #pragma unroll
             for (int e = 0; e < E; ++e) H(W + 1, lane, e) = h[e];
@@ -619,7 +573,6 @@ sweep_x_rows(const SweepArgs a, int W, int R) {
             a.dst[row + x + e * a.sE] = r * a.invd;
         }
     }
-    }   // rows
 }
 
 }  // namespace mfc

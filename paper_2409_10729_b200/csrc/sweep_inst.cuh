@@ -90,17 +90,10 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                 // row-parallel x sweep: W warps per row segment, shared tables only
                 const int W = (int)std::min<int64_t>(16, (a.nS + 31) / 32);
                 const int nseg = (a.nS + 32 * W - 1) / (32 * W);
-                static const int R = getenv("MFC_XROWS") ? std::max(1, atoi(getenv("MFC_XROWS"))) : 1;
                 const size_t smem = sizeof(double) *
                     ((size_t)(W + 2) * 4 * M::E + (size_t)(W + 1) * M::E +
-                     (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E + 2 * (size_t)M::E * (32 * W + 4));
-                static size_t attr = 0;
-                if (smem > attr) {
-                    cudaFuncSetAttribute(sweep_x_rows<M, ORD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    attr = smem;
-                }
-                sweep_x_rows<M, ORD><<<dim3(nseg, (a.nA + R - 1) / R, a.nB), 32 * W, smem, s>>>(a, W, R);
+                     (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E);
+                sweep_x_rows<M, ORD><<<dim3(nseg, a.nA, a.nB), 32 * W, smem, s>>>(a, W);
               } else {
                 // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
                 const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);

@@ -15,7 +15,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libmfc.so")
+# MFC_LIB: an alternative in-tree build (same-box A/B timing, tools/build_ab.sh)
+SO_PATH = os.environ.get("MFC_LIB") or os.path.join(_HERE, "libmfc.so")
 
 BC_PERIODIC = -1
 BC_REFLECTIVE = -2

@@ -161,31 +161,36 @@ __device__ __forceinline__ void prim_to_cons(const double (&v)[M::E], double (&q
 //   alpha_k ~ d_k / t_k, t_k = (beta'_k + eps')^2, multiplied through by t0 t1 t2:
 //             alpha_k ~ d_k P_k with P_k = product of the other two t_j,
 //   candidates as corrections to c: 6(p_k - c) = (5D1-2D0, D1+2D2, 4D2-D3) for v-,
-//             (D0-4D1, -2D1-D2, 2D3-5D2) for v+, with d_k folded into them,
-//   v = c + (sum_k P_k d_k 6(p_k - c)) / (6 sum_k d_k P_k):  one reciprocal per side.
+//             (D0-4D1, -2D1-D2, 2D3-5D2) for v+,
+//   v = c + (sum_k d_k P_k (p_k - c)) / (sum_k d_k P_k):  one reciprocal per side,
+//   with the linear weights scaled to integers (below) so no product is spent on them.
 __device__ __forceinline__ void weno5(double a, double b, double c, double d, double e,
                                       double eps4, double& vm, double& vp) {
     constexpr double k133 = 13.0 / 3.0;
     const double D0 = b - a, D1 = c - b, D2 = d - c, D3 = e - d;
     const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
     const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
-    double t0 = fma(k133 * s0, s0, r0 * r0) + eps4; t0 *= t0;
-    double t1 = fma(k133 * s1, s1, r1 * r1) + eps4; t1 *= t1;
-    double t2 = fma(k133 * s2, s2, r2 * r2) + eps4; t2 *= t2;
+    double t0 = fma(k133 * s0, s0, fma(r0, r0, eps4)); t0 *= t0;
+    double t1 = fma(k133 * s1, s1, fma(r1, r1, eps4)); t1 *= t1;
+    double t2 = fma(k133 * s2, s2, fma(r2, r2, eps4)); t2 *= t2;
     const double P0 = t1 * t2, P1 = t0 * t2, P2 = t0 * t1;
-    // v-: d = (0.1, 0.6, 0.3), folded into the corrections
-    const double xm0 = fma(0.5, D1, -0.2 * D0);
-    const double xm1 = fma(1.2, D2, 0.6 * D1);
-    const double xm2 = fma(1.2, D2, -0.3 * D3);
-    const double Dm = fma(0.6, P0, fma(3.6, P1, 1.8 * P2));
+    // sum_k d_k P_k scaled by 10 (integer weights), the corrections 6(p_k - c) by 10/6:
+    //   v- (10d = 1, 6, 3): Dm = P0 + 6 P1 + 3 P2,
+    //       Nm = P0 (5D1-2D0)/6 + P1 (D1+2D2) + P2 (2D2-D3/2),          v- = c + Nm/Dm
+    //   v+ (10d = 3, 6, 1): Dp = 3 P0 + 6 P1 + P2,
+    //       Np = P0 (D0/2-2D1) + P1 (-2D1-D2) + P2 (D3/3-5D2/6),        v+ = c + Np/Dp
+    constexpr double k56 = 5.0 / 6.0, k13 = 1.0 / 3.0;
+    const double xm0 = fma(k56, D1, -k13 * D0);
+    const double xm1 = fma(2.0, D2, D1);
+    const double xm2 = fma(2.0, D2, -0.5 * D3);
+    const double Dm = fma(6.0, P1, fma(3.0, P2, P0));
     const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
-    // v+: d = (0.3, 0.6, 0.1)
-    const double xp0 = fma(-1.2, D1, 0.3 * D0);
-    const double xp1 = fma(-1.2, D1, -0.6 * D2);
-    const double xp2 = fma(-0.5, D2, 0.2 * D3);
-    const double Dp = fma(1.8, P0, fma(3.6, P1, 0.6 * P2));
-    const double Np = fma(P2, xp2, fma(P1, xp1, P0 * xp0));
     vm = fma(Nm, rcp(Dm), c);
+    const double xp0 = fma(-2.0, D1, 0.5 * D0);
+    const double xp1 = fma(-2.0, D1, -D2);
+    const double xp2 = fma(k13, D3, -k56 * D2);
+    const double Dp = fma(3.0, P0, fma(6.0, P1, P2));
+    const double Np = fma(P2, xp2, fma(P1, xp1, P0 * xp0));
     vp = fma(Np, rcp(Dp), c);
 }
 

@@ -74,16 +74,22 @@ typedef struct {
     int32_t procs[3];       /* rank grid; product == comm.nranks; {1,1,P} = z-slabs */
 } mfc_grid;
 
-/* Communicator.  nranks == 1: single domain, no NCCL.  nranks > 1 with
- * loopback == 0: one process per GPU, NCCL over NVLink; nccl_unique_id points to
- * the 128-byte ncclUniqueId every rank received (e.g. broadcast with
- * torch.distributed).  loopback == 1: all nranks subdomains live in THIS process
- * on one device and halos are exchanged with device copies (tests; see the
- * *_group calls). */
+/* Communicator.  nranks == 1: single domain, no NCCL.  For nranks > 1 the field
+ * `loopback` selects the transport:
+ *   MFC_TRANSPORT_NCCL (0): one process per GPU, NCCL over NVLink; nccl_unique_id
+ *       points to the 128-byte ncclUniqueId every rank received (e.g. broadcast with
+ *       torch.distributed);
+ *   MFC_TRANSPORT_LOOPBACK (1): all nranks subdomains live in THIS process on one
+ *       device and halos are exchanged with device copies (tests; the *_group calls);
+ *   MFC_TRANSPORT_PEER (2): one process per rank, no NCCL; halos travel only as
+ *       fused-halo stores into the neighbours' CUDA-IPC-mapped buffers
+ *       (mfc_peer_export / mfc_peer_import below).  Works across GPUs with peer
+ *       access and between processes sharing one GPU. */
+enum { MFC_TRANSPORT_NCCL = 0, MFC_TRANSPORT_LOOPBACK = 1, MFC_TRANSPORT_PEER = 2 };
 typedef struct {
     int32_t rank, nranks;
     const void* nccl_unique_id;
-    int32_t loopback;
+    int32_t loopback;       /* transport, see above */
 } mfc_comm;
 
 /* Local layout, filled by mfc_get_layout. */
@@ -190,6 +196,38 @@ int mfc_rhs_group(mfc_ctx* const* ctxs, double* const* qs, double* const* rhss,
                   int32_t count, void* stream);
 int mfc_rk3_step_group(mfc_ctx* const* ctxs, double* const* qs, int32_t count, double dt,
                        void* stream);
+
+/* Fused halo (the halo exchange of P:94 fused into the producing
+ * kernel).  Once attached, the sweep that writes each RK stage result also stores the
+ * 3 cell layers next to every face shared with another rank directly into that
+ * neighbour's ghost layers, so an RK3 step launches no pack / exchange / unpack work.
+ * The state buffer q is REGISTERED at attach time: mfc_rk3_step, mfc_rk3_steps,
+ * mfc_rhs and mfc_halo_exchange then require that same q (ESTATE otherwise).  The
+ * steps keep q's ghost layers current; after writing q's interior by other means call
+ * mfc_halo_exchange(q) once before the next step.  Results are bitwise identical to
+ * the exchanged path.
+ *
+ * Loopback groups: mfc_fused_halo_group wires the contexts of one group (the same
+ * ctxs/qs arrays as the *_group calls) directly; ordering comes from the stream.
+ *
+ * One process per rank (transport NCCL or PEER): a collective attach --
+ *   mfc_peer_export(ctx, q, blob)       fills MFC_PEER_BLOB_BYTES bytes: CUDA-IPC
+ *                                       handles of q, the RK stage buffers and a flag
+ *                                       array (workspace must be bound);
+ *   exchange the blobs (e.g. torch.distributed.all_gather_object);
+ *   mfc_peer_import(ctx, face, blob)    for every face with a neighbour, with that
+ *                                       neighbour's blob (EINVAL if the blob is not
+ *                                       the neighbour's or the extents disagree);
+ *   a barrier on all ranks before the first fused call.
+ * Ranks then order their operations with stream memory operations on the flags
+ * (cuStreamWaitValue64 / cuStreamWriteValue64: no spinning kernels): every fused call
+ * is collective and all ranks must issue the same sequence.  mfc_rk3_steps does not
+ * use a CUDA graph in this mode.  EUNSUPPORTED if the device lacks 64-bit stream
+ * memory operations; ECUDA if IPC mapping fails. */
+#define MFC_PEER_BLOB_BYTES 512
+int mfc_fused_halo_group(mfc_ctx* const* ctxs, double* const* qs, int32_t count);
+int mfc_peer_export(mfc_ctx* ctx, double* q, void* blob);
+int mfc_peer_import(mfc_ctx* ctx, int32_t face, const void* blob);
 
 /* Generate the 128-byte NCCL unique id (rank 0 calls it and broadcasts the bytes,
  * e.g. over torch.distributed, before every rank calls mfc_init). */

@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -104,6 +106,19 @@ struct mfc_ctx {
     const double* graph_q = nullptr;
     double graph_dt = 0.0;
     int64_t graph_launches = 0;
+    // fused halo (F1): the last sweep of every RK stage stores the cells next to a
+    // shared face into the neighbour's ghost layers; pf[f][b] = destination in the
+    // neighbour across face f of its buffer b (0 = registered state q, 1 = S1, 2 = S2)
+    int transport = 0;             // MFC_TRANSPORT_NCCL / _LOOPBACK / _PEER
+    bool fused = false;            // every neighbour face attached
+    bool peer_sync = false;        // IPC peers: stream memory operations order the ops
+    double* fused_q = nullptr;     // the registered state buffer
+    PeerFace pf[6][3] = {};
+    bool pf_set[6] = {};
+    uint64_t* flags = nullptr;     // device [8]: flags[f] written by the neighbour across f
+    CUdeviceptr peer_flag[6] = {}; // the neighbour's flags[f^1]
+    uint64_t epoch = 0;            // fused-halo operations completed by this rank
+    std::vector<void*> ipc_maps;   // IPC mappings this context opened
 };
 
 namespace {
@@ -193,6 +208,61 @@ FaceGeom geom(const mfc_ctx* c) {
     for (int k = 0; k < 3; ++k) g.n[k] = (int32_t)c->nl[k];
     g.E = c->E;
     return g;
+}
+
+// Padded layout of a subdomain with interior extents nl (the same formula for every
+// rank, so a neighbour's layout follows from its extents).
+struct Lay {
+    int64_t dims[4], stride[4], offset, n_elems;
+};
+Lay layout_for(int D, int E, const int64_t nl[3]) {
+    Lay L;
+    const int64_t X = ((kXOff + nl[0] + kGhost) + 3) / 4 * 4;
+    const int64_t Y = D >= 2 ? nl[1] + 2 * kGhost : 1;
+    const int64_t Z = D >= 3 ? nl[2] + 2 * kGhost : 1;
+    L.dims[0] = E; L.dims[1] = Z; L.dims[2] = Y; L.dims[3] = X;
+    L.stride[3] = 1; L.stride[2] = X; L.stride[1] = X * Y; L.stride[0] = X * Y * Z;
+    L.offset = (D >= 3 ? kGhost : 0) * L.stride[1] + (D >= 2 ? kGhost : 0) * L.stride[2] + kXOff;
+    L.n_elems = E * X * Y * Z;
+    return L;
+}
+
+// Destination of my face f in a neighbour with interior extents nn and layout L
+// (buffer nbuf): my cells with coordinate in [lo, hi) along the face dimension land in
+// its ghost layer, at index + nn[k] across my low face, - n[k] across my high face.
+PeerFace make_peer_face(const mfc_ctx* c, int f, double* nbuf, const Lay& L, const int64_t nn[3]) {
+    const int k = f / 2, side = f % 2;
+    PeerFace p{};
+    p.dst = nbuf;
+    p.sE = L.stride[0];
+    p.sy = L.stride[2];
+    p.sz = L.stride[1];
+    const int64_t sk = k == 0 ? 1 : (k == 1 ? p.sy : p.sz);
+    const int64_t shift = side == 0 ? nn[k] : -c->nl[k];
+    p.off = L.offset + shift * sk;
+    p.dim = k;
+    p.lo = side == 0 ? 0 : (int32_t)c->nl[k] - kGhost;
+    p.hi = side == 0 ? kGhost : (int32_t)c->nl[k];
+    return p;
+}
+
+// Fused-halo exchange of a state (mfc_halo_exchange / mfc_rhs in fused mode): my 3
+// interior layers next to face p go straight into the neighbour's ghost layers.
+__global__ void peer_exchange_kernel(const double* q, FaceGeom g, PeerFace p) {
+    const int k = p.dim, t1 = (k + 1) % 3, t2 = (k + 2) % 3;
+    const int64_t area = (int64_t)g.n[t1] * g.n[t2];
+    const int64_t total = area * kGhost * g.E;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = t;
+        int xyz[3];
+        xyz[t1] = (int)(r % g.n[t1]); r /= g.n[t1];
+        xyz[t2] = (int)(r % g.n[t2]); r /= g.n[t2];
+        xyz[k] = p.lo + (int)(r % kGhost); r /= kGhost;
+        const int64_t e = r;
+        const double v = q[g.base + e * g.sE + xyz[0] + xyz[1] * g.s[1] + xyz[2] * g.s[2]];
+        p.dst[p.off + e * p.sE + xyz[0] + xyz[1] * p.sy + xyz[2] * p.sz] = v;
+    }
 }
 
 // ------------------------------------------------------------ profiling
@@ -291,8 +361,19 @@ int need_ws(const mfc_ctx* c, bool stages) {
 // Ghost fill for a set of contexts (count == 1: NCCL or single domain; > 1: loopback).
 // physical == false: only faces shared with another rank (the sweeps apply physical
 // boundary conditions themselves by index mapping, so the RHS path skips bc_fill).
+int exchange_fused(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
+                   bool physical);
+bool group_fused(mfc_ctx* const* cs, int count, int* err);
+
 int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
              bool physical = true) {
+    {
+        int err = MFC_OK;
+        if (group_fused(cs, count, &err)) return exchange_fused(cs, qs, count, s, physical);
+        if (err) return err;
+    }
+    if (cs[0]->transport == MFC_TRANSPORT_PEER)
+        return fail(MFC_ESTATE, "peer transport: attach every neighbour (mfc_peer_import) first");
     for (int r = 0; r < count; ++r) {
         int st = need_ws(cs[r], false);
         if (st) return st;
@@ -345,6 +426,84 @@ int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
     return MFC_OK;
 }
 
+// ------------------------------------------------------------ fused halo (F1)
+//
+// Every rank performs the same sequence of fused-halo operations (collective calls).
+// Operation number e (1, 2, ...) of a rank: wait until every neighbour has completed
+// operation e-1 (its flag in my flags[] >= e-1), read my ghost layers, write the
+// neighbours' ghost layers, then signal e into each neighbour's flag.  Ghosts read in
+// operation e were written in the neighbours' operation e-1; ghosts I write in
+// operation e are read by the neighbour in its operation e+1, and the neighbour read
+// the previous contents of that buffer (written 3 operations earlier, buffers rotate
+// q -> S1 -> S2 -> q) in its operation e-2, which the wait on e-1 covers.  Waits and
+// signals are stream memory operations (no spinning kernel); loopback groups on one
+// stream need neither.
+
+using FnStreamValue64 = CUresult(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+extern FnStreamValue64* p_wait_value;
+extern FnStreamValue64* p_write_value;
+
+int peer_wait(mfc_ctx* c, cudaStream_t s, uint64_t value) {
+    for (int f = 0; f < 2 * c->D; ++f) {
+        if (c->bc[f] != BC_NEIGHBOR) continue;
+        const CUresult r = p_wait_value((CUstream)s, (CUdeviceptr)(c->flags + f),
+                                        (cuuint64_t)value, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return fail(MFC_ECUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
+    }
+    return MFC_OK;
+}
+
+int peer_signal(mfc_ctx* c, cudaStream_t s) {
+    ++c->epoch;
+    for (int f = 0; f < 2 * c->D; ++f) {
+        if (c->bc[f] != BC_NEIGHBOR) continue;
+        // default flags: the write is ordered after (and flushes) all prior work
+        const CUresult r = p_write_value((CUstream)s, c->peer_flag[f], (cuuint64_t)c->epoch,
+                                         CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) return fail(MFC_ECUDA, "cuStreamWriteValue64 failed (%d)", (int)r);
+    }
+    return MFC_OK;
+}
+
+// Fused exchange of the registered states: (wait) -> physical ghosts, my boundary
+// layers into the neighbours' ghosts -> (signal, then wait until the neighbours'
+// layers have arrived in mine).
+int exchange_fused(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
+                   bool physical) {
+    for (int r = 0; r < count; ++r) {
+        mfc_ctx* c = cs[r];
+        if (qs[r] != c->fused_q)
+            return fail(MFC_ESTATE, "fused halo: q is not the registered state buffer");
+        int st;
+        if (c->peer_sync && (st = peer_wait(c, s, c->epoch))) return st;
+        if (physical && (st = bc_fill(c, qs[r], s))) return st;
+        const FaceGeom g = geom(c);
+        for (int f = 0; f < 2 * c->D; ++f) {
+            if (c->bc[f] != BC_NEIGHBOR) continue;
+            ProfScope ps(c, s, K_HALO);
+            peer_exchange_kernel<<<grid_for(c->face_elems[f / 2], 256), 256, 0, s>>>(
+                qs[r], g, c->pf[f][0]);
+            CU_TRY(cudaGetLastError());
+            ++c->launches;
+        }
+        if (c->peer_sync && (st = peer_signal(c, s))) return st;
+    }
+    for (int r = 0; r < count; ++r) {
+        int st;
+        if (cs[r]->peer_sync && (st = peer_wait(cs[r], s, cs[r]->epoch))) return st;
+    }
+    return MFC_OK;
+}
+
+bool group_fused(mfc_ctx* const* cs, int count, int* err) {
+    int nf = 0;
+    for (int r = 0; r < count; ++r) nf += cs[r]->fused ? 1 : 0;
+    *err = (nf != 0 && nf != count)
+               ? fail(MFC_ESTATE, "fused halo attached on some contexts of the group only")
+               : MFC_OK;
+    return nf == count;
+}
+
 // ------------------------------------------------------------------ sweeps
 
 // Segment length T of the marches.  Longer segments waste less on the (T+2)/T halo
@@ -369,8 +528,10 @@ int seg_len(const mfc_ctx* c, int dir, int resident_warps_per_sm) {
 
 int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const double* acc,
                      double* dst, const double* qn, double w, double ca, double cb,
-                     cudaStream_t s) {
+                     cudaStream_t s, const PeerOut* po = nullptr) {
     SweepArgs a;
+    a.po.nf = 0;
+    if (po) a.po = *po;
     a.q = q;
     a.acc = acc;
     a.dst = dst;
@@ -437,14 +598,20 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
 //   rk == true : dst = ca*qn + cb*(q + dt*(c_x + c_y + c_z)), accumulating in acc:
 //     1D: x = M_RKINIT -> dst;  2D/3D: x = M_SET -> acc, y = M_RKACC, z = M_ACC.
 int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const double* qn,
-           double dt, double ca, double cb, cudaStream_t s, cudaEvent_t halo = nullptr) {
+           double dt, double ca, double cb, cudaStream_t s, cudaEvent_t halo = nullptr,
+           int peer_buf = -1) {
     const double w = rk ? cb * dt : 1.0;
     bool waited = false;
     for (int dir = 0; dir < c->D; ++dir) {
         // only a sweep along a split dimension reads exchanged ghost layers: it (and
-        // everything after it on the stream) waits for the comm stream's halo event
-        if (halo && !waited && (c->bc[2 * dir] == BC_NEIGHBOR || c->bc[2 * dir + 1] == BC_NEIGHBOR)) {
-            CU_TRY(cudaStreamWaitEvent(s, halo, 0));
+        // everything after it on the stream) waits for the comm stream's halo event,
+        // or, with IPC peers, for every neighbour's flag to reach the last operation
+        if (!waited && (c->bc[2 * dir] == BC_NEIGHBOR || c->bc[2 * dir + 1] == BC_NEIGHBOR)) {
+            if (halo) CU_TRY(cudaStreamWaitEvent(s, halo, 0));
+            if (c->peer_sync && peer_buf >= 0) {
+                const int st = peer_wait(c, s, c->epoch);
+                if (st) return st;
+            }
             waited = true;
         }
         const bool last = dir == c->D - 1;
@@ -455,7 +622,12 @@ int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const
         else mode = M_ACC;
         // M_SET in an RK stage writes the unscaled c_x; M_RKACC scales (acc + c_y) by w
         const double wd = (mode == M_SET) ? 1.0 : w;
-        int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn, wd, ca, cb, s);
+        PeerOut po;
+        po.nf = 0;
+        if (last && peer_buf >= 0)
+            for (int f = 0; f < 2 * c->D; ++f)
+                if (c->bc[f] == BC_NEIGHBOR) po.f[po.nf++] = c->pf[f][peer_buf];
+        int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn, wd, ca, cb, s, &po);
         if (st) return st;
     }
     return MFC_OK;
@@ -498,19 +670,28 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
         if ((st = check_ptr(qs[r], "q"))) return st;
         cs[r]->launches = 0;
     }
+    int err = MFC_OK;
+    const bool fused = group_fused(cs, count, &err);
+    if (err) return err;
+    for (int r = 0; fused && r < count; ++r)
+        if (qs[r] != cs[r]->fused_q)
+            return fail(MFC_ESTATE, "fused halo: q is not the registered state buffer");
     std::vector<double*> in(count);
     for (int stage = 0; stage < 3; ++stage) {
         for (int r = 0; r < count; ++r)
             in[r] = stage == 0 ? qs[r] : (stage == 1 ? cs[r]->S1 : cs[r]->S2);
         cudaEvent_t halo = nullptr;
-        int st = halo_async(cs, in.data(), count, s, &halo);
-        if (st) return st;
+        int st;
+        // fused: the previous stage's last sweep already wrote the ghost layers
+        if (!fused && (st = halo_async(cs, in.data(), count, s, &halo))) return st;
         for (int r = 0; r < count; ++r) {
             mfc_ctx* c = cs[r];
             double* out = stage == 0 ? c->S1 : (stage == 1 ? c->S2 : qs[r]);
+            const int pb = fused ? (stage == 0 ? 1 : (stage == 1 ? 2 : 0)) : -1;
             if ((st = sweeps(c, in[r], c->acc, out, true, qs[r], dt, CA[stage], CB[stage], s,
-                             halo)))
+                             halo, pb)))
                 return st;
+            if (fused && c->peer_sync && (st = peer_signal(c, s))) return st;
         }
     }
     return MFC_OK;
@@ -524,6 +705,20 @@ int rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int co
         if (qs[r] == rhss[r]) return fail(MFC_EINVAL, "q and rhs alias");
         cs[r]->launches = 0;
     }
+    int err = MFC_OK;
+    const bool fused = group_fused(cs, count, &err);
+    if (err) return err;
+    if (fused) {
+        // exchange (operation e), then read the ghosts and signal e+1 when done
+        int st = exchange_fused(cs, qs, count, s, false);
+        if (st) return st;
+        for (int r = 0; r < count; ++r) {
+            if ((st = sweeps(cs[r], qs[r], rhss[r], rhss[r], false, nullptr, 0, 0, 0, s)))
+                return st;
+            if (cs[r]->peer_sync && (st = peer_signal(cs[r], s))) return st;
+        }
+        return MFC_OK;
+    }
     cudaEvent_t halo = nullptr;
     int st = halo_async(cs, qs, count, s, &halo);
     if (st) return st;
@@ -531,6 +726,79 @@ int rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int co
         if ((st = sweeps(cs[r], qs[r], rhss[r], rhss[r], false, nullptr, 0, 0, 0, s, halo)))
             return st;
     return MFC_OK;
+}
+
+// ---------------------------------------------------------- driver entry points
+// The few driver-API calls (stream memory operations, address ranges) are resolved
+// through the runtime at first use, so libmfc.so does not link libcuda and still
+// loads on a machine without a GPU driver.
+
+template <class F>
+int drv(const char* name, F** fn) {
+    if (*fn) return MFC_OK;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    void* p = nullptr;
+    const cudaError_t e = cudaGetDriverEntryPointByVersion(name, &p, 12000, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+        return fail(MFC_ECUDA, "driver entry point %s unavailable", name);
+    *fn = (F*)p;
+    return MFC_OK;
+}
+
+using FnMemGetAddressRange = CUresult(CUdeviceptr*, size_t*, CUdeviceptr);
+using FnDeviceGetAttribute = CUresult(int*, CUdevice_attribute, CUdevice);
+using FnDeviceGet = CUresult(CUdevice*, int);
+FnStreamValue64* p_wait_value = nullptr;
+FnStreamValue64* p_write_value = nullptr;
+FnMemGetAddressRange* p_addr_range = nullptr;
+FnDeviceGetAttribute* p_dev_attr = nullptr;
+FnDeviceGet* p_dev_get = nullptr;
+
+// ---------------------------------------------------------- CUDA IPC plumbing
+
+constexpr uint64_t kPeerMagic = 0x3152454550434d46ull;   // "FMCPEER1"
+
+struct PeerBlob {                 // what mfc_peer_export hands to the neighbours
+    uint64_t magic;
+    int32_t rank, E, D, pad;
+    int64_t nl[3];
+    cudaIpcMemHandle_t h[4];      // allocations holding q, S1, S2, flags
+    int64_t off[4];               // byte offsets of those buffers inside them
+};
+static_assert(sizeof(PeerBlob) <= MFC_PEER_BLOB_BYTES, "peer blob size");
+
+// A process maps each exported allocation once (cudaIpcOpenMemHandle refuses a second
+// mapping of the same handle); contexts share the mapping with a reference count.
+std::mutex g_ipc_mu;
+std::map<std::string, std::pair<void*, int>> g_ipc;
+
+int ipc_open(const cudaIpcMemHandle_t& h, void** out) {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    const std::string key((const char*)&h, sizeof h);
+    auto it = g_ipc.find(key);
+    if (it != g_ipc.end()) {
+        ++it->second.second;
+        *out = it->second.first;
+        return MFC_OK;
+    }
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(MFC_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    g_ipc[key] = {p, 1};
+    *out = p;
+    return MFC_OK;
+}
+
+void ipc_release(void* p) {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (auto it = g_ipc.begin(); it != g_ipc.end(); ++it) {
+        if (it->second.first != p) continue;
+        if (--it->second.second == 0) {
+            cudaIpcCloseMemHandle(p);
+            g_ipc.erase(it);
+        }
+        return;
+    }
 }
 
 }  // namespace
@@ -590,7 +858,12 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
     c->E = 2 * n_fluids + D + 1;
     c->rank = rank;
     c->nranks = nranks;
-    c->loopback = comm && comm->loopback;
+    c->transport = comm ? comm->loopback : MFC_TRANSPORT_NCCL;
+    if (c->transport < MFC_TRANSPORT_NCCL || c->transport > MFC_TRANSPORT_PEER) {
+        delete c;
+        return fail(MFC_EINVAL, "comm.loopback (transport) must be 0, 1 or 2");
+    }
+    c->loopback = c->transport == MFC_TRANSPORT_LOOPBACK;
     for (int k = 0; k < 3; ++k) c->procs[k] = grid->procs[k] > 0 ? grid->procs[k] : 1;
     c->coords[0] = rank % c->procs[0];
     c->coords[1] = (rank / c->procs[0]) % c->procs[1];
@@ -631,16 +904,16 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
         c->mat.Pi[i] = (gamma[i] * pi_inf[i]) / (gamma[i] - 1.0);
     }
     // layout
-    const int64_t X = ((kXOff + c->nl[0] + kGhost) + 3) / 4 * 4;
-    const int64_t Y = D >= 2 ? c->nl[1] + 2 * kGhost : 1;
-    const int64_t Z = D >= 3 ? c->nl[2] + 2 * kGhost : 1;
-    c->dims[0] = c->E; c->dims[1] = Z; c->dims[2] = Y; c->dims[3] = X;
-    c->stride[3] = 1; c->stride[2] = X; c->stride[1] = X * Y; c->stride[0] = X * Y * Z;
+    const Lay L = layout_for(D, c->E, c->nl);
+    for (int k = 0; k < 4; ++k) {
+        c->dims[k] = L.dims[k];
+        c->stride[k] = L.stride[k];
+    }
     c->off[0] = kXOff;
     c->off[1] = D >= 2 ? kGhost : 0;
     c->off[2] = D >= 3 ? kGhost : 0;
-    c->offset = c->off[2] * c->stride[1] + c->off[1] * c->stride[2] + c->off[0];
-    c->n_elems = c->E * X * Y * Z;
+    c->offset = L.offset;
+    c->n_elems = L.n_elems;
     size_t need = 3 * (size_t)c->n_elems * sizeof(double);
     for (int k = 0; k < D; ++k) {
         const int t1 = (k + 1) % 3, t2 = (k + 2) % 3;
@@ -658,7 +931,7 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
     // The device is only touched here when NCCL needs it; single-domain and loopback
     // contexts are pure host bookkeeping until the first GPU call (so layouts can be
     // queried on a machine without a GPU).
-    if (nranks > 1 && !c->loopback) {
+    if (nranks > 1 && c->transport == MFC_TRANSPORT_NCCL) {
         if (cudaSetDevice(device) != cudaSuccess) {
             delete c;
             return fail(MFC_ECUDA, "cudaSetDevice(%d) failed", device);
@@ -862,7 +1135,9 @@ int mfc_rk3_steps(mfc_ctx* c, double* q, double dt, int64_t nsteps, void* stream
     int st = set_device(c);
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    if (c->prof) {   // per-launch event timing needs the plain launches
+    if (c->prof || c->peer_sync) {
+        // per-launch event timing needs the plain launches; IPC-peer waits compare
+        // against per-operation values that a replayed graph could not advance
         for (int64_t i = 0; i < nsteps; ++i)
             if ((st = rk3_group(&c, &q, 1, dt, s))) return st;
         return MFC_OK;
@@ -950,6 +1225,118 @@ int mfc_rk3_step_group(mfc_ctx* const* cs, double* const* qs, int32_t count, dou
     return rk3_group(cs, qs, count, dt, (cudaStream_t)stream);
 }
 
+int mfc_fused_halo_group(mfc_ctx* const* cs, double* const* qs, int32_t count) {
+    if (!cs || !qs || count < 1) return fail(MFC_EINVAL, "bad group");
+    for (int r = 0; r < count; ++r) {
+        int st;
+        if (!cs[r]) return fail(MFC_EINVAL, "NULL ctx");
+        if ((st = need_ws(cs[r], true)) || (st = check_ptr(qs[r], "q"))) return st;
+        if (cs[r]->transport != MFC_TRANSPORT_LOOPBACK && count > 1)
+            return fail(MFC_EINVAL, "fused group needs loopback contexts");
+    }
+    for (int r = 0; r < count; ++r) {
+        mfc_ctx* c = cs[r];
+        for (int f = 0; f < 2 * c->D; ++f) {
+            if (c->bc[f] != BC_NEIGHBOR) continue;
+            const int o = c->nbr[f];
+            if (o < 0 || o >= count) return fail(MFC_EINVAL, "group lacks rank %d", o);
+            const mfc_ctx* n = cs[o];
+            for (int k = 0; k < 3; ++k)
+                if (k != f / 2 && n->nl[k] != c->nl[k])
+                    return fail(MFC_EINVAL, "neighbour extents do not match across face %d", f);
+            const Lay L = layout_for(n->D, n->E, n->nl);
+            c->pf[f][0] = make_peer_face(c, f, qs[o], L, n->nl);
+            c->pf[f][1] = make_peer_face(c, f, n->S1, L, n->nl);
+            c->pf[f][2] = make_peer_face(c, f, n->S2, L, n->nl);
+            c->pf_set[f] = true;
+        }
+        c->fused_q = qs[r];
+        c->fused = true;
+        c->peer_sync = false;
+    }
+    return MFC_OK;
+}
+
+int mfc_peer_export(mfc_ctx* c, double* q, void* blob) {
+    if (!c || !blob) return fail(MFC_EINVAL, "NULL argument");
+    int st;
+    if ((st = need_ws(c, true)) || (st = check_ptr(q, "q")) || (st = set_device(c))) return st;
+    if (c->transport == MFC_TRANSPORT_LOOPBACK)
+        return fail(MFC_EINVAL, "loopback contexts attach with mfc_fused_halo_group");
+    if ((st = drv("cuDeviceGet", &p_dev_get)) || (st = drv("cuDeviceGetAttribute", &p_dev_attr)) ||
+        (st = drv("cuMemGetAddressRange", &p_addr_range)) ||
+        (st = drv("cuStreamWaitValue64", &p_wait_value)) ||
+        (st = drv("cuStreamWriteValue64", &p_write_value)))
+        return st;
+    CUdevice dev;
+    int memops = 0;
+    if (p_dev_get(&dev, c->device) != CUDA_SUCCESS ||
+        p_dev_attr(&memops, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, dev) != CUDA_SUCCESS)
+        return fail(MFC_ECUDA, "cuDeviceGetAttribute failed");
+    if (!memops) return fail(MFC_EUNSUPPORTED, "device lacks 64-bit stream memory operations");
+    if (!c->flags) {
+        CU_TRY(cudaMalloc(&c->flags, 8 * sizeof(uint64_t)));
+        CU_TRY(cudaMemset(c->flags, 0, 8 * sizeof(uint64_t)));
+    }
+    PeerBlob b{};
+    b.magic = kPeerMagic;
+    b.rank = c->rank;
+    b.E = c->E;
+    b.D = c->D;
+    for (int k = 0; k < 3; ++k) b.nl[k] = c->nl[k];
+    const void* ptrs[4] = {q, c->S1, c->S2, c->flags};
+    for (int i = 0; i < 4; ++i) {
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (p_addr_range(&base, &size, (CUdeviceptr)ptrs[i]) != CUDA_SUCCESS)
+            return fail(MFC_ECUDA, "cuMemGetAddressRange failed for buffer %d", i);
+        CU_TRY(cudaIpcGetMemHandle(&b.h[i], (void*)base));
+        b.off[i] = (int64_t)((CUdeviceptr)ptrs[i] - base);
+    }
+    memcpy(blob, &b, sizeof b);
+    c->fused_q = q;
+    CU_TRY(cudaDeviceSynchronize());   // flags are zero before any neighbour signals
+    return MFC_OK;
+}
+
+int mfc_peer_import(mfc_ctx* c, int32_t face, const void* blob) {
+    if (!c || !blob) return fail(MFC_EINVAL, "NULL argument");
+    if (face < 0 || face >= 2 * c->D || c->bc[face] != BC_NEIGHBOR)
+        return fail(MFC_EINVAL, "face %d has no neighbour rank", face);
+    if (!c->fused_q || !c->flags) return fail(MFC_ESTATE, "call mfc_peer_export first");
+    int st;
+    if ((st = set_device(c))) return st;
+    PeerBlob b;
+    memcpy(&b, blob, sizeof b);
+    if (b.magic != kPeerMagic) return fail(MFC_EINVAL, "not an mfc_peer_export blob");
+    if (b.rank != c->nbr[face])
+        return fail(MFC_EINVAL, "blob of rank %d, face %d needs rank %d", b.rank, face, c->nbr[face]);
+    if (b.E != c->E || b.D != c->D) return fail(MFC_EINVAL, "neighbour has another model");
+    for (int k = 0; k < 3; ++k)
+        if (k != face / 2 && b.nl[k] != c->nl[k])
+            return fail(MFC_EINVAL, "neighbour extents do not match across face %d", face);
+    char* base[4];
+    for (int i = 0; i < 4; ++i) {
+        void* p = nullptr;
+        if ((st = ipc_open(b.h[i], &p))) return st;
+        c->ipc_maps.push_back(p);
+        base[i] = (char*)p + b.off[i];
+    }
+    const Lay L = layout_for(b.D, b.E, b.nl);
+    for (int i = 0; i < 3; ++i) c->pf[face][i] = make_peer_face(c, face, (double*)base[i], L, b.nl);
+    c->peer_flag[face] = (CUdeviceptr)((uint64_t*)base[3] + (face ^ 1));
+    c->pf_set[face] = true;
+    bool all = true;
+    for (int f = 0; f < 2 * c->D; ++f)
+        if (c->bc[f] == BC_NEIGHBOR && !c->pf_set[f]) all = false;
+    if (all) {
+        c->fused = true;
+        c->peer_sync = true;
+        c->epoch = 0;
+    }
+    return MFC_OK;
+}
+
 int64_t mfc_last_launch_count(const mfc_ctx* c) { return c ? c->launches : -1; }
 
 int mfc_nccl_get_unique_id(void* out128) {
@@ -985,6 +1372,8 @@ int mfc_profile_read(mfc_ctx* c, double* ms, int64_t* count, int32_t nkinds) {
 
 int mfc_finalize(mfc_ctx* c) {
     if (!c) return MFC_OK;
+    for (void* p : c->ipc_maps) ipc_release(p);
+    if (c->flags) cudaFree(c->flags);
     if (c->graph) cudaGraphExecDestroy(c->graph);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);

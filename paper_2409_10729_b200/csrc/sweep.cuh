@@ -72,6 +72,38 @@ __device__ __forceinline__ bool map_flip(int s, int n, const GhostMap& g) {
     return (s < 0 && g.flip_lo) || (s >= n && g.flip_hi);
 }
 
+// Fused halo: the sweep that writes an RK stage result also stores
+// every result cell lying within 3 cells of a face shared with another rank straight
+// into that neighbour's ghost layer (peer memory: the same device for loopback groups,
+// a CUDA-IPC mapping of the neighbour's buffer otherwise), so no pack / exchange /
+// unpack pass follows the stage.  My cell (x, y, z) with lo <= coord[dim] < hi goes to
+// the neighbour's element off + e*sE + x + y*sy + z*sz (off folds the neighbour's
+// interior offset and the index shift across the face: +n_nbr on my low face, -n on
+// my high face; tangential coordinates are shared by construction of the block
+// decomposition).
+struct PeerFace {
+    double* dst;                    // neighbour's buffer (element 0)
+    int64_t off, sE, sy, sz;        // neighbour's layout, shift folded into off
+    int32_t dim, lo, hi, pad;       // face dimension; my coordinates [lo, hi) are sent
+};
+struct PeerOut {
+    int32_t nf;                     // faces with a neighbour (0: plain sweep)
+    PeerFace f[6];
+};
+
+template <int E>
+__device__ __forceinline__ void peer_store(const PeerOut& po, int x, int y, int z,
+                                           const double (&v)[E]) {
+    for (int i = 0; i < po.nf; ++i) {
+        const PeerFace& p = po.f[i];
+        const int ck = p.dim == 0 ? x : (p.dim == 1 ? y : z);
+        if (ck < p.lo || ck >= p.hi) continue;
+        double* d = p.dst + p.off + x + (int64_t)y * p.sy + (int64_t)z * p.sz;
+#pragma unroll
+        for (int e = 0; e < E; ++e) d[e * p.sE] = v[e];
+    }
+}
+
 struct SweepArgs {
     const double* __restrict__ q;   // stencil state (padded layout, ghosts filled)
     const double* acc;              // accumulator input (M_ACC, M_RKACC)
@@ -88,6 +120,7 @@ struct SweepArgs {
     double eps;                     // WENO epsilon (weno3)
     double w, ca, cb;               // epilogue weights
     Materials mat;
+    PeerOut po;                     // fused halo stores (last sweep of a stage only)
 };
 
 // Per-thread shared-memory rings for the streamed operands (filled by cp.async two
@@ -128,7 +161,7 @@ __host__ __device__ constexpr int sweep_min_blocks() {
     return ((MODE == M_ACC || MODE == M_SET) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
-template <class M, int DIR, int MODE, int ORD>
+template <class M, int DIR, int MODE, int ORD, bool PEER = false>
 __global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, MODE>())
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
@@ -228,6 +261,7 @@ sweep_kernel(const SweepArgs a) {
                 const int cc = j - 1;
                 const int64_t c = line + (int64_t)cc * a.sS;
                 const double du = uf - uf_prev;
+                double outv[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     double r = F_prev[e] - F[e];                 // dx * c_e
@@ -245,6 +279,16 @@ sweep_kernel(const SweepArgs a) {
                                   : fma(a.w * a.invd, r, base);
                     }
                     a.dst[c + e * a.sE] = out;
+                    outv[e] = out;
+                }
+                if constexpr (PEER) {
+                    // cell coordinates: sweep axis DIR = cc, lane axis = ia, third = ib
+                    constexpr int LA = DIR == 0 ? 1 : 0, LB = DIR == 2 ? 1 : 2;
+                    int xyz[3];
+                    xyz[DIR] = cc;
+                    xyz[LA] = ia;
+                    xyz[LB] = ib;
+                    peer_store<E>(a.po, xyz[0], xyz[1], xyz[2], outv);
                 }
             }
 #pragma unroll

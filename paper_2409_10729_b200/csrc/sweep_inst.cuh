@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) wave_rate_kernel(const EosArgs a, double3
     if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(red[0]));
 }
 
-template <class M, int DIR, int MODE, int ORD>
+template <class M, int DIR, int MODE, int ORD, bool PEER = false>
 static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     constexpr int NTH = sweep_nth<M, MODE>();
     b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
@@ -74,11 +74,11 @@ static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     const size_t smem = sweep_smem_per_thread<M, MODE>() * NTH;
     static size_t attr = 0;
     if (smem > attr) {
-        cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE, ORD>,
+        cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE, ORD, PEER>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
-    sweep_kernel<M, DIR, MODE, ORD><<<g, b, smem, s>>>(a);
+    sweep_kernel<M, DIR, MODE, ORD, PEER><<<g, b, smem, s>>>(a);
 }
 
 template <class M, int DIR, int ORD>
@@ -108,14 +108,31 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
             } else {
                 launch_ring<M, DIR, M_SET, ORD>(a, g, b, s);
             }
-        } else if (mode == M_RKINIT && M::D == 1) {
-            launch_ring<M, DIR, M_RKINIT, ORD>(a, g, b, s);
+        } else if (mode == M_RKINIT) {
+            if constexpr (M::D == 1) {
+                if (a.po.nf) launch_ring<M, DIR, M_RKINIT, ORD, true>(a, g, b, s);
+                else launch_ring<M, DIR, M_RKINIT, ORD>(a, g, b, s);
+            } else {
+                return cudaErrorInvalidValue;
+            }
         } else {
             return cudaErrorInvalidValue;
         }
     } else {
-        if (mode == M_ACC) launch_ring<M, DIR, M_ACC, ORD>(a, g, b, s);
-        else if (DIR == 1 && mode == M_RKACC) launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
+        if (mode == M_ACC && a.po.nf) {
+            if constexpr (DIR == M::D - 1) launch_ring<M, DIR, M_ACC, ORD, true>(a, g, b, s);
+            else return cudaErrorInvalidValue;   // only the last sweep writes a stage
+        } else if (mode == M_ACC) launch_ring<M, DIR, M_ACC, ORD>(a, g, b, s);
+        else if (DIR == 1 && mode == M_RKACC) {
+            // 2D RK stage: the y sweep is the last one and may carry the fused halo
+            if constexpr (M::D == 2) {
+                if (a.po.nf) launch_ring<M, DIR, M_RKACC, ORD, true>(a, g, b, s);
+                else launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
+            } else {
+                if (a.po.nf) return cudaErrorInvalidValue;
+                launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
+            }
+        }
         else return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -18,6 +18,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MFC_LIB: an alternative in-tree build (same-box A/B timing, tools/build_ab.sh)
 SO_PATH = os.environ.get("MFC_LIB") or os.path.join(_HERE, "libmfc.so")
 
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER = 0, 1, 2
+PEER_BLOB_BYTES = 512
+
 BC_PERIODIC = -1
 BC_REFLECTIVE = -2
 BC_EXTRAPOLATION = -3
@@ -31,6 +34,7 @@ EXPORTED = [
     "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
     "mfc_rk3_steps", "mfc_max_wave_rate", "mfc_cfl_dt",
     "mfc_advance_host", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
+    "mfc_fused_halo_group", "mfc_peer_export", "mfc_peer_import",
     "mfc_nccl_get_unique_id", "mfc_last_launch_count", "mfc_profile_enable", "mfc_profile_read", "mfc_finalize", "mfc_last_error",
     "mfc_version",
 ]
@@ -86,6 +90,9 @@ def _load():
         "mfc_halo_exchange_group": [pp, pp, i32, vp],
         "mfc_rhs_group": [pp, pp, pp, i32, vp],
         "mfc_rk3_step_group": [pp, pp, i32, dbl, vp],
+        "mfc_fused_halo_group": [pp, pp, i32],
+        "mfc_peer_export": [vp, vp, vp],
+        "mfc_peer_import": [vp, i32, vp],
         "mfc_nccl_get_unique_id": [vp],
         "mfc_last_launch_count": [vp],
         "mfc_profile_enable": [vp, i32],
@@ -163,7 +170,7 @@ class Solver:
     """One subdomain (rank) of the 5-equation RHS / SSP-RK3 path on one GPU."""
 
     def __init__(self, problem, *, procs=(1, 1, 1), rank=0, nranks=1, nccl_id: bytes | None = None,
-                 loopback=False, device=None, weno_eps=None, n_global=None):
+                 loopback=False, peer=False, device=None, weno_eps=None, n_global=None):
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
@@ -181,7 +188,8 @@ class Solver:
         pinf = (ctypes.c_double * N)(*problem.pi_inf[:N])
         bc = (ctypes.c_int32 * 6)(*problem.bc)
         comm = _Comm()
-        comm.rank, comm.nranks, comm.loopback = rank, nranks, int(loopback)
+        comm.rank, comm.nranks = rank, nranks
+        comm.loopback = TRANSPORT_PEER if peer else (TRANSPORT_LOOPBACK if loopback else TRANSPORT_NCCL)
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         comm.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id else None
         h = ctypes.c_void_p()
@@ -290,6 +298,30 @@ class Solver:
         _check(lib.mfc_profile_read(self._h, ms, cnt, n), "mfc_profile_read")
         return {k: (ms[i], cnt[i]) for i, k in enumerate(self.KINDS)}
 
+    # ------------------------------------------------------------- fused halo (F1)
+    def peer_export(self, q) -> bytes:
+        """CUDA-IPC handles of q, the RK stage buffers and the flags (mfc_peer_export)."""
+        buf = ctypes.create_string_buffer(PEER_BLOB_BYTES)
+        _check(lib.mfc_peer_export(self._h, _ptr(q), buf), "mfc_peer_export")
+        return buf.raw
+
+    def peer_import(self, face: int, blob: bytes):
+        buf = ctypes.create_string_buffer(blob, PEER_BLOB_BYTES)
+        _check(lib.mfc_peer_import(self._h, int(face), buf), "mfc_peer_import")
+
+    def attach_fused_halo(self, q, group=None):
+        """Collective over the torch.distributed group: register q, exchange the IPC
+        blobs (all_gather_object) and attach every neighbour face; ends with a barrier.
+        Afterwards the RK3 steps write the neighbours' ghost layers directly."""
+        import torch.distributed as dist
+        blob = self.peer_export(q)
+        torch.cuda.synchronize(self.device)
+        blobs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(blobs, blob, group=group)
+        for face, blob_f in face_blobs(self.neighbors, blobs).items():
+            self.peer_import(face, blob_f)
+        dist.barrier(group=group)
+
     def last_launch_count(self) -> int:
         return int(lib.mfc_last_launch_count(self._h))
 
@@ -360,3 +392,17 @@ def halo_exchange_group(solvers, qs, stream=None):
     ps = _arr([q.data_ptr() for q in qs])
     _check(lib.mfc_halo_exchange_group(hs, ps, len(solvers), _stream(stream)),
            "mfc_halo_exchange_group")
+
+
+def face_blobs(neighbors, blobs) -> dict:
+    """{face: the blob of the neighbour rank across that face} (faces without a
+    neighbour rank, neighbors[f] == -1, are skipped)."""
+    return {f: blobs[r] for f, r in enumerate(neighbors) if r >= 0}
+
+
+def fused_halo_group(solvers, qs):
+    """Loopback group: the stage sweeps write the group members' ghost layers directly
+    (mfc_fused_halo_group); qs become the registered state buffers."""
+    hs = _arr([s._h.value for s in solvers])
+    ps = _arr([q.data_ptr() for q in qs])
+    _check(lib.mfc_fused_halo_group(hs, ps, len(solvers)), "mfc_fused_halo_group")

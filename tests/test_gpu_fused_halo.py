@@ -1,0 +1,216 @@
+"""Fused halo on ONE GPU.
+
+* Loopback groups: with mfc_fused_halo_group the last sweep of every RK stage writes
+  the neighbours' ghost layers directly (no pack / copy / unpack); RHS, halo exchange
+  and RK3 steps are BITWISE equal to the exchanged loopback path and to the single
+  domain, for slabs, pencils and 3D blocks, periodic and physical boundaries, 1D-3D.
+* One process per rank with CUDA-IPC peers (transport PEER, no NCCL): two processes
+  share the GPU, attach through mfc_peer_export / mfc_peer_import over a gloo group,
+  order their operations with stream memory operations, and reproduce the single
+  domain bitwise after several RK3 steps.  This exercises the multi-process protocol
+  (handles, flags, epochs) that a multi-GPU run uses, on the one GPU available.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2409_10729_b200 import workloads as W
+
+from parity import oracle_inputs, stable_dt
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2409_10729_b200 import mfc  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _scatter(solvers, q):
+    qs = []
+    for s in solvers:
+        L = s.layout
+        lo, n = L.lo_global, L.n_local
+        qs.append(s.state_from_cons(q[:, lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]]))
+    return qs
+
+
+def _gather(solvers, ts, like):
+    torch.cuda.synchronize()
+    full = np.empty_like(like)
+    for s, t in zip(solvers, ts):
+        L = s.layout
+        lo, n = L.lo_global, L.n_local
+        full[:, lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]] = s.interior(t).cpu().numpy()
+    return full
+
+
+def _group_run(pb, q, procs, dt, nsteps, fused):
+    P = int(np.prod(procs))
+    solvers = [mfc.Solver(pb, procs=procs, rank=r, nranks=P, loopback=True) for r in range(P)]
+    qs = _scatter(solvers, q)
+    if fused:
+        mfc.fused_halo_group(solvers, qs)
+    outs = [s.empty_state() for s in solvers]
+    mfc.rhs_group(solvers, qs, outs)
+    rhs = _gather(solvers, outs, q)
+    mfc.halo_exchange_group(solvers, qs)   # fused: ghosts of the registered states
+    for _ in range(nsteps):
+        mfc.rk3_step_group(solvers, qs, dt)
+    return rhs, _gather(solvers, qs, q), solvers, qs
+
+
+def _single(pb, q, dt, nsteps):
+    s = mfc.Solver(pb)
+    qd = s.state_from_cons(q)
+    r = s.rhs(qd)
+    torch.cuda.synchronize()
+    rhs = s.interior(r).cpu().numpy()
+    for _ in range(nsteps):
+        s.rk3_step(qd, dt)
+    torch.cuda.synchronize()
+    return rhs, s.interior(qd).cpu().numpy()
+
+
+@pytest.mark.parametrize("procs", [(1, 1, 2), (1, 1, 4), (1, 2, 2), (2, 2, 2), (2, 1, 1), (1, 1, 3)])
+def test_fused_group_bitwise_3d(procs):
+    pb = W.random_problem(3, (24, 20, 30), 2, "water")
+    _, v, q = oracle_inputs(pb)
+    dt = stable_dt(pb, v)
+    r_ref, q_ref = _single(pb, q, dt, 4)
+    r_x, q_x, _, _ = _group_run(pb, q, procs, dt, 4, fused=False)
+    r_f, q_f, _, _ = _group_run(pb, q, procs, dt, 4, fused=True)
+    assert np.array_equal(r_f, r_ref) and np.array_equal(r_x, r_ref)
+    assert np.array_equal(q_f, q_ref) and np.array_equal(q_x, q_ref)
+
+
+@pytest.mark.parametrize("ndim,procs,bc", [
+    (1, (3, 1, 1), W.BC_PERIODIC),
+    (1, (2, 1, 1), W.BC_EXTRAPOLATION),
+    (2, (1, 2, 1), W.BC_REFLECTIVE),
+    (2, (2, 2, 1), W.BC_PERIODIC),
+    (3, (1, 1, 4), W.BC_EXTRAPOLATION),
+])
+def test_fused_group_bitwise_dims_and_bcs(ndim, procs, bc):
+    n = {1: (60,), 2: (30, 26), 3: (16, 12, 24)}[ndim]
+    pb = W.random_problem(ndim, n, 3 if ndim == 3 else 2, "gas", bc=(bc,) * 6)
+    _, v, q = oracle_inputs(pb)
+    dt = stable_dt(pb, v)
+    r_ref, q_ref = _single(pb, q, dt, 3)
+    r_f, q_f, _, _ = _group_run(pb, q, procs, dt, 3, fused=True)
+    assert np.array_equal(r_f, r_ref)
+    assert np.array_equal(q_f, q_ref)
+
+
+def test_fused_group_keeps_ghosts_current_and_launches_no_halo_kernels():
+    """After fused steps the registered states' ghost layers hold the neighbours'
+    current boundary cells (what an exchange would write), and a fused RK3 step
+    launches only sweep kernels (3 per stage)."""
+    pb = W.random_problem(3, (16, 12, 18), 2, "water")
+    _, v, q = oracle_inputs(pb)
+    dt = stable_dt(pb, v)
+    _, _, solvers, qs = _group_run(pb, q, (1, 1, 3), dt, 2, fused=True)
+    fused_copy = [t.clone() for t in qs]
+    # an explicit (fused) exchange rewrites the same ghost values
+    mfc.halo_exchange_group(solvers, qs)
+    torch.cuda.synchronize()
+    for s, a, b in zip(solvers, fused_copy, qs):
+        L = s.layout
+        full_a = a.view(L.dims)
+        full_b = b.view(L.dims)
+        g = 3
+        nz = L.n_local[2]
+        for zs in (slice(0, g), slice(g + nz, g + nz + g)):     # z ghost planes
+            ia = full_a[:, zs, g:g + L.n_local[1], 4:4 + L.n_local[0]]
+            ib = full_b[:, zs, g:g + L.n_local[1], 4:4 + L.n_local[0]]
+            assert torch.equal(ia, ib)
+    mfc.rk3_step_group(solvers[:1] + solvers[1:], qs, dt)
+    assert all(s.last_launch_count() == 9 for s in solvers)
+
+
+def test_fused_requires_registered_state():
+    pb = W.random_problem(3, (12, 12, 12), 2, "gas")
+    _, v, q = oracle_inputs(pb)
+    solvers = [mfc.Solver(pb, procs=(1, 1, 2), rank=r, nranks=2, loopback=True) for r in range(2)]
+    qs = _scatter(solvers, q)
+    mfc.fused_halo_group(solvers, qs)
+    other = [t.clone() for t in qs]
+    with pytest.raises(mfc.MfcError, match="ESTATE"):
+        mfc.rk3_step_group(solvers, other, 1e-6)
+
+
+# ------------------------------------------------------------ IPC, 2 processes
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ipc_worker(rank, world, port, procs, nsteps, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch as T
+    T.cuda.set_device(0)
+    from paper_2409_10729_b200 import mfc as M
+    from paper_2409_10729_b200 import workloads as WW
+    from parity import oracle_inputs as oi, stable_dt as sd
+    pb = WW.random_problem(3, (20, 16, 24), 2, "water")
+    _, v, q = oi(pb)
+    dt = sd(pb, v)
+    s = M.Solver(pb, procs=procs, rank=rank, nranks=world, peer=True)
+    L = s.layout
+    lo, n = L.lo_global, L.n_local
+    qd = s.state_from_cons(q[:, lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]])
+    s.attach_fused_halo(qd)
+    rhs = s.rhs(qd)
+    s.halo_exchange(qd)
+    for _ in range(nsteps):
+        s.rk3_step(qd, dt)
+    T.cuda.synchronize()
+    np.save(os.path.join(out_dir, f"rhs{rank}.npy"), s.interior(rhs).cpu().numpy())
+    np.save(os.path.join(out_dir, f"q{rank}.npy"), s.interior(qd).cpu().numpy())
+    np.save(os.path.join(out_dir, f"lo{rank}.npy"), np.array(lo + n))
+    dist.barrier()
+    s.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("procs", [(1, 1, 2), (1, 2, 1)])
+def test_ipc_peer_two_processes_bitwise(procs, tmp_path):
+    import torch.multiprocessing as mp
+    world, nsteps = 2, 3
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, world, port, procs, nsteps, str(tmp_path)))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=240)
+    alive = [p for p in ps if p.is_alive()]
+    for p in alive:
+        p.kill()                      # the exact child processes this test started
+    assert not alive, "IPC peer run timed out"
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+    pb = W.random_problem(3, (20, 16, 24), 2, "water")
+    _, v, q = oracle_inputs(pb)
+    dt = stable_dt(pb, v)
+    r_ref, q_ref = _single(pb, q, dt, nsteps)
+    r_f = np.empty_like(q)
+    q_f = np.empty_like(q)
+    for r in range(world):
+        lo0, lo1, lo2, n0, n1, n2 = np.load(tmp_path / f"lo{r}.npy")
+        sl = (slice(None), slice(lo2, lo2 + n2), slice(lo1, lo1 + n1), slice(lo0, lo0 + n0))
+        r_f[sl] = np.load(tmp_path / f"rhs{r}.npy")
+        q_f[sl] = np.load(tmp_path / f"q{r}.npy")
+    assert np.array_equal(r_f, r_ref)
+    assert np.array_equal(q_f, q_ref)

@@ -249,6 +249,10 @@ def run_ours(args):
         s = mfc.Solver(pb, procs=(1, 1, 1), device=local)
         q = s.state_from_prims(W.c2_prims(pb))
         dt = pb.dt
+    if world > 1 and args.halo == "fused":
+        # F1: stage sweeps store boundary layers into the neighbours' IPC-mapped ghosts
+        s.attach_fused_halo(q)
+        s.halo_exchange(q)
     L = s.layout
     stream = torch.cuda.current_stream()
 
@@ -325,7 +329,8 @@ def run_ours(args):
                    "E": E, "n_fluids": pb.n_fluids, "decomposition": f"procs={list(procs)}",
                    "rhs_per_step": RHS_PER_STEP, "dt": dt,
                    "l2": f"inputs > L2: each state buffer {8 * L.n_elems / 1e9:.2f} GB >> 126 MB, no flush",
-                   "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU"},
+                   "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                   "halo": (args.halo if world > 1 else "none")},
         "hbm_gbs_step": hbm_step,
         "fp64_tflops_step": step_flops / (ms_max / args.steps * 1e-3) / 1e12,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
@@ -388,6 +393,9 @@ def main():
     ap.add_argument("--n", type=int, default=256, help="cells per dimension of the per-GPU block")
     ap.add_argument("--config", default="C3", choices=["C3", "C5", "C2"],
                     help="C3/C4 (default; weak scaling for N > 1), C5 (strong scaling), C2")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "fused"],
+                    help="N>1: NCCL pack/send/recv/unpack, or F1 fused stores into the "
+                         "neighbours' CUDA-IPC-mapped ghost layers")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

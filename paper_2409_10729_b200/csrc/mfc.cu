@@ -1195,6 +1195,8 @@ int mfc_advance_host(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
         return MFC_OK;
     };
     if ((st = copy(true))) return st;
+    // fused halo: the ghost layers of a freshly written state come from one exchange
+    if (c->fused && (st = exchange(&c, &q_dev, 1, s))) return st;
     if ((st = mfc_rk3_steps(c, q_dev, dt, nsteps, stream))) return st;
     if ((st = copy(false))) return st;
     CU_TRY(cudaStreamSynchronize(s));
@@ -1259,10 +1261,11 @@ int mfc_fused_halo_group(mfc_ctx* const* cs, double* const* qs, int32_t count) {
 
 int mfc_peer_export(mfc_ctx* c, double* q, void* blob) {
     if (!c || !blob) return fail(MFC_EINVAL, "NULL argument");
-    int st;
-    if ((st = need_ws(c, true)) || (st = check_ptr(q, "q")) || (st = set_device(c))) return st;
     if (c->transport == MFC_TRANSPORT_LOOPBACK)
         return fail(MFC_EINVAL, "loopback contexts attach with mfc_fused_halo_group");
+    if (c->nranks < 2) return fail(MFC_EINVAL, "a single-rank context has no peers");
+    int st;
+    if ((st = need_ws(c, true)) || (st = check_ptr(q, "q")) || (st = set_device(c))) return st;
     if ((st = drv("cuDeviceGet", &p_dev_get)) || (st = drv("cuDeviceGetAttribute", &p_dev_attr)) ||
         (st = drv("cuMemGetAddressRange", &p_addr_range)) ||
         (st = drv("cuStreamWaitValue64", &p_wait_value)) ||

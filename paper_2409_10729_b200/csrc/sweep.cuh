@@ -91,16 +91,20 @@ struct PeerOut {
     PeerFace f[6];
 };
 
+// Copy my just-written result cell (src, equation stride sE) to every neighbour whose
+// face it lies next to.  Called for the few boundary cells only (the values are read
+// back from the store just made -- L2 hits -- instead of being kept live in registers
+// through the march).
 template <int E>
-__device__ __forceinline__ void peer_store(const PeerOut& po, int x, int y, int z,
-                                           const double (&v)[E]) {
+__device__ __forceinline__ void peer_copy(const PeerOut& po, int x, int y, int z, const double* src,
+                                       int64_t sE) {
     for (int i = 0; i < po.nf; ++i) {
         const PeerFace& p = po.f[i];
         const int ck = p.dim == 0 ? x : (p.dim == 1 ? y : z);
         if (ck < p.lo || ck >= p.hi) continue;
         double* d = p.dst + p.off + x + (int64_t)y * p.sy + (int64_t)z * p.sz;
 #pragma unroll
-        for (int e = 0; e < E; ++e) d[e * p.sE] = v[e];
+        for (int e = 0; e < E; ++e) d[e * p.sE] = src[e * sE];
     }
 }
 
@@ -181,6 +185,18 @@ sweep_kernel(const SweepArgs a) {
     const int s1 = min(s0 + a.T, a.nS);   // cells s0 .. s1-1 are updated
     const int64_t line = a.base + (int64_t)ia * a.sA + (int64_t)ib * a.sB;
     const double* __restrict__ q = a.q;
+    // fused halo: does my line touch a shared face (tangential faces: the whole line;
+    // faces normal to the sweep: the 3 end cells of the line)?
+    bool peer_line = false, peer_ends = false;
+    if constexpr (PEER) {
+        constexpr int LA = DIR == 0 ? 1 : 0, LB = DIR == 2 ? 1 : 2;
+        for (int i = 0; i < a.po.nf; ++i) {
+            const PeerFace& p = a.po.f[i];
+            if (p.dim == DIR) peer_ends = true;
+            else if (p.dim == LA) peer_line |= ia >= p.lo && ia < p.hi;
+            else if (p.dim == LB) peer_line |= ib >= p.lo && ib < p.hi;
+        }
+    }
 
     auto fetch = [&](double* ring, int slot, const double* src, int cell) {
         const int sc = map_cell(cell, a.nS, a.gm);
@@ -261,7 +277,6 @@ sweep_kernel(const SweepArgs a) {
                 const int cc = j - 1;
                 const int64_t c = line + (int64_t)cc * a.sS;
                 const double du = uf - uf_prev;
-                double outv[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     double r = F_prev[e] - F[e];                 // dx * c_e
@@ -279,16 +294,17 @@ sweep_kernel(const SweepArgs a) {
                                   : fma(a.w * a.invd, r, base);
                     }
                     a.dst[c + e * a.sE] = out;
-                    outv[e] = out;
                 }
                 if constexpr (PEER) {
-                    // cell coordinates: sweep axis DIR = cc, lane axis = ia, third = ib
-                    constexpr int LA = DIR == 0 ? 1 : 0, LB = DIR == 2 ? 1 : 2;
-                    int xyz[3];
-                    xyz[DIR] = cc;
-                    xyz[LA] = ia;
-                    xyz[LB] = ib;
-                    peer_store<E>(a.po, xyz[0], xyz[1], xyz[2], outv);
+                    if (peer_line || (peer_ends && (cc < 3 || cc >= a.nS - 3))) {
+                        // cell coordinates: sweep axis DIR = cc, lane axis = ia, third = ib
+                        constexpr int LA = DIR == 0 ? 1 : 0, LB = DIR == 2 ? 1 : 2;
+                        int xyz[3];
+                        xyz[DIR] = cc;
+                        xyz[LA] = ia;
+                        xyz[LB] = ib;
+                        peer_copy<E>(a.po, xyz[0], xyz[1], xyz[2], a.dst + c, a.sE);
+                    }
                 }
             }
 #pragma unroll

@@ -156,3 +156,66 @@ def test_new_entry_points_validate_arguments(mfc):
 def test_ndim_needs_three_cells(mfc):
     rc, msg = _init(mfc, W.Problem("tiny", 2, 2, (8, 2, 1), gamma=(1.4, 1.4), pi_inf=(0, 0)))
     assert rc == -1 and "< 3" in msg
+
+
+def _ctx(mfc, pb, procs, rank, nranks, transport):
+    g = mfc._Grid()
+    g.ndim = pb.ndim
+    for k in range(3):
+        g.n_global[k] = pb.n[k]
+        g.lo[k], g.hi[k] = pb.lo[k], pb.hi[k]
+        g.procs[k] = procs[k]
+    N = pb.n_fluids
+    gam = (ctypes.c_double * N)(*pb.gamma)
+    pi = (ctypes.c_double * N)(*pb.pi_inf)
+    b = (ctypes.c_int32 * 6)(*pb.bc)
+    c = mfc._Comm()
+    c.rank, c.nranks, c.loopback = rank, nranks, transport
+    h = ctypes.c_void_p()
+    rc = mfc.lib.mfc_init(ctypes.byref(h), ctypes.byref(g), N, gam, pi, b, ctypes.byref(c), 0)
+    return rc, h
+
+
+def test_fused_halo_entry_points_validate_arguments(mfc):
+    """mfc_fused_halo_group / mfc_peer_export / mfc_peer_import reject bad use before
+    touching the GPU; the group attach itself is host bookkeeping."""
+    pb = W.random_problem(3, (12, 12, 12), 2, "gas")
+    assert _ctx(mfc, pb, (1, 1, 2), 0, 2, 3)[0] == -1                 # unknown transport
+    hs = []
+    for r in range(2):
+        rc, h = _ctx(mfc, pb, (1, 1, 2), r, 2, mfc.TRANSPORT_LOOPBACK)
+        assert rc == 0
+        hs.append(h)
+    try:
+        H = (ctypes.c_void_p * 2)(*[h.value for h in hs])
+        Q = (ctypes.c_void_p * 2)(256, 512)
+        assert mfc.lib.mfc_fused_halo_group(H, Q, 2) == -5              # no workspace
+        lay = mfc._Layout()
+        mfc.lib.mfc_get_layout(hs[0], ctypes.byref(lay))
+        for h in hs:     # a fake aligned address: binding only records the split
+            assert mfc.lib.mfc_bind_workspace(h, ctypes.c_void_p(1 << 20), lay.workspace_bytes) == 0
+        Qbad = (ctypes.c_void_p * 2)(256, 0)
+        assert mfc.lib.mfc_fused_halo_group(H, Qbad, 2) == -1           # NULL q
+        assert mfc.lib.mfc_fused_halo_group(H, Q, 1) == -1              # group lacks rank 1
+        assert mfc.lib.mfc_fused_halo_group(H, Q, 2) == 0
+        blob = ctypes.create_string_buffer(mfc.PEER_BLOB_BYTES)
+        assert mfc.lib.mfc_peer_export(hs[0], ctypes.c_void_p(256), blob) == -1   # loopback
+        assert mfc.lib.mfc_peer_import(hs[0], 0, blob) == -1           # x face: no neighbour
+    finally:
+        for h in hs:
+            mfc.lib.mfc_finalize(h)
+    rc, h = _ctx(mfc, pb, (1, 1, 2), 0, 2, mfc.TRANSPORT_PEER)           # no NCCL needed
+    assert rc == 0
+    try:
+        blob = ctypes.create_string_buffer(mfc.PEER_BLOB_BYTES)
+        assert mfc.lib.mfc_peer_import(h, 4, blob) == -5                # export first
+        assert mfc.lib.mfc_peer_import(h, 7, blob) == -1                # bad face
+        assert mfc.lib.mfc_peer_export(h, ctypes.c_void_p(256), blob) == -5   # no workspace
+    finally:
+        mfc.lib.mfc_finalize(h)
+
+
+def test_face_blobs_routes_each_face_to_its_neighbour(mfc):
+    blobs = [b"r0", b"r1", b"r2", b"r3"]
+    assert mfc.face_blobs((-1, -1, 2, 2, 1, 3), blobs) == {2: b"r2", 3: b"r2", 4: b"r1", 5: b"r3"}
+    assert mfc.face_blobs((-1,) * 6, blobs) == {}

@@ -127,17 +127,26 @@ struct SweepArgs {
     PeerOut po;                     // fused halo stores (last sweep of a stage only)
 };
 
-// Per-thread shared-memory rings for the streamed operands (filled by cp.async two
+// Per-thread shared-memory rings for the streamed operands (filled by cp.async PD
 // march steps ahead of use; element (slot, e) of thread t at [(slot*E + e)*nthreads + t],
 // so a warp's copies and reads are contiguous 256-byte rows):
 //   state ring : cells j+2 .. j+4 (RK y sweep: j-1 .. j+4, the stage operand q^s(j-1)
 //                is the state already streamed three steps earlier);
 //   acc / q^n rings : cells j-1 .. j+1.
+#ifndef MFC_RING_PD
+#define MFC_RING_PD 2    // prefetch distance of the rings, in march steps
+#endif
 template <int MODE>
 struct Rings {
-    static constexpr int QS = (MODE == M_RKACC || MODE == M_RKINIT) ? 6 : 3;
-    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC) ? 3 : 0;
-    static constexpr int NS = (MODE == M_RKACC || MODE == M_RKINIT) ? 3 : 0;
+    static constexpr int PD = MFC_RING_PD;
+    static constexpr bool RK = MODE == M_RKACC || MODE == M_RKINIT;
+    // state cell c lives from its fetch (step c-2-PD) to its conversion (step c-2), or
+    // to its use as the stage operand q^s (step c+1); operands of cell c from step
+    // c+1-PD to step c+1
+    static constexpr int QS = RK ? PD + 4 : PD + 1;
+    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC) ? PD + 1 : 0;
+    static constexpr int NS = RK ? PD + 1 : 0;
+    static constexpr int OS = PD + 1;   // operand ring length (AS or NS when present)
     static constexpr int SLOTS = QS + AS + NS;
 };
 
@@ -204,8 +213,9 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
         for (int e = 0; e < E; ++e) cp_async8(&at(ring, slot, e), p + e * a.sE);
     };
-    // group for step j: state of cell j+2 -> state slot sq, epilogue operands of cell
-    // j-1 -> operand slot sa.  Slots: state cell c at (c+3) % QS, operands at (c+3) % 3.
+    // group for step j (issued PD steps earlier): state of cell j+2 -> state slot sq,
+    // epilogue operands of cell j-1 -> operand slot sa.  Slots: state cell c at
+    // (c+3) % QS, operands at (c+3) % OS.
     auto issue = [&](int j, int sq, int sa) {
         if (j + 2 <= s1 + 2) fetch(ringQ, sq, q, j + 2);
         const int c = j - 1;
@@ -227,30 +237,31 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
             for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
             if (map_flip(s0 - 4 + k, a.nS, a.gm)) qc[M::IM + DIR] = -qc[M::IM + DIR];
-            if (R::QS == 6) {                         // keep for the q^s epilogue operand
+            if (R::RK) {                              // keep for the q^s epilogue operand
 #pragma unroll
                 for (int e = 0; e < E; ++e) at(ringQ, (s0 - 4 + k + 3) % R::QS, e) = qc[e];
             }
             cons_to_prim_fast<M>(qc, w[k], a.mat);
         }
     }
-    issue(s0 - 1, (s0 + 4) % R::QS, (s0 + 1) % 3);
-    issue(s0, (s0 + 5) % R::QS, (s0 + 2) % 3);
-    // rotating slots at step j: conversion (cell j+2), fetch (cell j+4), q^s (cell j-1),
-    // operands of cell j-1, operand fetch (cell j+1)
+#pragma unroll
+    for (int i = 0; i < R::PD; ++i) issue(s0 - 1 + i, (s0 + 4 + i) % R::QS, (s0 + 1 + i) % R::OS);
+    // rotating slots at step j: conversion (cell j+2), fetch (cell j+2+PD), q^s (cell
+    // j-1), operands of cell j-1, operand fetch (cell j-1+PD)
     int kq = (s0 + 4) % R::QS;
-    int kqf = (s0 + 6) % R::QS;
+    int kqf = (s0 + 4 + R::PD) % R::QS;
     int kqs = (s0 + 1) % R::QS;
-    int ka = (s0 + 1) % 3;
-    int kaf = (s0 + 3) % 3;
+    int ka = (s0 + 1) % R::OS;
+    int kaf = (s0 + 1 + R::PD) % R::OS;
 
     double vm_prev[E];     // v-_{j-1/2} (from cell j-1)
     double F_prev[E];      // flux at face j-3/2
     double uf_prev = 0.0;
 
     for (int j = s0 - 1; j <= s1; ++j) {
-        cp_async_wait_1();                             // group of step j has landed
-        issue(j + 2, kqf, kaf);
+        if constexpr (R::PD == 2) cp_async_wait_1();   // group of step j has landed
+        else cp_async_wait_all();
+        issue(j + R::PD, kqf, kaf);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
 #pragma unroll
@@ -316,8 +327,8 @@ sweep_kernel(const SweepArgs a) {
         kq = inc(kq, R::QS);
         kqf = inc(kqf, R::QS);
         kqs = inc(kqs, R::QS);
-        ka = inc(ka, 3);
-        kaf = inc(kaf, 3);
+        ka = inc(ka, R::OS);
+        kaf = inc(kaf, R::OS);
     }
     cp_async_wait_all();
 }

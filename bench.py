@@ -208,13 +208,20 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    peer = world > 1 and args.halo == "peer"
+    if args.same_device:      # protocol check only: every rank on GPU 0 (time-sliced)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if peer:   # no NCCL anywhere: gloo plumbing, halos as IPC peer stores
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if peer else dev
 
     n = args.n
-    nid = mfc.broadcast_unique_id() if world > 1 else None
+    nid = mfc.broadcast_unique_id() if world > 1 and not peer else None
     procs = (1, 1, world)
     if args.config == "C3":
         block = W.c3_droplet(n)                  # the per-GPU block (C3 / C4)
@@ -224,7 +231,8 @@ def run_ours(args):
         else:
             pb = W.c3_droplet(n, nz=n * world)   # global domain: blocks stacked along z
             workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
-        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local)
+        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
+                       peer=peer)
         # every rank holds the same C3 block (its local prims), converted on the GPU
         q = s.state_from_prims(W.c3_prims(block))
         dt = block.dt
@@ -232,7 +240,8 @@ def run_ours(args):
         nn = args.n if args.n != 256 else 512
         pb = W.c5_three_fluid(nn)                # strong scaling: fixed 512^3 split in z-slabs
         workload = f"C5 3D three-fluid shock-droplet {nn}^3 total, z-slabs x{world} (BASELINE configs[4])"
-        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local)
+        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
+                       peer=peer)
         L0 = s.layout
         v = s.empty_state()
         vi = s.interior(v)
@@ -249,7 +258,7 @@ def run_ours(args):
         s = mfc.Solver(pb, procs=(1, 1, 1), device=local)
         q = s.state_from_prims(W.c2_prims(pb))
         dt = pb.dt
-    if world > 1 and args.halo == "fused":
+    if world > 1 and args.halo in ("fused", "peer"):
         # F1: stage sweeps store boundary layers into the neighbours' IPC-mapped ghosts
         s.attach_fused_halo(q)
         s.halo_exchange(q)
@@ -284,7 +293,7 @@ def run_ours(args):
     prof = s.profile_read()
     s.profile(False)
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -330,7 +339,9 @@ def run_ours(args):
                    "rhs_per_step": RHS_PER_STEP, "dt": dt,
                    "l2": f"inputs > L2: each state buffer {8 * L.n_elems / 1e9:.2f} GB >> 126 MB, no flush",
                    "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
-                   "halo": (args.halo if world > 1 else "none")},
+                   "halo": (args.halo if world > 1 else "none"),
+                   **({"same_device": "all ranks on GPU 0: protocol check, time-sliced, not a "
+                                      "scaling number"} if args.same_device else {})},
         "hbm_gbs_step": hbm_step,
         "fp64_tflops_step": step_flops / (ms_max / args.steps * 1e-3) / 1e12,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
@@ -364,7 +375,7 @@ def run_ours(args):
         for _ in range(ke):
             s.advance_host(qh_in, qh_out, q, 1, dt)
         wall = time.perf_counter() - t0
-        tw = torch.tensor([wall], dtype=torch.float64, device=dev)
+        tw = torch.tensor([wall], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         nb = int(qh_in.numel() * 8)
@@ -390,12 +401,17 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=256, help="cells per dimension of the per-GPU block")
+    ap.add_argument("--n", "--cells", dest="n", type=int, default=256,
+                    help="cells per dimension of the per-GPU block")
     ap.add_argument("--config", default="C3", choices=["C3", "C5", "C2"],
                     help="C3/C4 (default; weak scaling for N > 1), C5 (strong scaling), C2")
-    ap.add_argument("--halo", default="nccl", choices=["nccl", "fused"],
-                    help="N>1: NCCL pack/send/recv/unpack, or F1 fused stores into the "
-                         "neighbours' CUDA-IPC-mapped ghost layers")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "fused", "peer"],
+                    help="N>1: NCCL pack/send/recv/unpack; 'fused': F1 stores into the "
+                         "neighbours' CUDA-IPC-mapped ghost layers (NCCL kept for the "
+                         "plumbing); 'peer': the same with gloo plumbing and no NCCL")
+    ap.add_argument("--same-device", action="store_true",
+                    help="put every rank on GPU 0 (multi-process protocol check on one GPU; "
+                         "its timings are time-sliced and not a scaling number)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

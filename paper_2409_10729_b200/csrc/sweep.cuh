@@ -187,8 +187,13 @@ sweep_kernel(const SweepArgs a) {
     double* const ringN = ringA + R::AS * E * nth;          // NS slots
     auto at = [&](double* ring, int slot, int e) -> double& { return ring[(slot * E + e) * nth]; };
 
-    const int ia = blockIdx.x * blockDim.x + threadIdx.x;
-    const int ib = blockIdx.y * blockDim.y + threadIdx.y;
+    // warp-lines (32 consecutive lines along the lane axis A) are numbered A-chunk
+    // fastest, and a block's warps take consecutive warp-lines: 2D / 1D grids (nB == 1)
+    // fill all warps of a block too
+    const int nAw = (a.nA + 31) >> 5;
+    const int wl = blockIdx.x * (nth >> 5) + threadIdx.y;
+    const int ia = (wl % nAw) * 32 + threadIdx.x;
+    const int ib = wl / nAw;
     if (ia >= a.nA || ib >= a.nB) return;                   // no block-level sync below
     const int s0 = blockIdx.z * a.T;
     const int s1 = min(s0 + a.T, a.nS);   // cells s0 .. s1-1 are updated

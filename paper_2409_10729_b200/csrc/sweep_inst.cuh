@@ -70,7 +70,8 @@ template <class M, int DIR, int MODE, int ORD, bool PEER = false>
 static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     constexpr int NTH = sweep_nth<M, MODE>();
     b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
-    g = dim3((a.nA + 31) / 32, (a.nB + b.y - 1) / b.y, g.z);
+    const int64_t warp_lines = (int64_t)((a.nA + 31) / 32) * a.nB;
+    g = dim3((unsigned)((warp_lines + b.y - 1) / b.y), 1, g.z);
     const size_t smem = sweep_smem_per_thread<M, MODE>() * NTH;
     static size_t attr = 0;
     if (smem > attr) {
@@ -86,9 +87,15 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
     if constexpr (DIR == 0) {
         if (mode == M_SET) {
             if constexpr (M::D >= 2) {
-              if (!getenv("MFC_X_STAGED")) {
+              // row-parallel kernel while a row fits 8 warps (two resident blocks per SM);
+              // longer rows (one 16-warp block per SM, or split rows with serial boundary
+              // passes) go to the staged march, measured faster there (C2, C5: r45)
+              static const int xrows = getenv("MFC_X_ROWS") ? atoi(getenv("MFC_X_ROWS")) : -1;
+              const bool rows = xrows >= 0 ? xrows != 0 : a.nS <= 256;
+              if (rows && !getenv("MFC_X_STAGED")) {
                 // row-parallel x sweep: W warps per row segment, shared tables only
-                const int W = (int)std::min<int64_t>(16, (a.nS + 31) / 32);
+                static const int wmax = getenv("MFC_XW") ? atoi(getenv("MFC_XW")) : 16;
+                const int W = (int)std::min<int64_t>(wmax, (a.nS + 31) / 32);
                 const int nseg = (a.nS + 32 * W - 1) / (32 * W);
                 const size_t smem = sizeof(double) *
                     ((size_t)(W + 2) * 4 * M::E + (size_t)(W + 1) * M::E +

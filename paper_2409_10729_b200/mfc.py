@@ -102,6 +102,8 @@ def _load():
         "mfc_version": [],
     }
     for name, args in sig.items():
+        if os.environ.get("MFC_LIB") and not hasattr(L, name):
+            continue                   # an older A/B build lacks newer entry points
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int

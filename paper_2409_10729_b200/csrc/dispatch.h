@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "sweep.cuh"
 
 namespace mfc {
@@ -12,6 +14,15 @@ namespace mfc {
 template <int N>
 cudaError_t launch_sweep(int D, int DIR, int mode, int order, const SweepArgs& a, dim3 grid,
                          dim3 block, cudaStream_t s);
+
+// Does the x sweep of a row of n cells use the row-parallel kernel (else the staged
+// march)?  MFC_X_ROWS=0/1 and MFC_X_STAGED override (measurements).
+inline bool x_rows_used(int n) {
+    static const int xr = getenv("MFC_X_ROWS") ? atoi(getenv("MFC_X_ROWS")) : -1;
+    static const bool staged = getenv("MFC_X_STAGED") != nullptr;
+    if (staged) return false;
+    return xr >= 0 ? xr != 0 : n <= 256;
+}
 
 struct EosArgs {
     const double* in;

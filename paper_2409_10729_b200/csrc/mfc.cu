@@ -91,6 +91,7 @@ struct mfc_ctx {
     int64_t launches = 0;
     int seg = 0;  // sweep segment length override (0 = heuristic)
     int seg_dir[3] = {0, 0, 0};  // per-direction overrides (MFC_SEG_X/Y/Z)
+    bool xbase = true;           // RK base in the row-parallel x sweep (MFC_XBASE=0: off)
     // optional per-launch CUDA-event timing (mfc_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -550,7 +551,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     a.nA = (int32_t)c->nl[la];
     a.nB = (int32_t)c->nl[lb];
     // resident warps per SM: 12 for the non-RK ring sweeps with E <= 8 (3 blocks), else 8
-    const bool three = c->E <= 8 && dir > 0 && mode == M_ACC;
+    const bool three = c->E <= 8 && dir > 0 && (mode == M_ACC || mode == M_ACCN);
     a.T = seg_len(c, dir, three ? 12 : 8);
     // physical faces are applied by index mapping inside the sweep; faces shared with
     // another rank read the ghost layers the halo exchange wrote
@@ -616,8 +617,14 @@ int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const
         }
         const bool last = dir == c->D - 1;
         double* out = last ? dst : acc;
+        // RK stage assembly (2D/3D): with the row-parallel x sweep, x writes
+        // cb*q^s + w*c_x (its own cells, coalesced), the middle sweep adds w*c_y and the
+        // last one w*c + ca*q^n (M_ACCN, stages 2-3); with the staged x sweep, x writes
+        // c_x and the y sweep assembles the base (M_RKACC)
+        const bool xb = rk && c->D >= 2 && c->xbase && x_rows_used((int)c->nl[0]);
         int mode;
-        if (dir == 0) mode = (rk && c->D == 1) ? M_RKINIT : M_SET;
+        if (dir == 0) mode = (rk && (c->D == 1 || xb)) ? M_RKINIT : M_SET;
+        else if (xb) mode = (last && ca != 0.0) ? M_ACCN : M_ACC;
         else if (dir == 1 && rk) mode = M_RKACC;
         else mode = M_ACC;
         // M_SET in an RK stage writes the unscaled c_x; M_RKACC scales (acc + c_y) by w
@@ -924,6 +931,7 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
     }
     c->ws_need = need;
     if (const char* sg = getenv("MFC_SEG")) c->seg = atoi(sg);
+    if (const char* xb = getenv("MFC_XBASE")) c->xbase = atoi(xb) != 0;
     const char* segenv[3] = {"MFC_SEG_X", "MFC_SEG_Y", "MFC_SEG_Z"};
     for (int k = 0; k < 3; ++k)
         if (const char* sg = getenv(segenv[k])) c->seg_dir[k] = atoi(sg);

@@ -24,6 +24,8 @@
 //   M_RKINIT: dst = ca*q^n + cb*q^s + w*c             (1D: the only sweep, RK stage)
 //   M_RKACC : dst = ca*q^n + cb*q^s + w*(acc + c)     (y sweep, RK stage)
 //   M_ACC   : dst = acc + w*c                         (y sweep of a RHS, z sweep)
+//   M_ACCN  : dst = acc + w*c + ca*q^n                (last sweep of an RK stage when the
+//                                                      row-parallel x sweep wrote cb*q^s + w*c_x)
 // so the SSP-RK3 stage q^(s+1) = ca q^n + cb (q^s + dt (c_x + c_y + c_z)) (S4) is
 // assembled across the sweeps; the extra operands q^s, q^n are streamed by the y sweep,
 // whose warp accesses are contiguous rows, never by the x sweep, whose lanes own
@@ -37,7 +39,7 @@
 
 namespace mfc {
 
-enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3 };
+enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3, M_ACCN = 4 };
 
 // Reconstruction of one variable of the window's centre cell (ORD = 5: cells w0..w4,
 // ORD = 3: the inner three).
@@ -138,14 +140,15 @@ struct SweepArgs {
 #endif
 template <int MODE>
 struct Rings {
-    static constexpr int PD = MFC_RING_PD;
+    // M_ACCN streams three operands: prefetch distance 1 keeps it at 48 KB per block
+    static constexpr int PD = MODE == M_ACCN ? 1 : MFC_RING_PD;
     static constexpr bool RK = MODE == M_RKACC || MODE == M_RKINIT;
     // state cell c lives from its fetch (step c-2-PD) to its conversion (step c-2), or
     // to its use as the stage operand q^s (step c+1); operands of cell c from step
     // c+1-PD to step c+1
     static constexpr int QS = RK ? PD + 4 : PD + 1;
-    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC) ? PD + 1 : 0;
-    static constexpr int NS = RK ? PD + 1 : 0;
+    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC || MODE == M_ACCN) ? PD + 1 : 0;
+    static constexpr int NS = (RK || MODE == M_ACCN) ? PD + 1 : 0;
     static constexpr int OS = PD + 1;   // operand ring length (AS or NS when present)
     static constexpr int SLOTS = QS + AS + NS;
 };
@@ -171,7 +174,7 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 // non-RK modes for E <= 8); 2 blocks otherwise.
 template <class M, int MODE>
 __host__ __device__ constexpr int sweep_min_blocks() {
-    return ((MODE == M_ACC || MODE == M_SET) && M::E <= 8) ? MFC_ACC_MINB : 2;
+    return ((MODE == M_ACC || MODE == M_SET || MODE == M_ACCN) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
@@ -300,6 +303,8 @@ sweep_kernel(const SweepArgs a) {
                     double out;
                     if (MODE == M_SET) out = r * a.invd;
                     else if (MODE == M_ACC) out = fma(a.w * a.invd, r, at(ringA, ka, e));
+                    else if (MODE == M_ACCN)
+                        out = fma(a.ca, at(ringN, ka, e), fma(a.w * a.invd, r, at(ringA, ka, e)));
                     else {
                         const double qs = at(ringQ, kqs, e);
                         const double base = a.ca != 0.0
@@ -487,7 +492,10 @@ namespace mfc {
 // (boundary-mapped) ghost cells, which are the right stencil halo.
 // ---------------------------------------------------------------------------
 
-template <class M, int ORD>
+// RKB = true (first sweep of a 2D/3D RK stage): dst = cb*q^s + w*c_x, the stage's
+// q^s term taken from the cell this thread converted (re-read, an L1/L2 hit); the later
+// sweeps add w*c_y (M_ACC) and w*c_z + ca*q^n (M_ACCN).
+template <class M, int ORD, bool RKB>
 __global__ void __launch_bounds__(512, 1)
 sweep_x_rows(const SweepArgs a, int W) {
     constexpr int E = M::E;
@@ -642,11 +650,15 @@ sweep_x_rows(const SweepArgs a, int W) {
     }
     if (x < x1) {
         const double du = ufR - uf;
+        const double wi = a.w * a.invd;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             double r = F[e] - FR[e];
             if (e >= M::IA) r = fma(v[e], du, r);
-            a.dst[row + x + e * a.sE] = r * a.invd;
+            if constexpr (RKB)
+                a.dst[row + x + e * a.sE] = fma(wi, r, a.cb * __ldg(a.q + row + x + e * a.sE));
+            else
+                a.dst[row + x + e * a.sE] = r * a.invd;
         }
     }
 }

@@ -85,23 +85,23 @@ static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
 template <class M, int DIR, int ORD>
 static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     if constexpr (DIR == 0) {
-        if (mode == M_SET) {
+        if (mode == M_SET || (mode == M_RKINIT && M::D >= 2)) {
             if constexpr (M::D >= 2) {
               // row-parallel kernel while a row fits 8 warps (two resident blocks per SM);
               // longer rows (one 16-warp block per SM, or split rows with serial boundary
-              // passes) go to the staged march, measured faster there (C2, C5: r45)
-              static const int xrows = getenv("MFC_X_ROWS") ? atoi(getenv("MFC_X_ROWS")) : -1;
-              const bool rows = xrows >= 0 ? xrows != 0 : a.nS <= 256;
-              if (rows && !getenv("MFC_X_STAGED")) {
-                // row-parallel x sweep: W warps per row segment, shared tables only
+              // passes) go to the staged march, measured faster there (C2, C5: r45).
+              // The host asks x_rows_used() before choosing M_RKINIT (x_rows only).
+              if (x_rows_used(a.nS)) {
                 static const int wmax = getenv("MFC_XW") ? atoi(getenv("MFC_XW")) : 16;
                 const int W = (int)std::min<int64_t>(wmax, (a.nS + 31) / 32);
                 const int nseg = (a.nS + 32 * W - 1) / (32 * W);
                 const size_t smem = sizeof(double) *
                     ((size_t)(W + 2) * 4 * M::E + (size_t)(W + 1) * M::E +
                      (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E);
-                sweep_x_rows<M, ORD><<<dim3(nseg, a.nA, a.nB), 32 * W, smem, s>>>(a, W);
-              } else {
+                const dim3 gr(nseg, a.nA, a.nB);
+                if (mode == M_SET) sweep_x_rows<M, ORD, false><<<gr, 32 * W, smem, s>>>(a, W);
+                else sweep_x_rows<M, ORD, true><<<gr, 32 * W, smem, s>>>(a, W);
+              } else if (mode == M_SET) {
                 // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
                 const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
                 static size_t attr = 0;
@@ -111,6 +111,8 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                     attr = smem;
                 }
                 sweep_x_staged<M, ORD><<<g, b, smem, s>>>(a);
+              } else {
+                return cudaErrorInvalidValue;
               }
             } else {
                 launch_ring<M, DIR, M_SET, ORD>(a, g, b, s);
@@ -130,6 +132,14 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
             if constexpr (DIR == M::D - 1) launch_ring<M, DIR, M_ACC, ORD, true>(a, g, b, s);
             else return cudaErrorInvalidValue;   // only the last sweep writes a stage
         } else if (mode == M_ACC) launch_ring<M, DIR, M_ACC, ORD>(a, g, b, s);
+        else if (mode == M_ACCN) {
+            if constexpr (DIR == M::D - 1) {
+                if (a.po.nf) launch_ring<M, DIR, M_ACCN, ORD, true>(a, g, b, s);
+                else launch_ring<M, DIR, M_ACCN, ORD>(a, g, b, s);
+            } else {
+                return cudaErrorInvalidValue;
+            }
+        }
         else if (DIR == 1 && mode == M_RKACC) {
             // 2D RK stage: the y sweep is the last one and may carry the fused halo
             if constexpr (M::D == 2) {

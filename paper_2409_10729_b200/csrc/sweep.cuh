@@ -476,184 +476,137 @@ sweep_x_staged(const SweepArgs a) {
 namespace mfc {
 
 // ---------------------------------------------------------------------------
-// x sweep, row-parallel form (2D/3D, epilogue M_SET).
+// x sweep, row-parallel tile form (2D/3D, epilogue M_SET or the RK stage base).
 //
-// A block owns a row segment of 32*W consecutive cells [x0, x1) of one (y, z) row;
-// warp w owns cells x0+32w .. x0+32w+31, lane l one cell.  Loads and stores are
-// contiguous along x.  Each lane converts its cell (S2); the WENO stencil
-// neighbours come from lanes l-2..l+2 by warp shuffles and, across warp borders,
-// from a small shared-memory table each warp fills with its two first / last cells.
-// Lane l computes the face x-1/2 (HLLC) from v-(x-1) (shuffle / shared memory) and its
-// own v+; the cell update takes F(x+1/2) from lane l+1.  No register window, no
-// transpose, every face computed once.  Segment ends: for a periodic row that fits
-// in one block the face at x = -1/2 IS the face at x = n-1/2 (shared through shared
-// memory); otherwise warp 0 reconstructs the two boundary cells x0-1 (v-) and x1
-// (v+) in one extra pass.  Cells of the last warp beyond the row end hold the
-// (boundary-mapped) ghost cells, which are the right stencil halo.
+// A block owns the row segment [x0, x0+32W) of one (y, z) row (W <= 8 warps; one
+// block per row up to 256 cells), thread t the cell x0+t: loads and stores are
+// contiguous along x, no transpose, no register window, every face computed once.
+// Every exchange between cells goes through one shared-memory row per quantity,
+// indexed by cell:
+//   V  [E][seg+6] : primitives of cells x0-3 .. x0+seg+2 (6 halo cells loaded by
+//                   threads 0..5, boundary-mapped like every other cell);
+//   VM [E][seg+2] : v-_{m+1/2} of cells x0-1 .. x0+seg;
+//   FS [E+1][seg+1]: F and u^f of faces x0-1/2 .. x0+seg-1/2 (aliases V, dead by then).
+// WENO reads its four stencil neighbours as four conflict-free row loads per variable
+// (no warp borders, no lane-indexed selects: r48's shuffle form spent ~20 extra
+// instructions per variable on them); the face x-1/2 takes v-(x-1) from VM, the cell
+// update F(x+1/2) from FS.  A whole periodic row wraps by index (face -1/2 = face
+// n-1/2); otherwise 2E threads of the last warp reconstruct the two boundary cells
+// x0-1 (v-) and x0+seg (v+), one variable each, and one thread the face x0+seg-1/2.
+// Nothing but v, v+ and F is live across the three barriers: 80 registers, 3 blocks
+// (24 warps) per SM without spills (the shuffle form needed 128 and ran 2 per SM).
 // ---------------------------------------------------------------------------
+#ifndef MFC_XT_MINB
+#define MFC_XT_MINB 3    // resident 256-thread blocks per SM for E <= 8 (80 registers, no
+#endif                   // spills); E > 8 takes 2 (128 registers; 80 spills 24-48 bytes)
+template <class M>
+__host__ __device__ constexpr int x_tile_minb() { return M::E <= 8 ? MFC_XT_MINB : 2; }
 
-// RKB = true (first sweep of a 2D/3D RK stage): dst = cb*q^s + w*c_x, the stage's
-// q^s term taken from the cell this thread converted (re-read, an L1/L2 hit); the later
-// sweeps add w*c_y (M_ACC) and w*c_z + ca*q^n (M_ACCN).
+template <class M>
+__host__ __device__ constexpr size_t x_tile_smem_doubles(int seg) {
+    return (size_t)((M::E * (seg + 6) > (M::E + 1) * (seg + 1)) ? M::E * (seg + 6)
+                                                                 : (M::E + 1) * (seg + 1)) +
+           (size_t)M::E * (seg + 2) + M::E;
+}
+
 template <class M, int ORD, bool RKB>
-__global__ void __launch_bounds__(512, 1)
-sweep_x_rows(const SweepArgs a, int W) {
+__global__ void __launch_bounds__(256, x_tile_minb<M>())
+sweep_x_tile(const SweepArgs a, int W) {
     constexpr int E = M::E;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t = threadIdx.x;
     const int seg = 32 * W;
     const int x0 = blockIdx.x * seg;
     const int n = a.nS;
     const int x1 = min(x0 + seg, n);                 // cells x0 .. x1-1 are updated
-    const bool whole_periodic = (a.gm.blo == 1 && a.gm.alo == n) && x0 == 0 && x1 == n;
-    const int x = x0 + tid;                          // my cell (>= n: boundary-mapped ghost)
+    const bool wrap = (a.gm.blo == 1 && a.gm.alo == n) && x0 == 0 && x1 == n;
+    const int x = x0 + t;
     const int64_t row = a.base + (int64_t)blockIdx.y * a.sA + (int64_t)blockIdx.z * a.sB;
-
-    // shared tables (doubles):
-    //   halo [W+2][4][E]: slot w+1 = warp w's cells 0,1 (k=0,1) and 30,31 (k=2,3);
-    //                     slot 0 k=2,3 = cells x0-2, x0-1; slot W+1 k=0,1 = cells x0+seg, +1
-    //   vmL [W+1][E]: slot w+1 = v- of warp w's last cell; slot 0 = v-(x0-1)
-    //   Ff  [W+1][E+1]: slot w = F, u^f of warp w's first face (x0+32w-1/2); slot W =
-    //                   the face x0+seg-1/2 when the segment ends on a warp border
-    //   st  [2][5][E]: stencils of the two boundary cells (warp 0, lanes 0/1)
+    const int LV = seg + 6, LM = seg + 2, LF = seg + 1;
     extern __shared__ double sm[];
-    double* halo = sm;
-    double* vmL = halo + (W + 2) * 4 * E;
-    double* Ff = vmL + (W + 1) * E;
-    auto H = [&](int slot, int k, int e) -> double& { return halo[(slot * 4 + k) * E + e]; };
+    double* const V = sm;                            // [E][LV]; FS [E+1][LF] after phase 2
+    double* const FS = sm;
+    double* const VM = sm + x_tile_smem_doubles<M>(seg) - (size_t)E * LM - E;   // [E][LM]
+    double* const VPX = VM + (size_t)E * LM;         // [E]: v+(x0+seg)
 
     auto load_prim = [&](int cell, double (&v)[E]) {
-        const int sc = map_cell(cell, n, a.gm);
+        const int sc = map_cell(min(cell, x1 + 2), n, a.gm);   // beyond x1+2: unused
         const double* p = a.q + row + sc;
         double qc[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
-        if (map_flip(cell, n, a.gm)) qc[M::IM] = -qc[M::IM];
+        if (map_flip(min(cell, x1 + 2), n, a.gm)) qc[M::IM] = -qc[M::IM];
         cons_to_prim_fast<M>(qc, v, a.mat);
     };
 
-    // 1. my cell's primitives; publish the warp's border cells and the segment halo
+    // 1. primitives of my cell (index t+3) and of the six halo cells
     double v[E];
     load_prim(x, v);
-    if (lane < 2 || lane >= 30) {
-        const int k = lane < 2 ? lane : lane - 28;
 #pragma unroll
-        for (int e = 0; e < E; ++e) H(warp + 1, k, e) = v[e];
-    }
-    if ((warp == 0 || warp == W - 1) && lane < 2) {
+    for (int e = 0; e < E; ++e) V[e * LV + t + 3] = v[e];
+    if (t < 6) {
         double h[E];
-        const bool left = warp == 0;
-        load_prim(left ? x0 - 2 + lane : x0 + seg + lane, h);
+        load_prim(t < 3 ? x0 - 3 + t : x0 + seg + t - 3, h);
+        const int i = t < 3 ? t : seg + t;
 #pragma unroll
-        for (int e = 0; e < E; ++e) H(left ? 0 : W + 1, left ? 2 + lane : lane, e) = h[e];
-        if (W == 1 && lane < 2) {                    // one warp: it is also the last
-            load_prim(x0 + seg + lane, h);
+        for (int e = 0; e < E; ++e) V[e * LV + i] = h[e];
+    }
+    __syncthreads();
+
+    // 2. WENO of my cell: stencil cells x-2 .. x+2 at V[e][t+1 .. t+5]
+    double vp[E];
 #pragma unroll
-            for (int e = 0; e < E; ++e) H(W + 1, lane, e) = h[e];
+    for (int e = 0; e < E; ++e) {
+        const double* r = V + e * LV + t + 1;
+        double vm;
+        reconstruct<ORD>(r[0], r[1], v[e], r[3], r[4], a.eps4, a.eps, vm, vp[e]);
+        VM[e * LM + t + 1] = vm;
+    }
+    if (!wrap) {
+        const int k = t - (seg - 32);                // lanes 0 .. 2E-1 of the last warp
+        if (k >= 0 && k < 2 * E) {
+            const bool right = k >= E;
+            const int e = right ? k - E : k;
+            const double* r = V + e * LV + (right ? seg + 1 : 0);
+            double bm, bp;
+            reconstruct<ORD>(r[0], r[1], r[2], r[3], r[4], a.eps4, a.eps, bm, bp);
+            if (right) VPX[e] = bp;
+            else VM[e * LM] = bm;
         }
     }
     __syncthreads();
 
-    // 2. WENO of my cell from lanes l-2 .. l+2 (tables across warp borders)
-    double vm[E], vp[E];
-    // branch-free: every lane reads lane-indexed table entries, selects apply them
-    //   lanes 0,1: m2 = prev warp's cell 30+lane, lane 0: m1 = prev warp's cell 31
-    //   lanes 30,31: p2 = next warp's cell lane-30, lane 31: p1 = next warp's cell 0
-    const double* hm2 = &H(warp, 2 + (lane & 1), 0);
-    const double* hm1 = &H(warp, 3, 0);
-    const double* hp2 = &H(warp + 2, lane & 1, 0);
-    const double* hp1 = &H(warp + 2, 0, 0);
-    const bool lo2 = lane < 2, lo1 = lane == 0, hi2 = lane >= 30, hi1 = lane == 31;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        double m2 = __shfl_up_sync(0xffffffffu, v[e], 2);
-        double m1 = __shfl_up_sync(0xffffffffu, v[e], 1);
-        double p1 = __shfl_down_sync(0xffffffffu, v[e], 1);
-        double p2 = __shfl_down_sync(0xffffffffu, v[e], 2);
-        const double tm2 = hm2[e], tm1 = hm1[e], tp2 = hp2[e], tp1 = hp1[e];
-        m2 = lo2 ? tm2 : m2;
-        m1 = lo1 ? tm1 : m1;
-        p2 = hi2 ? tp2 : p2;
-        p1 = hi1 ? tp1 : p1;
-        reconstruct<ORD>(m2, m1, v[e], p1, p2, a.eps4, a.eps, vm[e], vp[e]);
-    }
-    if (lane == 31) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) vmL[(warp + 1) * E + e] = vm[e];
-    }
-    // v-(x0-1): for a whole periodic row it is v-(n-1) (same stencil values);
-    // otherwise warp 0 reconstructs the boundary cells x0-1 (lane 0) and x0+seg (lane 1)
-    if (whole_periodic && x == n - 1) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) vmL[e] = vm[e];
-    }
-    double bp[E];                                    // lane 1 of warp 0: v+(x0+seg)
-    const bool boundary_pass = !whole_periodic && warp == 0;
-    if (boundary_pass && lane < 2) {
-        // stencil of cell c through the shared table st[lane][5][E] (few registers)
-        const int c = lane == 0 ? x0 - 1 : x0 + seg;
-        double* st = Ff + (W + 1) * (E + 1) + lane * 5 * E;
-#pragma unroll 1
-        for (int k = 0; k < 5; ++k) {
-            double h[E];
-            load_prim(c - 2 + k, h);
-#pragma unroll
-            for (int e = 0; e < E; ++e) st[k * E + e] = h[e];
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            double bm;
-            reconstruct<ORD>(st[e], st[E + e], st[2 * E + e], st[3 * E + e], st[4 * E + e], a.eps4,
-                             a.eps, bm, bp[e]);
-            if (lane == 0) vmL[e] = bm;
-        }
-    }
-    __syncthreads();
-
-    // 3. face x-1/2 from v-(x-1) (lane l-1 / table) and my v+
-    double vL[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const double t = __shfl_up_sync(0xffffffffu, vm[e], 1);
-        vL[e] = lane == 0 ? vmL[warp * E + e] : t;
-    }
+    // 3. face x-1/2 from v-(x-1) and my v+  (phase-2 reads of V are complete: FS
+    //    overwrites it)
     double F[E], uf;
-    hllc<M, 0>(vL, vp, a.mat, F, uf);
-    if (lane == 0) {
+    {
+        const int li = (wrap && t == 0) ? n : t;
+        double vL[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) Ff[warp * (E + 1) + e] = F[e];
-        Ff[warp * (E + 1) + E] = uf;
+        for (int e = 0; e < E; ++e) vL[e] = VM[e * LM + li];
+        hllc<M, 0>(vL, vp, a.mat, F, uf);
     }
-    // face x0+seg-1/2 (needed when the segment is full and not a whole periodic row)
-    if (boundary_pass && lane == 1) {
-        double vl[E], FB[E], ufB;
 #pragma unroll
-        for (int e = 0; e < E; ++e) vl[e] = vmL[W * E + e];
-        hllc<M, 0>(vl, bp, a.mat, FB, ufB);
+    for (int e = 0; e < E; ++e) FS[e * LF + t] = F[e];
+    FS[E * LF + t] = uf;
+    if (!wrap && x1 == x0 + seg && t == 0) {         // face x0+seg-1/2
+        double vl[E], vr[E], FB[E], ufB;
 #pragma unroll
-        for (int e = 0; e < E; ++e) Ff[W * (E + 1) + e] = FB[e];
-        Ff[W * (E + 1) + E] = ufB;
+        for (int e = 0; e < E; ++e) { vl[e] = VM[e * LM + seg]; vr[e] = VPX[e]; }
+        hllc<M, 0>(vl, vr, a.mat, FB, ufB);
+#pragma unroll
+        for (int e = 0; e < E; ++e) FS[e * LF + seg] = FB[e];
+        FS[E * LF + seg] = ufB;
     }
     __syncthreads();
 
-    // 4. F(x+1/2) from lane l+1, or for lane 31 the next warp's first face (for the
-    //    last warp: face 0 of a whole periodic row, else the boundary face)
-    double FR[E], ufR;
-    {
-        const int nxt = warp + 1 < W ? warp + 1 : (whole_periodic ? 0 : W);
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const double t = __shfl_down_sync(0xffffffffu, F[e], 1);
-            FR[e] = lane == 31 ? Ff[nxt * (E + 1) + e] : t;
-        }
-        const double t = __shfl_down_sync(0xffffffffu, uf, 1);
-        ufR = lane == 31 ? Ff[nxt * (E + 1) + E] : t;
-    }
+    // 4. cell update with F(x+1/2)
     if (x < x1) {
-        const double du = ufR - uf;
+        const int ri = (wrap && t + 1 == n) ? 0 : t + 1;
+        const double du = FS[E * LF + ri] - uf;
         const double wi = a.w * a.invd;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            double r = F[e] - FR[e];
+            double r = F[e] - FS[e * LF + ri];
             if (e >= M::IA) r = fma(v[e], du, r);
             if constexpr (RKB)
                 a.dst[row + x + e * a.sE] = fma(wi, r, a.cb * __ldg(a.q + row + x + e * a.sE));

@@ -87,20 +87,24 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
     if constexpr (DIR == 0) {
         if (mode == M_SET || (mode == M_RKINIT && M::D >= 2)) {
             if constexpr (M::D >= 2) {
-              // row-parallel kernel while a row fits 8 warps (two resident blocks per SM);
-              // longer rows (one 16-warp block per SM, or split rows with serial boundary
-              // passes) go to the staged march, measured faster there (C2, C5: r45).
-              // The host asks x_rows_used() before choosing M_RKINIT (x_rows only).
+              // row-parallel tile kernel (rows longer than 256 cells: several 8-warp
+              // segments with boundary cells); MFC_X_STAGED: the staged march.
+              // The host asks x_rows_used() before choosing M_RKINIT (tile kernel only).
               if (x_rows_used(a.nS)) {
-                static const int wmax = getenv("MFC_XW") ? atoi(getenv("MFC_XW")) : 16;
-                const int W = (int)std::min<int64_t>(wmax, (a.nS + 31) / 32);
+                const int W = (int)std::min<int64_t>(8, (a.nS + 31) / 32);
                 const int nseg = (a.nS + 32 * W - 1) / (32 * W);
-                const size_t smem = sizeof(double) *
-                    ((size_t)(W + 2) * 4 * M::E + (size_t)(W + 1) * M::E +
-                     (size_t)(W + 1) * (M::E + 1) + 2 * 5 * M::E);
+                const size_t smem = sizeof(double) * x_tile_smem_doubles<M>(32 * W);
+                static size_t attr = 0;
+                if (smem > attr) {
+                    cudaFuncSetAttribute(sweep_x_tile<M, ORD, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    cudaFuncSetAttribute(sweep_x_tile<M, ORD, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    attr = smem;
+                }
                 const dim3 gr(nseg, a.nA, a.nB);
-                if (mode == M_SET) sweep_x_rows<M, ORD, false><<<gr, 32 * W, smem, s>>>(a, W);
-                else sweep_x_rows<M, ORD, true><<<gr, 32 * W, smem, s>>>(a, W);
+                if (mode == M_SET) sweep_x_tile<M, ORD, false><<<gr, 32 * W, smem, s>>>(a, W);
+                else sweep_x_tile<M, ORD, true><<<gr, 32 * W, smem, s>>>(a, W);
               } else if (mode == M_SET) {
                 // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
                 const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);

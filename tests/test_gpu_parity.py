@@ -45,6 +45,10 @@ RHS_CASES = [
     ("GR-3D-N3-water", lambda: W.random_problem(3, (41, 33, 70), 3, "water")),
     ("GR-3D-refl", lambda: W.random_problem(3, (20, 21, 22), 2, "gas",
                                             bc=(W.BC_REFLECTIVE, W.BC_EXTRAPOLATION) * 3)),
+    # rows longer than one x-tile block (several segments with boundary cells)
+    ("GR-2D-long-rows", lambda: W.random_problem(2, (300, 9), 2, "water")),
+    ("GR-3D-long-rows-refl", lambda: W.random_problem(3, (520, 4, 3), 3, "gas",
+                                                      bc=(W.BC_REFLECTIVE, W.BC_EXTRAPOLATION) * 3)),
 ]
 
 

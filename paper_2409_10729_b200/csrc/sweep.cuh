@@ -498,9 +498,12 @@ namespace mfc {
 // ---------------------------------------------------------------------------
 #ifndef MFC_XT_MINB
 #define MFC_XT_MINB 3    // resident 256-thread blocks per SM for E <= 8 (80 registers, no
-#endif                   // spills); E > 8 takes 2 (128 registers; 80 spills 24-48 bytes)
+#endif                   // spills)
+#ifndef MFC_XT_MINB_BIG
+#define MFC_XT_MINB_BIG 3    // E > 8: 3 blocks too (24-48 bytes of spills, still faster: C5 x 29.1 -> 24.1 ms/step, r51)
+#endif
 template <class M>
-__host__ __device__ constexpr int x_tile_minb() { return M::E <= 8 ? MFC_XT_MINB : 2; }
+__host__ __device__ constexpr int x_tile_minb() { return M::E <= 8 ? MFC_XT_MINB : MFC_XT_MINB_BIG; }
 
 template <class M>
 __host__ __device__ constexpr size_t x_tile_smem_doubles(int seg) {

@@ -37,13 +37,37 @@ def raw(rep):
     return hdr, units, data
 
 
+def fp64_ops(rep):
+    """DFMA / DMUL / DADD thread instructions per kernel row (SASS opcode instances)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-metric-instances",
+                          "details", "--metrics", "sass__thread_inst_executed_true_per_opcode"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    res = []
+    for r in rows[1:]:
+        cell = r[-1] if r else ""
+        if "(" not in cell:
+            continue
+        ops = {}
+        for part in cell[cell.find("(") + 1:cell.rfind(")")].split(";"):
+            if ":" in part:
+                k, v = part.split(":")
+                ops[k.strip()] = float(v)
+        res.append({k: ops.get(k, 0.0) for k in ("DFMA", "DMUL", "DADD", "MUFU")})
+    return res
+
+
 def main():
     rep = sys.argv[1]
     hdr, units, data = raw(rep)
     idx = {h: i for i, h in enumerate(hdr)}
     name_i = idx.get("Kernel Name")
     print(f"# ncu summary: `{rep.split('/')[-1]}`\n")
-    for row in data:
+    try:
+        ops = fp64_ops(rep)
+    except Exception:  # older reports / ncu without the metric
+        ops = []
+    for ri, row in enumerate(data):
         kname = row[name_i]
         short = kname.split("(")[0].replace("void ", "")
         tmpl = kname[kname.find("<"):kname.rfind(">") + 1] if "<" in kname else ""
@@ -52,6 +76,12 @@ def main():
         for k, label in KEYS:
             if k in idx:
                 print(f"| {label} (`{k}`) | {row[idx[k]]} {units[idx[k]]} |")
+        if ri < len(ops):
+            o = ops[ri]
+            tot = o["DFMA"] + o["DMUL"] + o["DADD"]
+            print(f"| FP64 thread instructions (SASS DFMA {o['DFMA']:.4g} + DMUL {o['DMUL']:.4g} "
+                  f"+ DADD {o['DADD']:.4g}) | {tot:.4g} |")
+            print(f"| MUFU thread instructions | {o['MUFU']:.4g} |")
         samples = {}
         for s in STALLS:
             k = f"smsp__pcsamp_warps_issue_stalled_{s}"

@@ -176,15 +176,16 @@ def run_reference(args):
 # --------------------------------------------------------------------- ours
 def algorithmic_bytes(kind: str, E: int) -> float:
     """Algorithmic HBM bytes per interior cell for one launch of each sweep kind in an
-    RK3 step: x: read q, write acc (16E); y: read q, acc, q^s (the
-    stencil state, counted once), q^n (stages 2, 3 only), write acc (32E + 8E*2/3);
-    z: read q, acc, write q_out (24E)."""
+    RK3 step (DESIGN.md §6.3; 3D, row-parallel x sweep): x: read q^s (the stencil state;
+    its re-read for the RK base cb*q^s is the same cell, counted once), write acc (16E);
+    y: read q^s, acc, write acc (24E); z: read q^s, acc, q^n (stages 2, 3 only), write
+    the stage result (24E + 8E*2/3)."""
     if kind == "sweep_x":
         return 16.0 * E
     if kind == "sweep_y":
-        return 32.0 * E + 8.0 * E * 2.0 / 3.0
-    if kind == "sweep_z":
         return 24.0 * E
+    if kind == "sweep_z":
+        return 24.0 * E + 8.0 * E * 2.0 / 3.0
     return 0.0
 
 

@@ -1,0 +1,4 @@
+#!/bin/bash
+OUT=gpurun_out; L=paper_2409_10729_b200; REF=${1:-8209603}
+{ MFC_LIB=$L/libmfc_$REF.so python tools/xvariant_dump.py /tmp/a.npz && MFC_XT_PERSIST=1 python tools/xvariant_dump.py /tmp/b.npz && python tools/xvariant_dump.py --compare /tmp/a.npz /tmp/b.npz; } > $OUT/t5_bitwise.log 2>&1
+bash tools/gpu_ab.sh "MFC_LIB=$L/libmfc_$REF.so" "MFC_XT_PERSIST=0" "MFC_XT_PERSIST=1" "MFC_LIB=$L/libmfc_$REF.so" "MFC_XT_PERSIST=0" "MFC_XT_PERSIST=1" > $OUT/t5_ab.log 2>&1

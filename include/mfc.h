@@ -183,7 +183,14 @@ int mfc_rk3_steps(mfc_ctx* ctx, double* q, double dt, int64_t nsteps, void* stre
 /* End-to-end call with HOST buffers: copy the dense interior q_in[E][nz][ny][nx]
  * (host, pinned or pageable) into the padded device buffer q_dev, run nsteps RK3
  * steps of size dt, copy the interior back to q_out (host; may equal q_in), and
- * synchronise `stream`.  Host arrays are dense, x fastest, n_local extents. */
+ * synchronise `stream`.  Host arrays are dense, x fastest, n_local extents.
+ * Needs a bound workspace.  One step of a single-rank 3D domain with enough z planes
+ * is STREAMED: z-chunks are computed as independent sub-domains over their planes +-9
+ * (3 stages x the 3-cell stencil reach) while later input planes are still being
+ * copied in and earlier results copied out (two copy streams besides `stream`; the
+ * chunk states live in the workspace); the result is bitwise that of mfc_rk3_step.
+ * After a streamed step q_dev holds the INPUT state, otherwise the result.
+ * MFC_STREAM=0 disables streaming; MFC_STREAM=P (> 1) asks for P chunks. */
 int mfc_advance_host(mfc_ctx* ctx, const double* q_in, double* q_out, double* q_dev,
                      int64_t nsteps, double dt, void* stream);
 

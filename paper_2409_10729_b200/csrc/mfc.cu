@@ -120,6 +120,14 @@ struct mfc_ctx {
     CUdeviceptr peer_flag[6] = {}; // the neighbour's flags[f^1]
     uint64_t epoch = 0;            // fused-halo operations completed by this rank
     std::vector<void*> ipc_maps;   // IPC mappings this context opened
+    // streamed mfc_advance_host (one step, host buffers): z-chunk contexts whose state
+    // and workspace live in this context's workspace, copy streams, per-chunk events
+    std::vector<mfc_ctx*> chunks;
+    int64_t chunk_cz = 0;
+    char* chunk_ws = nullptr;      // workspace the chunk buffers were carved from
+    cudaStream_t st_in = nullptr, st_out = nullptr;
+    std::vector<cudaEvent_t> ev_piece, ev_comp, ev_out;
+    cudaEvent_t ev_start = nullptr;
 };
 
 namespace {
@@ -704,6 +712,222 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
     return MFC_OK;
 }
 
+// ------------------------------------------------------- streamed advance_host
+//
+// One RK3 step of a host-resident state with the PCIe transfers overlapped: the
+// domain is cut into P z-chunks of Cz planes.  Chunk k's result depends only on input
+// planes within 9 = 3 stages x 3 cells (the WENO5/HLLC stencil reach per RHS) of it, so
+// it is computed as an independent sub-domain over its planes +-9 (periodic wrap, or
+// clipped at a physical boundary that keeps its BC; the cut faces take extrapolation
+// ghosts, whose error reaches exactly 9 planes into the extension and never the
+// chunk).  Every face flux is computed from the same values by the same code as in the
+// whole domain (AMB-22), so the result is bitwise the one-domain step.  Pipeline:
+//   st_in : H2D of input piece j into q_dev (periodic: the pieces of the last 9 planes
+//           first, so the first chunk's wrap-around halo arrives first) -> ev_piece[j]
+//   s     : chunk k waits for the pieces it overlaps (and for the D2H of chunk k-2,
+//           whose buffers it reuses), copies its planes +-9 from q_dev into its own
+//           state (device copy), runs the RK3 step                   -> ev_comp[k]
+//   st_out: D2H of chunk k's own planes into q_out                   -> ev_out[k]
+// The chunk states and workspaces (two sets, alternating) are carved out of this
+// context's workspace: 8 chunk buffers must fit in the 3 state-sized buffers S1, S2,
+// acc.  On return q_dev holds the input state, not the result.
+constexpr int kStreamHalo = 9;
+
+int copy_planes_h(const mfc_ctx* c, bool h2d, const double* host_in, double* host_out,
+                  double* dev, const mfc_ctx* dl, int64_t zdev, int64_t zhost, int64_t nz,
+                  cudaStream_t st) {
+    // planes [zhost, zhost+nz) of the dense host array <-> planes [zdev, ...) of the
+    // device state with layout dl (interior coordinates)
+    const size_t row = (size_t)c->nl[0] * sizeof(double);
+    const size_t pitch = (size_t)dl->stride[2] * sizeof(double);
+    const size_t plane_h = (size_t)c->nl[0] * c->nl[1];
+    for (int e = 0; e < c->E; ++e) {
+        cudaMemcpy3DParms p = {};
+        double* d = dev + dl->offset + e * dl->stride[0] + zdev * dl->stride[1];
+        const size_t ho = (size_t)e * plane_h * c->nl[2] + (size_t)zhost * plane_h;
+        double* h = h2d ? const_cast<double*>(host_in) + ho : host_out + ho;
+        cudaPitchedPtr hp = make_cudaPitchedPtr(h, row, c->nl[0], c->nl[1]);
+        cudaPitchedPtr dp = make_cudaPitchedPtr(d, pitch, c->nl[0], dl->dims[2]);
+        p.srcPtr = h2d ? hp : dp;
+        p.dstPtr = h2d ? dp : hp;
+        p.extent = make_cudaExtent(row, c->nl[1], nz);
+        p.kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+        CU_TRY(cudaMemcpy3DAsync(&p, st));
+    }
+    return MFC_OK;
+}
+
+void free_chunks(mfc_ctx* c) {
+    for (mfc_ctx* k : c->chunks) mfc_finalize(k);
+    c->chunks.clear();
+    c->chunk_cz = 0;
+}
+
+// chunk k of depth cz: interior planes [z0, z1), extension [e0, e1) (may wrap)
+void chunk_range(const mfc_ctx* c, int64_t cz, int k, int64_t* z0, int64_t* z1, int64_t* e0,
+                 int64_t* e1) {
+    const int64_t nz = c->nl[2];
+    const bool per = c->bc[4] == MFC_BC_PERIODIC;
+    *z0 = k * cz;
+    *z1 = std::min(nz, *z0 + cz);
+    *e0 = *z0 - kStreamHalo;
+    *e1 = *z1 + kStreamHalo;
+    if (!per) {
+        *e0 = std::max<int64_t>(0, *e0);
+        *e1 = std::min(nz, *e1);
+    }
+}
+
+// Chunk depth for the streamed step, 0 when the step is not streamed.
+int64_t stream_cz(const mfc_ctx* c) {
+    static const int env = getenv("MFC_STREAM") ? atoi(getenv("MFC_STREAM")) : -1;
+    if (env == 0 || c->D != 3 || c->nranks != 1 || c->fused || !c->ws) return 0;
+    const int64_t nz = c->nl[2];
+    const int64_t want = env > 1 ? env : 16;                 // chunks
+    int64_t cz = std::max<int64_t>(kStreamHalo, (nz + want - 1) / want);
+    if ((nz + cz - 1) / cz < 3) return 0;
+    // 8 chunk buffers of (cz + 18 + 6) planes within S1, S2, acc of (nz + 6) planes
+    const int64_t plane = c->stride[1];
+    const size_t cb = ((size_t)c->E * (cz + 2 * kStreamHalo + 2 * kGhost) * plane * sizeof(double) +
+                       255) / 256 * 256;
+    if (8 * cb > 3 * (size_t)c->n_elems * sizeof(double)) return 0;
+    return cz;
+}
+
+int build_chunks(mfc_ctx* c, int64_t cz) {
+    if (c->chunk_cz == cz && c->chunk_ws == c->ws && !c->chunks.empty()) return MFC_OK;
+    free_chunks(c);
+    const int64_t nz = c->nl[2];
+    const int P = (int)((nz + cz - 1) / cz);
+    const int64_t plane = c->stride[1];
+    const size_t cb = ((size_t)c->E * (cz + 2 * kStreamHalo + 2 * kGhost) * plane * sizeof(double) +
+                       255) / 256 * 256;
+    for (int k = 0; k < P; ++k) {
+        int64_t z0, z1, e0, e1;
+        chunk_range(c, cz, k, &z0, &z1, &e0, &e1);
+        mfc_grid g{};
+        g.ndim = 3;
+        g.n_global[0] = c->nl[0];
+        g.n_global[1] = c->nl[1];
+        g.n_global[2] = e1 - e0;
+        for (int d = 0; d < 3; ++d) {
+            g.lo[d] = 0.0;
+            g.hi[d] = c->dx[d] * (double)g.n_global[d];
+            g.procs[d] = 1;
+        }
+        int32_t bc[6] = {c->bc[0], c->bc[1], c->bc[2], c->bc[3], MFC_BC_EXTRAPOLATION,
+                         MFC_BC_EXTRAPOLATION};
+        if (c->bc[4] != MFC_BC_PERIODIC) {
+            if (e0 == 0) bc[4] = c->bc[4];
+            if (e1 == nz) bc[5] = c->bc[5];
+        }
+        const double gam[3] = {1.4, 1.4, 1.4}, pinf[3] = {0, 0, 0};   // replaced below
+        mfc_ctx* k_ctx = nullptr;
+        int st = mfc_init(&k_ctx, &g, c->N, gam, pinf, bc, nullptr, c->device);
+        if (st) {
+            free_chunks(c);
+            return st;
+        }
+        c->chunks.push_back(k_ctx);
+        char* set = c->ws + (size_t)(k & 1) * 4 * cb;       // state, S1, S2, acc
+        if ((st = mfc_bind_workspace(k_ctx, set + cb, 3 * cb))) {
+            free_chunks(c);
+            return st;
+        }
+    }
+    c->chunk_cz = cz;
+    c->chunk_ws = c->ws;
+    auto mk = [](std::vector<cudaEvent_t>& v, int n) -> cudaError_t {
+        while ((int)v.size() < n) {
+            cudaEvent_t e;
+            cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            if (r != cudaSuccess) return r;
+            v.push_back(e);
+        }
+        return cudaSuccess;
+    };
+    CU_TRY(mk(c->ev_piece, P));
+    CU_TRY(mk(c->ev_comp, P));
+    CU_TRY(mk(c->ev_out, P));
+    if (!c->ev_start) CU_TRY(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+    if (!c->st_in) CU_TRY(cudaStreamCreateWithFlags(&c->st_in, cudaStreamNonBlocking));
+    if (!c->st_out) CU_TRY(cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking));
+    return MFC_OK;
+}
+
+int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_dev, double dt,
+                     int64_t cz, cudaStream_t s) {
+    int st = build_chunks(c, cz);
+    if (st) return st;
+    for (mfc_ctx* kc : c->chunks) {   // the parent's settings, bit for bit (constants are
+        kc->mat = c->mat;             // copied, not re-derived from gamma, pi_inf)
+        for (int d = 0; d < 3; ++d) {
+            kc->dx[d] = c->dx[d];
+            kc->seg_dir[d] = c->seg_dir[d];
+        }
+        kc->eps = c->eps;
+        kc->weno_order = c->weno_order;
+        kc->seg = c->seg;
+        kc->xbase = c->xbase;
+        kc->prof = false;
+    }
+    const int64_t nz = c->nl[2];
+    const int P = (int)c->chunks.size();
+    const bool per = c->bc[4] == MFC_BC_PERIODIC;
+    const size_t cb = ((size_t)c->E * (cz + 2 * kStreamHalo + 2 * kGhost) * c->stride[1] *
+                           sizeof(double) + 255) / 256 * 256;
+    CU_TRY(cudaEventRecord(c->ev_start, s));
+    CU_TRY(cudaStreamWaitEvent(c->st_in, c->ev_start, 0));
+    CU_TRY(cudaStreamWaitEvent(c->st_out, c->ev_start, 0));
+    // 1. input pieces (piece j = planes of chunk j); periodic: the pieces holding the
+    //    last 9 planes (the first chunk's wrap-around halo) go first
+    const int first = per ? (int)((nz - kStreamHalo) / cz) : 0;
+    for (int i = 0; i < P; ++i) {
+        const int j = (first + i) % P;
+        int64_t z0, z1, e0, e1;
+        chunk_range(c, cz, j, &z0, &z1, &e0, &e1);
+        if ((st = copy_planes_h(c, true, q_in, nullptr, q_dev, c, z0, z0, z1 - z0, c->st_in)))
+            return st;
+        CU_TRY(cudaEventRecord(c->ev_piece[j], c->st_in));
+    }
+    // 2. chunks
+    for (int k = 0; k < P; ++k) {
+        mfc_ctx* kc = c->chunks[k];
+        int64_t z0, z1, e0, e1;
+        chunk_range(c, cz, k, &z0, &z1, &e0, &e1);
+        // pieces overlapping [e0, e1) (mod nz)
+        for (int64_t z = e0; z < e1; z += 1) {
+            const int64_t zz = ((z % nz) + nz) % nz;
+            const int j = (int)(zz / cz);
+            if (z == e0 || zz % cz == 0) CU_TRY(cudaStreamWaitEvent(s, c->ev_piece[j], 0));
+        }
+        if (k >= 2) CU_TRY(cudaStreamWaitEvent(s, c->ev_out[k - 2], 0));
+        double* qk = (double*)(c->ws + (size_t)(k & 1) * 4 * cb);
+        // planes [e0, e1) of q_dev -> chunk planes [0, e1-e0): contiguous runs mod nz
+        const size_t plane_b = (size_t)c->stride[1] * sizeof(double);
+        for (int64_t z = e0; z < e1;) {
+            const int64_t zz = ((z % nz) + nz) % nz;
+            const int64_t run = std::min(e1 - z, nz - zz);
+            const double* src = q_dev + (c->off[2] + zz) * c->stride[1];
+            double* dst = qk + (kc->off[2] + (z - e0)) * kc->stride[1];
+            CU_TRY(cudaMemcpy2DAsync(dst, (size_t)kc->stride[0] * sizeof(double), src,
+                                     (size_t)c->stride[0] * sizeof(double), run * plane_b, c->E,
+                                     cudaMemcpyDeviceToDevice, s));
+            z += run;
+        }
+        if ((st = rk3_group(&kc, &qk, 1, dt, s))) return st;
+        c->launches += kc->launches;
+        CU_TRY(cudaEventRecord(c->ev_comp[k], s));
+        CU_TRY(cudaStreamWaitEvent(c->st_out, c->ev_comp[k], 0));
+        if ((st = copy_planes_h(c, false, nullptr, q_out, qk, kc, z0 - e0, z0, z1 - z0, c->st_out)))
+            return st;
+        CU_TRY(cudaEventRecord(c->ev_out[k], c->st_out));
+    }
+    CU_TRY(cudaStreamWaitEvent(s, c->ev_out[P - 1], 0));
+    CU_TRY(cudaStreamSynchronize(s));
+    return MFC_OK;
+}
+
 int rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int count,
               cudaStream_t s) {
     for (int r = 0; r < count; ++r) {
@@ -1185,6 +1409,13 @@ int mfc_advance_host(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
     int st;
     if ((st = check_ptr(q_dev, "q_dev")) || (st = set_device(c))) return st;
     cudaStream_t s = (cudaStream_t)stream;
+    if (nsteps == 1) {
+        const int64_t cz = stream_cz(c);
+        if (cz > 0) {
+            c->launches = 0;
+            return advance_streamed(c, q_in, q_out, q_dev, dt, cz, s);
+        }
+    }
     const size_t row = (size_t)c->nl[0] * sizeof(double);
     const size_t pitch = (size_t)c->stride[2] * sizeof(double);
     auto copy = [&](bool h2d) -> int {
@@ -1392,6 +1623,13 @@ int mfc_finalize(mfc_ctx* c) {
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
+    free_chunks(c);
+    for (auto e : c->ev_piece) cudaEventDestroy(e);
+    for (auto e : c->ev_comp) cudaEventDestroy(e);
+    for (auto e : c->ev_out) cudaEventDestroy(e);
+    if (c->ev_start) cudaEventDestroy(c->ev_start);
+    if (c->st_in) cudaStreamDestroy(c->st_in);
+    if (c->st_out) cudaStreamDestroy(c->st_out);
     delete c;
     return MFC_OK;
 }

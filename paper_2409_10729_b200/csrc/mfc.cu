@@ -203,6 +203,18 @@ __global__ void halo_pack_kernel(const double* q, double* buf, FaceGeom g, int d
     }
 }
 
+// dst[e*dE + i] = src[e*sE + i] for i < n (16-byte vectors; n, offsets even): the
+// streamed step's chunk copies on the SMs, off the copy engines that carry PCIe traffic
+__global__ void copy_planes_kernel(double* dst, int64_t dE, const double* src, int64_t sE,
+                                   int64_t n2, int E) {
+    const int64_t tot = n2 * E;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = t / n2, i = t - e * n2;
+        reinterpret_cast<double2*>(dst + e * dE)[i] = reinterpret_cast<const double2*>(src + e * sE)[i];
+    }
+}
+
 int grid_for(int64_t n, int threads) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 148 * 32));
 }
@@ -783,7 +795,7 @@ int64_t stream_cz(const mfc_ctx* c) {
     static const int env = getenv("MFC_STREAM") ? atoi(getenv("MFC_STREAM")) : -1;
     if (env == 0 || c->D != 3 || c->nranks != 1 || c->fused || !c->ws) return 0;
     const int64_t nz = c->nl[2];
-    const int64_t want = env > 1 ? env : 16;                 // chunks
+    const int64_t want = env > 1 ? env : 20;   // chunks (r55: 8 / 12 / 16 / 20 / 32 -> 30 / 28 / 26.7 / 26.0 / 31 ms per C3 step)
     int64_t cz = std::max<int64_t>(kStreamHalo, (nz + want - 1) / want);
     if ((nz + cz - 1) / cz < 3) return 0;
     // 8 chunk buffers of (cz + 18 + 6) planes within S1, S2, acc of (nz + 6) planes
@@ -910,9 +922,19 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
             const int64_t run = std::min(e1 - z, nz - zz);
             const double* src = q_dev + (c->off[2] + zz) * c->stride[1];
             double* dst = qk + (kc->off[2] + (z - e0)) * kc->stride[1];
-            CU_TRY(cudaMemcpy2DAsync(dst, (size_t)kc->stride[0] * sizeof(double), src,
-                                     (size_t)c->stride[0] * sizeof(double), run * plane_b, c->E,
-                                     cudaMemcpyDeviceToDevice, s));
+            static const bool ce = getenv("MFC_STREAM_CE") != nullptr;
+            if (ce || (run * c->stride[1]) % 2 || c->stride[0] % 2 || kc->stride[0] % 2 ||
+                (c->off[2] + zz) * c->stride[1] % 2 || (kc->off[2] + z - e0) * kc->stride[1] % 2) {
+                CU_TRY(cudaMemcpy2DAsync(dst, (size_t)kc->stride[0] * sizeof(double), src,
+                                         (size_t)c->stride[0] * sizeof(double), run * plane_b,
+                                         c->E, cudaMemcpyDeviceToDevice, s));
+            } else {
+                const int64_t n2 = run * c->stride[1] / 2;
+                copy_planes_kernel<<<grid_for(n2 * c->E, 256), 256, 0, s>>>(
+                    dst, kc->stride[0], src, c->stride[0], n2, c->E);
+                CU_TRY(cudaGetLastError());
+                ++c->launches;
+            }
             z += run;
         }
         if ((st = rk3_group(&kc, &qk, 1, dt, s))) return st;

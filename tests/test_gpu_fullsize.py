@@ -53,6 +53,22 @@ def test_c3_full_rk3_step(c3):
     assert np.all(err <= 10 * RHS_TOL), err
 
 
+def test_c3_full_advance_host_streamed(c3):
+    """The e2e call of bench.py at full size: mfc_advance_host streams the step in
+    z-chunks; it must equal the device step (test above) bit for bit."""
+    pb, P, v, q = c3
+    s = mfc.Solver(pb)
+    qd = s.state_from_cons(q)
+    s.rk3_step(qd, pb.dt)
+    torch.cuda.synchronize()
+    ref = s.interior(qd).cpu().numpy()
+    q_in = torch.as_tensor(q).pin_memory()
+    q_out = torch.empty_like(q_in).pin_memory()
+    s.advance_host(q_in, q_out, qd, 1, pb.dt)
+    assert s.last_launch_count() > 9        # streamed
+    assert np.array_equal(q_out.numpy(), ref)
+
+
 def test_c5_full_size_sampled():
     """512^3, 3 fluids (E = 10, 10.7 GB state): the GPU computes the whole RHS; the
     oracle computes it at 400 sampled cells (incl. the domain corners, the droplet and

@@ -57,6 +57,9 @@ int fail(int code, const char* fmt, ...) {
     } while (0)
 
 constexpr int kXOff = 4;  // interior x starts at pitch index 4: 1 pad + 3 ghosts (32 B aligned)
+constexpr int kStreamChunks = 32;   // z-chunks of a streamed advance_host step
+constexpr int kStageCzMin = 3;      // a chunk spans at least the 3-cell stencil reach
+constexpr int kStageSlots = 4;      // dense staging slots per direction
 constexpr int BC_NEIGHBOR = 1;
 
 }  // namespace
@@ -120,17 +123,24 @@ struct mfc_ctx {
     CUdeviceptr peer_flag[6] = {}; // the neighbour's flags[f^1]
     uint64_t epoch = 0;            // fused-halo operations completed by this rank
     std::vector<void*> ipc_maps;   // IPC mappings this context opened
-    // streamed mfc_advance_host (one step, host buffers): z-chunk contexts whose state
-    // and workspace live in this context's workspace, copy streams, per-chunk events
-    std::vector<mfc_ctx*> chunks;
-    int64_t chunk_cz = 0;
-    char* chunk_ws = nullptr;      // workspace the chunk buffers were carved from
+    // streamed mfc_advance_host (one step, host buffers): the sweeps of one RK stage
+    // restricted to z planes [zr0, zr1) (zr1 < 0: whole domain), copy streams, events
+    int64_t zr0 = 0, zr1 = -1;
+    int64_t stage_cz = 0;          // planes per staging slot (0: no staging rings)
+    double* stage_in = nullptr;    // kStageSlots dense input pieces [E][cz][ny][nx]
+    double* stage_out = nullptr;   // kStageSlots dense result chunks
+    std::vector<cudaEvent_t> ev_scat;
     cudaStream_t st_in = nullptr, st_out = nullptr;
     std::vector<cudaEvent_t> ev_piece, ev_comp, ev_out;
     cudaEvent_t ev_start = nullptr;
 };
 
 namespace {
+
+// bytes of one dense staging slot of the streamed step (E x stage_cz planes)
+size_t stage_slot_bytes(const mfc_ctx* c) {
+    return ((size_t)c->E * c->stage_cz * c->nl[0] * c->nl[1] * sizeof(double) + 255) / 256 * 256;
+}
 
 // ---------------------------------------------------------------- kernels
 
@@ -212,6 +222,23 @@ __global__ void copy_planes_kernel(double* dst, int64_t dE, const double* src, i
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = t / n2, i = t - e * n2;
         reinterpret_cast<double2*>(dst + e * dE)[i] = reinterpret_cast<const double2*>(src + e * sE)[i];
+    }
+}
+
+// Dense <-> padded planes: dense[e][z][y][x] (nz planes) <-> padded interior planes
+// z0 .. z0+nz of a state with strides sE, sZ, sY (x unit stride), base = interior offset.
+__global__ void dense_planes_kernel(double* dense, double* padded, int64_t base, int64_t sE,
+                                    int64_t sZ, int64_t sY, int nx, int ny, int64_t z0, int nz,
+                                    int E, bool to_dense) {
+    const int64_t plane = (int64_t)nx * ny, tot = plane * nz * E;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ez = t / plane, r = t - ez * plane;
+        const int64_t e = ez / nz, z = ez - e * nz;
+        const int64_t y = r / nx, x = r - y * nx;
+        double* p = padded + base + e * sE + (z0 + z) * sZ + y * sY + x;
+        if (to_dense) dense[t] = *p;
+        else *p = dense[t];
     }
 }
 
@@ -573,6 +600,19 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     // resident warps per SM: 12 for the non-RK ring sweeps with E <= 8 (3 blocks), else 8
     const bool three = c->E <= 8 && dir > 0 && (mode == M_ACC || mode == M_ACCN);
     a.T = seg_len(c, dir, three ? 12 : 8);
+    a.s_lo = 0;
+    a.s_hi = a.nS;
+    // a z-plane range (streamed step, c->zr1 >= 0): the z sweep updates cells
+    // [zr0, zr1) of its lines, the x and y sweeps only the planes of that range
+    if (c->zr1 >= 0 && c->D == 3) {
+        if (dir == 2) {
+            a.s_lo = (int32_t)c->zr0;
+            a.s_hi = (int32_t)c->zr1;
+        } else {
+            a.base += c->zr0 * a.sB;
+            a.nB = (int32_t)(c->zr1 - c->zr0);
+        }
+    }
     // physical faces are applied by index mapping inside the sweep; faces shared with
     // another rank read the ghost layers the halo exchange wrote
     {
@@ -600,7 +640,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
         by = (int)std::max<int64_t>(1, std::min<int64_t>(c->E <= 8 ? 4 : 2, a.nB));
     }   // (ring sweeps fix their own block shape: 32 x NTH/32, see sweep_nth)
     dim3 block(bx, by);
-    dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.nS + a.T - 1) / a.T);
+    dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.s_hi - a.s_lo + a.T - 1) / a.T);
     cudaError_t e;
     ProfScope ps(c, s, K_SWEEP_X + dir);
     switch (c->N) {
@@ -726,40 +766,40 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
 
 // ------------------------------------------------------- streamed advance_host
 //
-// One RK3 step of a host-resident state with the PCIe transfers overlapped: the
-// domain is cut into P z-chunks of Cz planes.  Chunk k's result depends only on input
-// planes within 9 = 3 stages x 3 cells (the WENO5/HLLC stencil reach per RHS) of it, so
-// it is computed as an independent sub-domain over its planes +-9 (periodic wrap, or
-// clipped at a physical boundary that keeps its BC; the cut faces take extrapolation
-// ghosts, whose error reaches exactly 9 planes into the extension and never the
-// chunk).  Every face flux is computed from the same values by the same code as in the
-// whole domain (AMB-22), so the result is bitwise the one-domain step.  Pipeline:
-//   st_in : H2D of input piece j into q_dev (periodic: the pieces of the last 9 planes
-//           first, so the first chunk's wrap-around halo arrives first) -> ev_piece[j]
-//   s     : chunk k waits for the pieces it overlaps (and for the D2H of chunk k-2,
-//           whose buffers it reuses), copies its planes +-9 from q_dev into its own
-//           state (device copy), runs the RK3 step                   -> ev_comp[k]
-//   st_out: D2H of chunk k's own planes into q_out                   -> ev_out[k]
-// The chunk states and workspaces (two sets, alternating) are carved out of this
-// context's workspace: 8 chunk buffers must fit in the 3 state-sized buffers S1, S2,
-// acc.  On return q_dev holds the input state, not the result.
-constexpr int kStreamHalo = 9;
+// One RK3 step of a host-resident state with the PCIe transfers overlapped by a
+// wavefront over z-chunks of cz >= 3 planes.  A stage's sweeps restricted to the planes
+// of chunk k read the stage input within 3 planes of it (the WENO5/HLLC reach), i.e.
+// only chunks k-1, k, k+1, so stage s of chunk k can run as soon as stage s-1 of its
+// two neighbours is done:
+//   step j: stage 1 of chunk j, stage 2 of chunk j-1, stage 3 of chunk j-2.
+// The buffers are the whole-domain ones of an ordinary step (q_dev, S1, S2, acc); every
+// plane of every stage is computed exactly once, by the same code as the whole-domain
+// step (the z sweep's line segments merely start at chunk boundaries: AMB-22), so the
+// result is bitwise mfc_rk3_step's and it is left in q_dev.  Stage 3 writes q_dev in
+// place, which is safe because stage 1 of chunk k+1 (the last reader of chunk k's input
+// planes) runs before stage 3 of chunk k.  A periodic z axis closes the ring at chunk
+// 0: its stages 2 and 3 wait for the end (stage 2 of chunk 0 before stage 3 of chunk
+// P-1, which reads it), and its input planes stay intact until then.
+//   st_in : H2D of input piece j (= chunk j's planes) into q_dev; periodic: the piece
+//           holding the last 3 planes first                             -> ev_piece[j]
+//   s     : the stage sweeps in wavefront order; stage 1 of chunk k waits for the
+//           pieces within 3 planes of it                                 -> ev_comp[k]
+//   st_out: D2H of chunk k's result planes into q_out                    -> ev_out[k]
+constexpr int kStageReach = 3;
 
 int copy_planes_h(const mfc_ctx* c, bool h2d, const double* host_in, double* host_out,
-                  double* dev, const mfc_ctx* dl, int64_t zdev, int64_t zhost, int64_t nz,
-                  cudaStream_t st) {
-    // planes [zhost, zhost+nz) of the dense host array <-> planes [zdev, ...) of the
-    // device state with layout dl (interior coordinates)
+                  double* dev, int64_t z0, int64_t nz, cudaStream_t st) {
+    // planes [z0, z0+nz) of the dense host array <-> the same interior planes of dev
     const size_t row = (size_t)c->nl[0] * sizeof(double);
-    const size_t pitch = (size_t)dl->stride[2] * sizeof(double);
+    const size_t pitch = (size_t)c->stride[2] * sizeof(double);
     const size_t plane_h = (size_t)c->nl[0] * c->nl[1];
     for (int e = 0; e < c->E; ++e) {
         cudaMemcpy3DParms p = {};
-        double* d = dev + dl->offset + e * dl->stride[0] + zdev * dl->stride[1];
-        const size_t ho = (size_t)e * plane_h * c->nl[2] + (size_t)zhost * plane_h;
+        double* d = dev + c->offset + e * c->stride[0] + z0 * c->stride[1];
+        const size_t ho = (size_t)e * plane_h * c->nl[2] + (size_t)z0 * plane_h;
         double* h = h2d ? const_cast<double*>(host_in) + ho : host_out + ho;
         cudaPitchedPtr hp = make_cudaPitchedPtr(h, row, c->nl[0], c->nl[1]);
-        cudaPitchedPtr dp = make_cudaPitchedPtr(d, pitch, c->nl[0], dl->dims[2]);
+        cudaPitchedPtr dp = make_cudaPitchedPtr(d, pitch, c->nl[0], c->dims[2]);
         p.srcPtr = h2d ? hp : dp;
         p.dstPtr = h2d ? dp : hp;
         p.extent = make_cudaExtent(row, c->nl[1], nz);
@@ -769,86 +809,38 @@ int copy_planes_h(const mfc_ctx* c, bool h2d, const double* host_in, double* hos
     return MFC_OK;
 }
 
-void free_chunks(mfc_ctx* c) {
-    for (mfc_ctx* k : c->chunks) mfc_finalize(k);
-    c->chunks.clear();
-    c->chunk_cz = 0;
-}
-
-// chunk k of depth cz: interior planes [z0, z1), extension [e0, e1) (may wrap)
-void chunk_range(const mfc_ctx* c, int64_t cz, int k, int64_t* z0, int64_t* z1, int64_t* e0,
-                 int64_t* e1) {
-    const int64_t nz = c->nl[2];
-    const bool per = c->bc[4] == MFC_BC_PERIODIC;
-    *z0 = k * cz;
-    *z1 = std::min(nz, *z0 + cz);
-    *e0 = *z0 - kStreamHalo;
-    *e1 = *z1 + kStreamHalo;
-    if (!per) {
-        *e0 = std::max<int64_t>(0, *e0);
-        *e1 = std::min(nz, *e1);
-    }
-}
-
-// Chunk depth for the streamed step, 0 when the step is not streamed.
+// Chunk depth of the streamed step, 0 when the step is not streamed.
 int64_t stream_cz(const mfc_ctx* c) {
     static const int env = getenv("MFC_STREAM") ? atoi(getenv("MFC_STREAM")) : -1;
     if (env == 0 || c->D != 3 || c->nranks != 1 || c->fused || !c->ws) return 0;
     const int64_t nz = c->nl[2];
-    const int64_t want = env > 1 ? env : 20;   // chunks (r55: 8 / 12 / 16 / 20 / 32 -> 30 / 28 / 26.7 / 26.0 / 31 ms per C3 step)
-    int64_t cz = std::max<int64_t>(kStreamHalo, (nz + want - 1) / want);
-    if ((nz + cz - 1) / cz < 3) return 0;
-    // 8 chunk buffers of (cz + 18 + 6) planes within S1, S2, acc of (nz + 6) planes
-    const int64_t plane = c->stride[1];
-    const size_t cb = ((size_t)c->E * (cz + 2 * kStreamHalo + 2 * kGhost) * plane * sizeof(double) +
-                       255) / 256 * 256;
-    if (8 * cb > 3 * (size_t)c->n_elems * sizeof(double)) return 0;
-    return cz;
+    const int64_t want = env > 1 ? env : kStreamChunks;      // chunks
+    const int64_t cz = std::max<int64_t>(kStageReach, (nz + want - 1) / want);
+    return nz / kStageReach >= 3 ? cz : 0;
 }
 
-int build_chunks(mfc_ctx* c, int64_t cz) {
-    if (c->chunk_cz == cz && c->chunk_ws == c->ws && !c->chunks.empty()) return MFC_OK;
-    free_chunks(c);
+// stage (0, 1, 2) of the RK3 step of q, restricted to z planes [za, zb)
+int rk3_stage_planes(mfc_ctx* c, double* q, int stage, double dt, int64_t za, int64_t zb,
+                     cudaStream_t s) {
+    static const double CA[3] = {0.0, 0.75, 1.0 / 3.0};
+    static const double CB[3] = {1.0, 0.25, 2.0 / 3.0};
+    double* in = stage == 0 ? q : (stage == 1 ? c->S1 : c->S2);
+    double* out = stage == 0 ? c->S1 : (stage == 1 ? c->S2 : q);
+    c->zr0 = za;
+    c->zr1 = zb;
+    const int st = sweeps(c, in, c->acc, out, true, q, dt, CA[stage], CB[stage], s);
+    c->zr0 = 0;
+    c->zr1 = -1;
+    return st;
+}
+
+int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_dev, double dt,
+                     int64_t cz, cudaStream_t s) {
     const int64_t nz = c->nl[2];
-    const int P = (int)((nz + cz - 1) / cz);
-    const int64_t plane = c->stride[1];
-    const size_t cb = ((size_t)c->E * (cz + 2 * kStreamHalo + 2 * kGhost) * plane * sizeof(double) +
-                       255) / 256 * 256;
-    for (int k = 0; k < P; ++k) {
-        int64_t z0, z1, e0, e1;
-        chunk_range(c, cz, k, &z0, &z1, &e0, &e1);
-        mfc_grid g{};
-        g.ndim = 3;
-        g.n_global[0] = c->nl[0];
-        g.n_global[1] = c->nl[1];
-        g.n_global[2] = e1 - e0;
-        for (int d = 0; d < 3; ++d) {
-            g.lo[d] = 0.0;
-            g.hi[d] = c->dx[d] * (double)g.n_global[d];
-            g.procs[d] = 1;
-        }
-        int32_t bc[6] = {c->bc[0], c->bc[1], c->bc[2], c->bc[3], MFC_BC_EXTRAPOLATION,
-                         MFC_BC_EXTRAPOLATION};
-        if (c->bc[4] != MFC_BC_PERIODIC) {
-            if (e0 == 0) bc[4] = c->bc[4];
-            if (e1 == nz) bc[5] = c->bc[5];
-        }
-        const double gam[3] = {1.4, 1.4, 1.4}, pinf[3] = {0, 0, 0};   // replaced below
-        mfc_ctx* k_ctx = nullptr;
-        int st = mfc_init(&k_ctx, &g, c->N, gam, pinf, bc, nullptr, c->device);
-        if (st) {
-            free_chunks(c);
-            return st;
-        }
-        c->chunks.push_back(k_ctx);
-        char* set = c->ws + (size_t)(k & 1) * 4 * cb;       // state, S1, S2, acc
-        if ((st = mfc_bind_workspace(k_ctx, set + cb, 3 * cb))) {
-            free_chunks(c);
-            return st;
-        }
-    }
-    c->chunk_cz = cz;
-    c->chunk_ws = c->ws;
+    // balanced chunks of floor/ceil(nz/P) >= 3 planes (every chunk spans the stencil
+    // reach, so stage s of chunk k reads stage s-1 of chunks k-1, k, k+1 only)
+    const int P = (int)std::min<int64_t>((nz + cz - 1) / cz, nz / kStageReach);
+    const bool per = c->bc[4] == MFC_BC_PERIODIC;
     auto mk = [](std::vector<cudaEvent_t>& v, int n) -> cudaError_t {
         while ((int)v.size() < n) {
             cudaEvent_t e;
@@ -864,89 +856,150 @@ int build_chunks(mfc_ctx* c, int64_t cz) {
     if (!c->ev_start) CU_TRY(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     if (!c->st_in) CU_TRY(cudaStreamCreateWithFlags(&c->st_in, cudaStreamNonBlocking));
     if (!c->st_out) CU_TRY(cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking));
-    return MFC_OK;
-}
-
-int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_dev, double dt,
-                     int64_t cz, cudaStream_t s) {
-    int st = build_chunks(c, cz);
-    if (st) return st;
-    for (mfc_ctx* kc : c->chunks) {   // the parent's settings, bit for bit (constants are
-        kc->mat = c->mat;             // copied, not re-derived from gamma, pi_inf)
-        for (int d = 0; d < 3; ++d) {
-            kc->dx[d] = c->dx[d];
-            kc->seg_dir[d] = c->seg_dir[d];
-        }
-        kc->eps = c->eps;
-        kc->weno_order = c->weno_order;
-        kc->seg = c->seg;
-        kc->xbase = c->xbase;
-        kc->prof = false;
-    }
-    const int64_t nz = c->nl[2];
-    const int P = (int)c->chunks.size();
-    const bool per = c->bc[4] == MFC_BC_PERIODIC;
-    const size_t cb = ((size_t)c->E * (cz + 2 * kStreamHalo + 2 * kGhost) * c->stride[1] *
-                           sizeof(double) + 255) / 256 * 256;
+    auto z0 = [&](int k) { return k * nz / P; };
+    auto z1 = [&](int k) { return (k + 1) * nz / P; };
+    int st;
+    static const bool tr = getenv("MFC_STREAM_TRACE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> tr_ev;
+    auto mark = [&](const std::string& name, cudaStream_t on) {
+        if (!tr) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, on);
+        tr_ev.emplace_back(name, e);
+    };
     CU_TRY(cudaEventRecord(c->ev_start, s));
+    mark("start", s);
     CU_TRY(cudaStreamWaitEvent(c->st_in, c->ev_start, 0));
     CU_TRY(cudaStreamWaitEvent(c->st_out, c->ev_start, 0));
-    // 1. input pieces (piece j = planes of chunk j); periodic: the pieces holding the
-    //    last 9 planes (the first chunk's wrap-around halo) go first
-    const int first = per ? (int)((nz - kStreamHalo) / cz) : 0;
+    // Dense staging (c->stage_in / stage_out rings of kStageSlots pieces): the PCIe
+    // copies are plain contiguous runs (E per piece) instead of 2 KB-row pitched
+    // copies, which lost a quarter of the bidirectional bandwidth (r57 trace); a small
+    // kernel scatters / gathers the padded planes on the compute stream.
+    const bool staged = c->stage_in && (nz + P - 1) / P <= c->stage_cz &&
+                        !getenv("MFC_STREAM_PITCHED");
+    CU_TRY(mk(c->ev_scat, P));
+    const int64_t plane_d = c->nl[0] * c->nl[1];
+    const size_t slot = stage_slot_bytes(c) / sizeof(double);
+    // one 2D copy per piece: E rows of n planes (host row pitch nz planes)
+    auto dense_copy = [&](bool h2d, double* dense, int64_t za, int64_t n, cudaStream_t on) -> int {
+        double* h = (h2d ? const_cast<double*>(q_in) : q_out) + (size_t)za * plane_d;
+        const size_t w = (size_t)n * plane_d * sizeof(double);
+        const size_t hp = (size_t)nz * plane_d * sizeof(double);
+        if (h2d) CU_TRY(cudaMemcpy2DAsync(dense, w, h, hp, w, c->E, cudaMemcpyHostToDevice, on));
+        else CU_TRY(cudaMemcpy2DAsync(h, hp, dense, w, w, c->E, cudaMemcpyDeviceToHost, on));
+        return MFC_OK;
+    };
+    auto planes_kernel = [&](double* dense, int64_t za, int64_t n, bool to_dense) -> int {
+        dense_planes_kernel<<<grid_for(n * plane_d * c->E, 256), 256, 0, s>>>(
+            dense, q_dev, c->offset, c->stride[0], c->stride[1], c->stride[2], (int)c->nl[0],
+            (int)c->nl[1], za, (int)n, c->E, to_dense);
+        CU_TRY(cudaGetLastError());
+        ++c->launches;
+        return MFC_OK;
+    };
+    // 1. input pieces (upload order: periodic, the piece holding the last 3 planes first)
+    const int first = per ? P - 1 : 0;
+    std::vector<int> order(P), rank_of(P);
     for (int i = 0; i < P; ++i) {
-        const int j = (first + i) % P;
-        int64_t z0, z1, e0, e1;
-        chunk_range(c, cz, j, &z0, &z1, &e0, &e1);
-        if ((st = copy_planes_h(c, true, q_in, nullptr, q_dev, c, z0, z0, z1 - z0, c->st_in)))
-            return st;
+        order[i] = (first + i) % P;
+        rank_of[order[i]] = i;
+    }
+    auto enqueue_h2d = [&](int i) -> int {   // input piece of upload rank i
+        const int j = order[i];
+        int r;
+        if (staged) {
+            // slot i % R is free once piece order[i - R] has been scattered (that scatter
+            // is enqueued on s before this call: see need_piece)
+            if (i >= kStageSlots)
+                CU_TRY(cudaStreamWaitEvent(c->st_in, c->ev_scat[order[i - kStageSlots]], 0));
+            if ((r = dense_copy(true, c->stage_in + (i % kStageSlots) * slot, z0(j), z1(j) - z0(j),
+                                c->st_in)))
+                return r;
+        } else if ((r = copy_planes_h(c, true, q_in, nullptr, q_dev, z0(j), z1(j) - z0(j), c->st_in))) {
+            return r;
+        }
         CU_TRY(cudaEventRecord(c->ev_piece[j], c->st_in));
-    }
-    // 2. chunks
-    for (int k = 0; k < P; ++k) {
-        mfc_ctx* kc = c->chunks[k];
-        int64_t z0, z1, e0, e1;
-        chunk_range(c, cz, k, &z0, &z1, &e0, &e1);
-        // pieces overlapping [e0, e1) (mod nz)
-        for (int64_t z = e0; z < e1; z += 1) {
-            const int64_t zz = ((z % nz) + nz) % nz;
-            const int j = (int)(zz / cz);
-            if (z == e0 || zz % cz == 0) CU_TRY(cudaStreamWaitEvent(s, c->ev_piece[j], 0));
+        mark("in" + std::to_string(j), c->st_in);
+        return MFC_OK;
+    };
+    for (int i = 0; i < (staged ? std::min(P, kStageSlots) : P); ++i)
+        if ((st = enqueue_h2d(i))) return st;
+    // 2. the wavefront
+    int scattered = 0;   // pieces scattered into q_dev, in upload order
+    auto need_piece = [&](int j) -> int {
+        if (!staged) return cudaStreamWaitEvent(s, c->ev_piece[j], 0) == cudaSuccess
+                                ? MFC_OK : fail(MFC_ECUDA, "stream wait");
+        while (scattered <= rank_of[j]) {
+            const int jj = order[scattered];
+            CU_TRY(cudaStreamWaitEvent(s, c->ev_piece[jj], 0));
+            int r = planes_kernel(c->stage_in + (scattered % kStageSlots) * slot, z0(jj),
+                                  z1(jj) - z0(jj), false);
+            if (r) return r;
+            CU_TRY(cudaEventRecord(c->ev_scat[jj], s));
+            if (scattered + kStageSlots < P && (r = enqueue_h2d(scattered + kStageSlots))) return r;
+            ++scattered;
         }
-        if (k >= 2) CU_TRY(cudaStreamWaitEvent(s, c->ev_out[k - 2], 0));
-        double* qk = (double*)(c->ws + (size_t)(k & 1) * 4 * cb);
-        // planes [e0, e1) of q_dev -> chunk planes [0, e1-e0): contiguous runs mod nz
-        const size_t plane_b = (size_t)c->stride[1] * sizeof(double);
-        for (int64_t z = e0; z < e1;) {
-            const int64_t zz = ((z % nz) + nz) % nz;
-            const int64_t run = std::min(e1 - z, nz - zz);
-            const double* src = q_dev + (c->off[2] + zz) * c->stride[1];
-            double* dst = qk + (kc->off[2] + (z - e0)) * kc->stride[1];
-            static const bool ce = getenv("MFC_STREAM_CE") != nullptr;
-            if (ce || (run * c->stride[1]) % 2 || c->stride[0] % 2 || kc->stride[0] % 2 ||
-                (c->off[2] + zz) * c->stride[1] % 2 || (kc->off[2] + z - e0) * kc->stride[1] % 2) {
-                CU_TRY(cudaMemcpy2DAsync(dst, (size_t)kc->stride[0] * sizeof(double), src,
-                                         (size_t)c->stride[0] * sizeof(double), run * plane_b,
-                                         c->E, cudaMemcpyDeviceToDevice, s));
-            } else {
-                const int64_t n2 = run * c->stride[1] / 2;
-                copy_planes_kernel<<<grid_for(n2 * c->E, 256), 256, 0, s>>>(
-                    dst, kc->stride[0], src, c->stride[0], n2, c->E);
-                CU_TRY(cudaGetLastError());
-                ++c->launches;
+        return MFC_OK;
+    };
+    std::vector<int> gathered;   // chunks gathered for D2H, in order
+    auto stage = [&](int sg, int k) -> int {
+        int r;
+        if (sg == 0) {   // the input pieces within reach of chunk k
+            for (int m = k - 1; m <= k + 1; ++m) {
+                if (!per && (m < 0 || m >= P)) continue;
+                if ((r = need_piece((m + P) % P))) return r;
             }
-            z += run;
         }
-        if ((st = rk3_group(&kc, &qk, 1, dt, s))) return st;
-        c->launches += kc->launches;
-        CU_TRY(cudaEventRecord(c->ev_comp[k], s));
-        CU_TRY(cudaStreamWaitEvent(c->st_out, c->ev_comp[k], 0));
-        if ((st = copy_planes_h(c, false, nullptr, q_out, qk, kc, z0 - e0, z0, z1 - z0, c->st_out)))
-            return st;
-        CU_TRY(cudaEventRecord(c->ev_out[k], c->st_out));
+        if ((r = rk3_stage_planes(c, q_dev, sg, dt, z0(k), z1(k), s))) return r;
+        mark("s" + std::to_string(sg + 1) + "c" + std::to_string(k), s);
+        if (sg == 2) {
+            double* dense = nullptr;
+            if (staged) {
+                const int o = (int)gathered.size();
+                dense = c->stage_out + (o % kStageSlots) * slot;
+                // slot o % R is free once the D2H of the chunk gathered R earlier is done
+                if (o >= kStageSlots) CU_TRY(cudaStreamWaitEvent(s, c->ev_out[gathered[o - kStageSlots]], 0));
+                gathered.push_back(k);
+                if ((r = planes_kernel(dense, z0(k), z1(k) - z0(k), true))) return r;
+            }
+            CU_TRY(cudaEventRecord(c->ev_comp[k], s));
+            CU_TRY(cudaStreamWaitEvent(c->st_out, c->ev_comp[k], 0));
+            if (staged) {
+                if ((r = dense_copy(false, dense, z0(k), z1(k) - z0(k), c->st_out))) return r;
+            } else if ((r = copy_planes_h(c, false, nullptr, q_out, q_dev, z0(k), z1(k) - z0(k),
+                                          c->st_out))) {
+                return r;
+            }
+            CU_TRY(cudaEventRecord(c->ev_out[k], c->st_out));
+            mark("out" + std::to_string(k), c->st_out);
+        }
+        return MFC_OK;
+    };
+    c->launches = 0;
+    const int k0 = per ? 1 : 0;                     // periodic: chunk 0's stages 2, 3 last
+    for (int j = 0; j <= P + 1; ++j) {
+        if (j < P && (st = stage(0, j))) return st;
+        if (j - 1 >= k0 && j - 1 < P && (st = stage(1, j - 1))) return st;
+        if (j - 2 >= k0 && j - 2 < (per ? P - 1 : P) && (st = stage(2, j - 2))) return st;
     }
-    CU_TRY(cudaStreamWaitEvent(s, c->ev_out[P - 1], 0));
+    if (per) {
+        if ((st = stage(1, 0)) || (st = stage(2, P - 1)) || (st = stage(2, 0))) return st;
+    }
+    CU_TRY(cudaStreamWaitEvent(s, c->ev_out[per ? 0 : P - 1], 0));
     CU_TRY(cudaStreamSynchronize(s));
+    if (tr) {   // MFC_STREAM_TRACE: ms after the start at which each piece / chunk finished
+        std::string line = "mfc stream trace (ms): ";
+        for (size_t i = 0; i < tr_ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tr_ev[0].second, tr_ev[i].second);
+            char b[64];
+            snprintf(b, sizeof b, "%s %.2f; ", tr_ev[i].first.c_str(), ms);
+            line += b;
+        }
+        fprintf(stderr, "%s\n", line.c_str());
+        for (auto& e : tr_ev) cudaEventDestroy(e.second);
+    }
     return MFC_OK;
 }
 
@@ -1175,6 +1228,11 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
             if (c->bc[2 * k + sd] == BC_NEIGHBOR)
                 need += 2 * (((size_t)c->face_elems[k] * sizeof(double) + 255) / 256 * 256);
     }
+    // streamed advance_host (single-rank 3D): dense staging rings for the PCIe copies
+    if (D == 3 && nranks == 1 && c->nl[2] >= 3 * kStageCzMin) {
+        c->stage_cz = std::max<int64_t>(kStageCzMin, (c->nl[2] + kStreamChunks - 1) / kStreamChunks);
+        need += 2 * kStageSlots * stage_slot_bytes(c);
+    }
     c->ws_need = need;
     if (const char* sg = getenv("MFC_SEG")) c->seg = atoi(sg);
     if (const char* xb = getenv("MFC_XBASE")) c->xbase = atoi(xb) != 0;
@@ -1244,6 +1302,10 @@ int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
     c->S1 = (double*)w; w += sb;
     c->S2 = (double*)w; w += sb;
     c->acc = (double*)w; w += sb;
+    if (c->stage_cz) {
+        c->stage_in = (double*)w; w += kStageSlots * stage_slot_bytes(c);
+        c->stage_out = (double*)w; w += kStageSlots * stage_slot_bytes(c);
+    }
     for (int f = 0; f < 6; ++f) {
         c->sendb[f] = c->recvb[f] = nullptr;
         if (f / 2 < c->D && c->bc[f] == BC_NEIGHBOR) {
@@ -1645,10 +1707,10 @@ int mfc_finalize(mfc_ctx* c) {
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->comm) ncclCommDestroy(c->comm);
-    free_chunks(c);
     for (auto e : c->ev_piece) cudaEventDestroy(e);
     for (auto e : c->ev_comp) cudaEventDestroy(e);
     for (auto e : c->ev_out) cudaEventDestroy(e);
+    for (auto e : c->ev_scat) cudaEventDestroy(e);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
     if (c->st_in) cudaStreamDestroy(c->st_in);
     if (c->st_out) cudaStreamDestroy(c->st_out);

@@ -120,6 +120,8 @@ struct SweepArgs {
     int64_t base;                   // offset of interior cell (0,0,0), equation 0
     int32_t nS, nA, nB;             // interior extents along sweep / lane / third axis
     int32_t T;                      // segment length along the sweep
+    int32_t s_lo, s_hi;             // cells [s_lo, s_hi) of the sweep axis are updated
+                                    // (segments start at s_lo; [0, nS) for a whole sweep)
     GhostMap gm;                    // boundary maps of the sweep axis (see map_cell)
     double invd;                    // 1/dx along DIR
     double eps4;                    // 4 x WENO epsilon (weno5 works with beta' = 4 beta)
@@ -198,8 +200,8 @@ sweep_kernel(const SweepArgs a) {
     const int ia = (wl % nAw) * 32 + threadIdx.x;
     const int ib = wl / nAw;
     if (ia >= a.nA || ib >= a.nB) return;                   // no block-level sync below
-    const int s0 = blockIdx.z * a.T;
-    const int s1 = min(s0 + a.T, a.nS);   // cells s0 .. s1-1 are updated
+    const int s0 = a.s_lo + blockIdx.z * a.T;
+    const int s1 = min(s0 + a.T, a.s_hi);   // cells s0 .. s1-1 are updated
     const int64_t line = a.base + (int64_t)ia * a.sA + (int64_t)ib * a.sB;
     const double* __restrict__ q = a.q;
     // fused halo: does my line touch a shared face (tangential faces: the whole line;

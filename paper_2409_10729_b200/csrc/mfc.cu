@@ -1,10 +1,13 @@
-// mfc.cu -- libmfc context, layout, ghost/halo kernels and the C ABI of include/mfc.h.
+// mfc.cu -- libmfc context, layout, ghost/halo kernels, the streamed host-to-host step
+// and the C ABI of include/mfc.h.
 //
-// Call graph of one SSP-RK3 step (DESIGN.md §5):
+// Call graph of one SSP-RK3 step (DESIGN.md §6):
 //   for stage s = 1..3:
-//     ghost fill of the stage state: bc_fill (physical faces, one kernel per active
-//       dimension) + halo exchange (pack -> NCCL send/recv or loopback copies -> unpack)
-//     sweep x (acc = c_x), sweep y (acc += c_y), sweep z with the RK stage epilogue
+//     halo exchange of the stage state with neighbour ranks only (pack -> NCCL
+//       send/recv or loopback copies -> unpack, on a comm stream; or none with the
+//       fused halo); physical boundaries are applied inside the sweeps by index mapping
+//     sweep x (acc = cb*q^s + w*c_x), sweep y (acc += w*c_y), sweep z (stage result =
+//       acc + w*c_z + ca*q^n), the sweeps along split dimensions waiting for the halo
 //   stage 1: q -> S1,  stage 2: S1 -> S2,  stage 3: S2 -> q (in place, pointwise)
 #include <cuda.h>
 #include <cuda_runtime.h>

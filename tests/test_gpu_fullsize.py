@@ -53,6 +53,29 @@ def test_c3_full_rk3_step(c3):
     assert np.all(err <= 10 * RHS_TOL), err
 
 
+def test_c2_full_rhs_and_step():
+    """C2 at its BASELINE size (1024 x 512, 2D, E = 7; x extrapolation, y reflective),
+    the configuration `bench.py --config C2` times: full RHS and one RK3 step."""
+    pb = W.c2_shock_bubble()
+    P, v, q = oracle_inputs(pb)
+    s = mfc.Solver(pb)
+    qd = s.state_from_cons(q)
+    rd = s.rhs(qd)
+    torch.cuda.synchronize()
+    got = s.interior(rd).cpu().numpy()
+    ref = O.rhs(P, q)
+    err = rel_err(got, ref, rhs_flux_scale(pb, v, q))
+    record("rhs C2 full 1024x512 (bench launch config)", err, RHS_TOL, rel_err(got, ref))
+    assert np.all(err <= RHS_TOL), err
+    s.rk3_step(qd, pb.dt)
+    torch.cuda.synchronize()
+    got = s.interior(qd).cpu().numpy()
+    ref = O.rk3_step(P, q, pb.dt, 1)
+    err = rel_err(got - q, ref - q, pb.dt * rhs_flux_scale(pb, v, q))
+    record("1 RK3 step increment C2 full 1024x512", err, 10 * RHS_TOL)
+    assert np.all(err <= 10 * RHS_TOL), err
+
+
 def test_c3_full_advance_host_streamed(c3):
     """The e2e call of bench.py at full size: mfc_advance_host streams the step in
     z-chunks; it must equal the device step (test above) bit for bit."""

@@ -194,6 +194,40 @@ __device__ __forceinline__ void weno5(double a, double b, double c, double d, do
     vp = fma(Np, rcp(Dp), c);
 }
 
+// WENO5-JS with two FP64 operations fewer per variable than weno5 (same beta'_k, t_k,
+// P_k), used by the row-parallel x tile, whose 80 registers leave room for it; in the
+// 168-register y/z marches its longer-lived differences spill (r61: y/z +47% per
+// launch), so those keep weno5.
+//   candidates as corrections to c: A_k = 6(p_k - c) = (5D1-2D0, D1+2D2, 4D2-D3) for v-,
+//             (D0-4D1, -2D1-D2, 2D3-5D2) for v+,
+//   v = c + (1/6) (sum_k d_k P_k A_k) / (sum_k d_k P_k):  one reciprocal per side.
+// The numerator takes X_k = lambda (10 d_k/6) A_k with lambda = 2, which makes every X_k
+// ONE operation on the differences already formed (no product spent on a weight):
+//   v-: X = (A0/3, 2 A1, A2) = ((2/3) s0 + D1, 3 r1 + s1, D2 - r2),
+//       denominator 20 sum d_k P_k = 2 P0 + 12 P1 + 6 P2;
+//   v+: X = (A0, 2 A1, A2/3) = -(r0 + D1, 3 r1 - s1, D2 - (2/3) s2),
+//       denominator 6 P0 + 12 P1 + 2 P2.
+// (51 FP64 operations per variable; weno5 takes 53.)
+__device__ __forceinline__ void weno5_fewop(double a, double b, double c, double d, double e,
+                                      double eps4, double& vm, double& vp) {
+    constexpr double k133 = 13.0 / 3.0, k23 = 2.0 / 3.0;
+    const double D0 = b - a, D1 = c - b, D2 = d - c, D3 = e - d;
+    const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
+    const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
+    double t0 = fma(k133 * s0, s0, fma(r0, r0, eps4)); t0 *= t0;
+    double t1 = fma(k133 * s1, s1, fma(r1, r1, eps4)); t1 *= t1;
+    double t2 = fma(k133 * s2, s2, fma(r2, r2, eps4)); t2 *= t2;
+    const double P0 = t1 * t2, P1 = t0 * t2, P2 = t0 * t1;
+    const double xm0 = fma(k23, s0, D1), xm1 = fma(3.0, r1, s1), xm2 = D2 - r2;
+    const double Dm = fma(12.0, P1, fma(6.0, P2, 2.0 * P0));
+    const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
+    vm = fma(Nm, rcp(Dm), c);
+    const double yp0 = r0 + D1, yp1 = fma(3.0, r1, -s1), yp2 = fma(-k23, s2, D2);   // = -X
+    const double Dp = fma(12.0, P1, fma(2.0, P2, 6.0 * P0));
+    const double Np = fma(P2, yp2, fma(P1, yp1, P0 * yp0));
+    vp = fma(-Np, rcp(Dp), c);
+}
+
 // WENO3-JS ("third or fifth-order"; F2) for one variable of cell m from
 // a..c = v_{m-1..m+1}, in first differences D0 = b-a, D1 = c-b:
 //   beta = (D0^2, D1^2), alpha_k ~ d_k/(beta_k+eps)^2 multiplied through by t0 t1,

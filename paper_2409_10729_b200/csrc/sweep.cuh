@@ -43,10 +43,13 @@ enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3, M_ACCN = 4 };
 
 // Reconstruction of one variable of the window's centre cell (ORD = 5: cells w0..w4,
 // ORD = 3: the inner three).
-template <int ORD>
+// FEWOP: the WENO5 form with fewer FP64 operations but longer-lived temporaries
+// (x tile only, see weno5_fewop).
+template <int ORD, bool FEWOP = false>
 __device__ __forceinline__ void reconstruct(double w0, double w1, double w2, double w3, double w4,
                                             double eps4, double eps, double& vm, double& vp) {
-    if constexpr (ORD == 5) weno5(w0, w1, w2, w3, w4, eps4, vm, vp);
+    if constexpr (ORD == 5 && FEWOP) weno5_fewop(w0, w1, w2, w3, w4, eps4, vm, vp);
+    else if constexpr (ORD == 5) weno5(w0, w1, w2, w3, w4, eps4, vm, vp);
     else weno3(w1, w2, w3, eps, vm, vp);
 }
 
@@ -563,7 +566,7 @@ sweep_x_tile(const SweepArgs a, int W) {
     for (int e = 0; e < E; ++e) {
         const double* r = V + e * LV + t + 1;
         double vm;
-        reconstruct<ORD>(r[0], r[1], v[e], r[3], r[4], a.eps4, a.eps, vm, vp[e]);
+        reconstruct<ORD, true>(r[0], r[1], v[e], r[3], r[4], a.eps4, a.eps, vm, vp[e]);
         VM[e * LM + t + 1] = vm;
     }
     if (!wrap) {
@@ -573,7 +576,7 @@ sweep_x_tile(const SweepArgs a, int W) {
             const int e = right ? k - E : k;
             const double* r = V + e * LV + (right ? seg + 1 : 0);
             double bm, bp;
-            reconstruct<ORD>(r[0], r[1], r[2], r[3], r[4], a.eps4, a.eps, bm, bp);
+            reconstruct<ORD, true>(r[0], r[1], r[2], r[3], r[4], a.eps4, a.eps, bm, bp);
             if (right) VPX[e] = bp;
             else VM[e * LM] = bm;
         }

@@ -33,6 +33,9 @@
 #pragma once
 #include "physics.cuh"
 
+#ifndef MFC_MARCH_FEWOP
+#define MFC_MARCH_FEWOP false   // weno5_fewop in the ring marches (spills at 168 registers)
+#endif
 #ifndef MFC_ACC_MINB
 #define MFC_ACC_MINB 3   // resident 128-thread blocks per SM for the non-RK sweep modes
 #endif
@@ -177,13 +180,23 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 
 // 3 resident blocks (12 warps/SM, <= 168 registers) where that does not spill (the
 // non-RK modes for E <= 8); 2 blocks otherwise.
-template <class M, int MODE>
+// The y march of a 3D sweep set (M_ACC, E <= 8) runs the fewer-op WENO (weno5_fewop) at
+// 2 blocks/SM, where it has the registers for it: C3 y 2.176 -> 2.096 ms per step with
+// 128-cell segments (r62-r63, same box; mfc.cu launch_sweep_dir keeps the same test).  The z march loses at 2 blocks/SM (2.246 -> 2.292 ms) and spills
+// with weno5_fewop at 3, so it keeps weno5.
+template <class M, int DIR, int MODE>
+__host__ __device__ constexpr bool march_fewop() {
+    return MFC_MARCH_FEWOP || (DIR == 1 && M::D == 3 && MODE == M_ACC && M::E <= 8);
+}
+
+template <class M, int DIR, int MODE>
 __host__ __device__ constexpr int sweep_min_blocks() {
+    if (march_fewop<M, DIR, MODE>()) return 2;
     return ((MODE == M_ACC || MODE == M_SET || MODE == M_ACCN) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
-__global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, MODE>())
+__global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, DIR, MODE>())
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
     using R = Rings<MODE>;
@@ -291,7 +304,8 @@ sweep_kernel(const SweepArgs a) {
         double vm[E], vp[E];
 #pragma unroll
         for (int e = 0; e < E; ++e)
-            reconstruct<ORD>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, a.eps, vm[e], vp[e]);
+            reconstruct<ORD, march_fewop<M, DIR, MODE>()>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e],
+                                                            a.eps4, a.eps, vm[e], vp[e]);
 
         if (j >= s0) {
             double F[E], uf;
@@ -452,7 +466,7 @@ sweep_x_staged(const SweepArgs a) {
         double vm[E], vp[E];
 #pragma unroll
         for (int e = 0; e < E; ++e)
-            reconstruct<ORD>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, a.eps, vm[e], vp[e]);
+            reconstruct<ORD, MFC_MARCH_FEWOP>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, a.eps, vm[e], vp[e]);
         if (j >= s0) {
             double F[E], uf;
             hllc<M, 0>(vm_prev, vp, a.mat, F, uf);

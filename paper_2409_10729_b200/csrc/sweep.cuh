@@ -137,6 +137,18 @@ struct SweepArgs {
     PeerOut po;                     // fused halo stores (last sweep of a stage only)
 };
 
+// The 3D y and z marches (M_ACC, M_ACCN; E <= 8) run the fewer-op WENO (weno5_fewop) at
+// 2 blocks/SM, where they have the registers for it, with 128-cell segments and ring
+// prefetch distance 2 for all operands (mfc.cu launch_sweep_dir keeps the same test):
+// C3 y 2.177 -> 2.096, z 2.246 -> 2.189 ms per step (r62-r64, same box).  The lean
+// weno5 at 3 blocks/SM (168 registers) is what the other marches run; weno5_fewop
+// spills there (+47%).
+template <class M, int DIR, int MODE>
+__host__ __device__ constexpr bool march_fewop() {
+    return MFC_MARCH_FEWOP ||
+           (DIR >= 1 && M::D == 3 && (MODE == M_ACC || MODE == M_ACCN) && M::E <= 8);
+}
+
 // Per-thread shared-memory rings for the streamed operands (filled by cp.async PD
 // march steps ahead of use; element (slot, e) of thread t at [(slot*E + e)*nthreads + t],
 // so a warp's copies and reads are contiguous 256-byte rows):
@@ -146,10 +158,9 @@ struct SweepArgs {
 #ifndef MFC_RING_PD
 #define MFC_RING_PD 2    // prefetch distance of the rings, in march steps
 #endif
-template <int MODE>
+template <int MODE, int PD_>
 struct Rings {
-    // M_ACCN streams three operands: prefetch distance 1 keeps it at 48 KB per block
-    static constexpr int PD = MODE == M_ACCN ? 1 : MFC_RING_PD;
+    static constexpr int PD = PD_;
     static constexpr bool RK = MODE == M_RKACC || MODE == M_RKINIT;
     // state cell c lives from its fetch (step c-2-PD) to its conversion (step c-2), or
     // to its use as the stage operand q^s (step c+1); operands of cell c from step
@@ -161,8 +172,17 @@ struct Rings {
     static constexpr int SLOTS = QS + AS + NS;
 };
 
-template <class M, int MODE>
-constexpr size_t sweep_smem_per_thread() { return (size_t)Rings<MODE>::SLOTS * M::E * sizeof(double); }
+// M_ACCN streams three operands: prefetch distance 1 keeps it at 48 KB per block at
+// 3 blocks/SM
+template <class M, int DIR, int MODE>
+__host__ __device__ constexpr int ring_pd() {
+    return (MODE == M_ACCN && !march_fewop<M, DIR, MODE>()) ? 1 : MFC_RING_PD;
+}
+template <class M, int DIR, int MODE>
+using RingsOf = Rings<MODE, ring_pd<M, DIR, MODE>()>;
+
+template <class M, int DIR, int MODE>
+constexpr size_t sweep_smem_per_thread() { return (size_t)RingsOf<M, DIR, MODE>::SLOTS * M::E * sizeof(double); }
 
 // Threads per block of the ring sweeps (a compile-time constant so that ring offsets
 // fold into instruction immediates): 128, or 64 where 12 ring slots of E > 9 doubles
@@ -178,17 +198,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-// 3 resident blocks (12 warps/SM, <= 168 registers) where that does not spill (the
-// non-RK modes for E <= 8); 2 blocks otherwise.
-// The y march of a 3D sweep set (M_ACC, E <= 8) runs the fewer-op WENO (weno5_fewop) at
-// 2 blocks/SM, where it has the registers for it: C3 y 2.176 -> 2.096 ms per step with
-// 128-cell segments (r62-r63, same box; mfc.cu launch_sweep_dir keeps the same test).  The z march loses at 2 blocks/SM (2.246 -> 2.292 ms) and spills
-// with weno5_fewop at 3, so it keeps weno5.
-template <class M, int DIR, int MODE>
-__host__ __device__ constexpr bool march_fewop() {
-    return MFC_MARCH_FEWOP || (DIR == 1 && M::D == 3 && MODE == M_ACC && M::E <= 8);
-}
-
 template <class M, int DIR, int MODE>
 __host__ __device__ constexpr int sweep_min_blocks() {
     if (march_fewop<M, DIR, MODE>()) return 2;
@@ -199,7 +208,7 @@ template <class M, int DIR, int MODE, int ORD, bool PEER = false>
 __global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, DIR, MODE>())
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
-    using R = Rings<MODE>;
+    using R = RingsOf<M, DIR, MODE>;
     extern __shared__ double smem[];
     constexpr int nth = sweep_nth<M, MODE>();            // == blockDim.x * blockDim.y
     const int tid = threadIdx.y * 32 + threadIdx.x;      // blockDim.x == 32

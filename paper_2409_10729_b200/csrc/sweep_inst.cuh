@@ -72,7 +72,7 @@ static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
     const int64_t warp_lines = (int64_t)((a.nA + 31) / 32) * a.nB;
     g = dim3((unsigned)((warp_lines + b.y - 1) / b.y), 1, g.z);
-    const size_t smem = sweep_smem_per_thread<M, MODE>() * NTH;
+    const size_t smem = sweep_smem_per_thread<M, DIR, MODE>() * NTH;
     static size_t attr = 0;
     if (smem > attr) {
         cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE, ORD, PEER>,

@@ -86,31 +86,33 @@ __device__ __forceinline__ void cons_to_prim(const double (&q)[M::E], double (&v
 template <class M>
 __device__ __forceinline__ void cons_to_prim_fast(const double (&q)[M::E], double (&v)[M::E],
                                                   const Materials& mat) {
+    // explicit roundings: a march converts its first cells and the streamed ones at two
+    // inline sites, which must not contract differently (bitwise segment independence)
     double rho = q[0];
 #pragma unroll
-    for (int i = 1; i < M::N; ++i) rho += q[i];
-    double G = q[M::IA] * mat.Gam[0];
-    double P = q[M::IA] * mat.Pi[0];
+    for (int i = 1; i < M::N; ++i) rho = __dadd_rn(rho, q[i]);
+    double G = __dmul_rn(q[M::IA], mat.Gam[0]);
+    double P = __dmul_rn(q[M::IA], mat.Pi[0]);
 #pragma unroll
     for (int i = 1; i < M::N; ++i) {
-        G = fma(q[M::IA + i], mat.Gam[i], G);
-        P = fma(q[M::IA + i], mat.Pi[i], P);
+        G = __fma_rn(q[M::IA + i], mat.Gam[i], G);
+        P = __fma_rn(q[M::IA + i], mat.Pi[i], P);
     }
-    const double r = rcp(rho * G);
-    const double irho = G * r, iG = rho * r;
+    const double r = rcp(__dmul_rn(rho, G));
+    const double irho = __dmul_rn(G, r), iG = __dmul_rn(rho, r);
     double ke = 0.0;
 #pragma unroll
     for (int k = 0; k < M::D; ++k) {
-        const double u = q[M::IM + k] * irho;
+        const double u = __dmul_rn(q[M::IM + k], irho);
         v[M::IM + k] = u;
-        ke = fma(q[M::IM + k], u, ke);
+        ke = __fma_rn(q[M::IM + k], u, ke);
     }
 #pragma unroll
     for (int i = 0; i < M::N; ++i) {
         v[i] = q[i];
         v[M::IA + i] = q[M::IA + i];
     }
-    v[M::IE] = (fma(-0.5, ke, q[M::IE]) - P) * iG;
+    v[M::IE] = __dmul_rn(__dsub_rn(__fma_rn(-0.5, ke, q[M::IE]), P), iG);
 }
 
 // Fast reciprocal square root: MUFU.RSQ64H seed y0 and one third-order correction
@@ -164,10 +166,12 @@ __device__ __forceinline__ void prim_to_cons(const double (&v)[M::E], double (&q
 //             (D0-4D1, -2D1-D2, 2D3-5D2) for v+,
 //   v = c + (sum_k d_k P_k (p_k - c)) / (sum_k d_k P_k):  one reciprocal per side,
 //   with the linear weights scaled to integers (below) so no product is spent on them.
-__device__ __forceinline__ void weno5(double a, double b, double c, double d, double e,
-                                      double eps4, double& vm, double& vp) {
+// (weno5_d takes the differences D0..D3 and the centre value c: the marches carry
+//  D0, D1 from the previous step, where they were that step's D1, D2 -- the same
+//  subtractions of the same operands, so bitwise the same values.)
+__device__ __forceinline__ void weno5_d(double D0, double D1, double D2, double D3, double c,
+                                        double eps4, double& vm, double& vp) {
     constexpr double k133 = 13.0 / 3.0;
-    const double D0 = b - a, D1 = c - b, D2 = d - c, D3 = e - d;
     const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
     const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
     double t0 = fma(k133 * s0, s0, fma(r0, r0, eps4)); t0 *= t0;
@@ -208,10 +212,9 @@ __device__ __forceinline__ void weno5(double a, double b, double c, double d, do
 //   v+: X = (A0, 2 A1, A2/3) = -(r0 + D1, 3 r1 - s1, D2 - (2/3) s2),
 //       denominator 6 P0 + 12 P1 + 2 P2.
 // (51 FP64 operations per variable; weno5 takes 53.)
-__device__ __forceinline__ void weno5_fewop(double a, double b, double c, double d, double e,
-                                      double eps4, double& vm, double& vp) {
+__device__ __forceinline__ void weno5_fewop_d(double D0, double D1, double D2, double D3, double c,
+                                              double eps4, double& vm, double& vp) {
     constexpr double k133 = 13.0 / 3.0, k23 = 2.0 / 3.0;
-    const double D0 = b - a, D1 = c - b, D2 = d - c, D3 = e - d;
     const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
     const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
     double t0 = fma(k133 * s0, s0, fma(r0, r0, eps4)); t0 *= t0;
@@ -226,6 +229,15 @@ __device__ __forceinline__ void weno5_fewop(double a, double b, double c, double
     const double Dp = fma(12.0, P1, fma(2.0, P2, 6.0 * P0));
     const double Np = fma(P2, yp2, fma(P1, yp1, P0 * yp0));
     vp = fma(-Np, rcp(Dp), c);
+}
+
+__device__ __forceinline__ void weno5(double a, double b, double c, double d, double e,
+                                      double eps4, double& vm, double& vp) {
+    weno5_d(b - a, c - b, d - c, e - d, c, eps4, vm, vp);
+}
+__device__ __forceinline__ void weno5_fewop(double a, double b, double c, double d, double e,
+                                            double eps4, double& vm, double& vp) {
+    weno5_fewop_d(b - a, c - b, d - c, e - d, c, eps4, vm, vp);
 }
 
 // WENO3-JS ("third or fifth-order"; F2) for one variable of cell m from

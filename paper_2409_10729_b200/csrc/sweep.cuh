@@ -262,7 +262,15 @@ sweep_kernel(const SweepArgs a) {
     };
     auto inc = [](int k, int n) { return k + 1 == n ? 0 : k + 1; };
 
-    double w[5][E];        // primitive window: cells j-2 .. j+2
+    // Primitive window of cells j-2 .. j+2 (a, b, c, d, e).  The DW marches carry it in
+    // first differences instead: w[0] = D0 = b-a, w[1] = D1 = c-b, w[2] = c, w[3] = d,
+    // w[4] = e (the cell converted this step), so a step forms D2 = d-c, D3 = e-d only
+    // (-2 FP64 per variable; bitwise the same differences), and the volume fractions
+    // of cell j-1 (the alpha div(u) source) ride along in bA.
+    // (the 2-block 3D marches only: at 168 registers the 2D/1D RHS marches spill with it)
+    constexpr bool DW = ORD == 5 && march_fewop<M, DIR, MODE>();
+    double w[5][E];
+    double bA[M::N];
     {
         double qc[E];
 #pragma unroll
@@ -277,6 +285,17 @@ sweep_kernel(const SweepArgs a) {
                 for (int e = 0; e < E; ++e) at(ringQ, (s0 - 4 + k + 3) % R::QS, e) = qc[e];
             }
             cons_to_prim_fast<M>(qc, w[k], a.mat);
+        }
+        if constexpr (DW) {           // cells s0-3 .. s0 in w[1..4] -> D0, D1, c, d, b_alpha
+#pragma unroll
+            for (int i = 0; i < M::N; ++i) bA[i] = w[2][M::IA + i];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                w[0][e] = w[2][e] - w[1][e];
+                w[1][e] = w[3][e] - w[2][e];
+                w[2][e] = w[3][e];
+                w[3][e] = w[4][e];
+            }
         }
     }
 #pragma unroll
@@ -297,10 +316,12 @@ sweep_kernel(const SweepArgs a) {
         if constexpr (R::PD == 2) cp_async_wait_1();   // group of step j has landed
         else cp_async_wait_all();
         issue(j + R::PD, kqf, kaf);
+        if constexpr (!DW) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < 4; ++k) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) w[k][e] = w[k + 1][e];
+                for (int e = 0; e < E; ++e) w[k][e] = w[k + 1][e];
+            }
         }
         {
             double qc[E];
@@ -311,10 +332,25 @@ sweep_kernel(const SweepArgs a) {
         }
 
         double vm[E], vp[E];
+        double bAn[M::N];      // (DW) volume fractions of cell j, the next step's b_alpha
 #pragma unroll
-        for (int e = 0; e < E; ++e)
-            reconstruct<ORD, march_fewop<M, DIR, MODE>()>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e],
-                                                            a.eps4, a.eps, vm[e], vp[e]);
+        for (int e = 0; e < E; ++e) {
+            if constexpr (DW) {
+                const double D2 = w[3][e] - w[2][e], D3 = w[4][e] - w[3][e];
+                if constexpr (march_fewop<M, DIR, MODE>())
+                    weno5_fewop_d(w[0][e], w[1][e], D2, D3, w[2][e], a.eps4, vm[e], vp[e]);
+                else
+                    weno5_d(w[0][e], w[1][e], D2, D3, w[2][e], a.eps4, vm[e], vp[e]);
+                if (e >= M::IA) bAn[e - M::IA] = w[2][e];
+                w[0][e] = w[1][e];
+                w[1][e] = D2;
+                w[2][e] = w[3][e];
+                w[3][e] = w[4][e];
+            } else {
+                reconstruct<ORD, march_fewop<M, DIR, MODE>()>(w[0][e], w[1][e], w[2][e], w[3][e],
+                                                                w[4][e], a.eps4, a.eps, vm[e], vp[e]);
+            }
+        }
 
         if (j >= s0) {
             double F[E], uf;
@@ -327,7 +363,7 @@ sweep_kernel(const SweepArgs a) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     double r = F_prev[e] - F[e];                 // dx * c_e
-                    if (e >= M::IA) r = fma(w[1][e], du, r);
+                    if (e >= M::IA) r = fma(DW ? bA[e - M::IA] : w[1][e], du, r);
                     double out;
                     if (MODE == M_SET) out = r * a.invd;
                     else if (MODE == M_ACC) out = fma(a.w * a.invd, r, at(ringA, ka, e));
@@ -362,6 +398,10 @@ sweep_kernel(const SweepArgs a) {
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
+        if constexpr (DW) {
+#pragma unroll
+            for (int i = 0; i < M::N; ++i) bA[i] = bAn[i];
+        }
         kq = inc(kq, R::QS);
         kqf = inc(kqf, R::QS);
         kqs = inc(kqs, R::QS);

@@ -36,6 +36,9 @@
 #ifndef MFC_MARCH_FEWOP
 #define MFC_MARCH_FEWOP false   // weno5_fewop in the ring marches (spills at 168 registers)
 #endif
+#ifndef MFC_FEWOP_EMAX
+#define MFC_FEWOP_EMAX 8
+#endif
 #ifndef MFC_ACC_MINB
 #define MFC_ACC_MINB 3   // resident 128-thread blocks per SM for the non-RK sweep modes
 #endif
@@ -140,13 +143,16 @@ struct SweepArgs {
 // The 3D y and z marches (M_ACC, M_ACCN; E <= 8) run the fewer-op WENO (weno5_fewop) at
 // 2 blocks/SM, where they have the registers for it, with 128-cell segments and ring
 // prefetch distance 2 for all operands (mfc.cu launch_sweep_dir keeps the same test):
-// C3 y 2.177 -> 2.096, z 2.246 -> 2.189 ms per step (r62-r64, same box).  The lean
+// C3 y 2.177 -> 2.096, z 2.246 -> 2.189 ms per step (r62-r64, same box).  E = 10 (C5,
+// already 2 blocks/SM): the y march gains (20.8 -> 19.9 ms per step), the z march
+// loses (22.1 -> 23.2), r68.  The lean
 // weno5 at 3 blocks/SM (168 registers) is what the other marches run; weno5_fewop
 // spills there (+47%).
 template <class M, int DIR, int MODE>
 __host__ __device__ constexpr bool march_fewop() {
     return MFC_MARCH_FEWOP ||
-           (DIR >= 1 && M::D == 3 && (MODE == M_ACC || MODE == M_ACCN) && M::E <= 8);
+           (DIR >= 1 && M::D == 3 && (MODE == M_ACC || MODE == M_ACCN) &&
+            (M::E <= MFC_FEWOP_EMAX || DIR == 1));
 }
 
 // Per-thread shared-memory rings for the streamed operands (filled by cp.async PD

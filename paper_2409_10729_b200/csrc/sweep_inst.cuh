@@ -91,7 +91,8 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
               // segments with boundary cells); MFC_X_STAGED: the staged march.
               // The host asks x_rows_used() before choosing M_RKINIT (tile kernel only).
               if (x_rows_used(a.nS)) {
-                const int W = (int)std::min<int64_t>(8, (a.nS + 31) / 32);
+                static const int wmax = getenv("MFC_XTILE_W") ? atoi(getenv("MFC_XTILE_W")) : 8;
+                const int W = (int)std::min<int64_t>(wmax, (a.nS + 31) / 32);
                 const int nseg = (a.nS + 32 * W - 1) / (32 * W);
                 const size_t smem = sizeof(double) * x_tile_smem_doubles<M>(32 * W);
                 static size_t attr = 0;

@@ -36,6 +36,9 @@
 #ifndef MFC_MARCH_FEWOP
 #define MFC_MARCH_FEWOP false   // weno5_fewop in the ring marches (spills at 168 registers)
 #endif
+#ifndef MFC_DW_ALL
+#define MFC_DW_ALL false        // experiment: the difference window in every WENO5 march
+#endif
 #ifndef MFC_FEWOP_EMAX
 #define MFC_FEWOP_EMAX 8
 #endif
@@ -273,8 +276,11 @@ sweep_kernel(const SweepArgs a) {
     // w[4] = e (the cell converted this step), so a step forms D2 = d-c, D3 = e-d only
     // (-2 FP64 per variable; bitwise the same differences), and the volume fractions
     // of cell j-1 (the alpha div(u) source) ride along in bA.
-    // (the 2-block 3D marches only: at 168 registers the 2D/1D RHS marches spill with it)
-    constexpr bool DW = ORD == 5 && march_fewop<M, DIR, MODE>();
+    // (the 3D y/z marches, all at 2 blocks/SM: C5 z 22.3 -> 22.0 ms per step with the lean
+    // weno5 too, r70; at 168 registers the 2D/1D RHS marches spill with it, and C2's
+    // y march gains nothing)
+    constexpr bool DW = ORD == 5 && (MFC_DW_ALL || (M::D == 3 && DIR >= 1 &&
+                                                    (MODE == M_ACC || MODE == M_ACCN)));
     double w[5][E];
     double bA[M::N];
     {

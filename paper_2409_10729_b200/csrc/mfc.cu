@@ -133,8 +133,8 @@ struct mfc_ctx {
     double* stage_in = nullptr;    // kStageSlots dense input pieces [E][cz][ny][nx]
     double* stage_out = nullptr;   // kStageSlots dense result chunks
     std::vector<cudaEvent_t> ev_scat;
-    cudaStream_t st_in = nullptr, st_out = nullptr;
-    std::vector<cudaEvent_t> ev_piece, ev_comp, ev_out;
+    cudaStream_t st_in = nullptr, st_out = nullptr, st_s1 = nullptr;
+    std::vector<cudaEvent_t> ev_piece, ev_comp, ev_out, ev_s1;
     cudaEvent_t ev_start = nullptr;
 };
 
@@ -791,6 +791,15 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
 //   s     : the stage sweeps in wavefront order; stage 1 of chunk k waits for the
 //           pieces within 3 planes of it                                 -> ev_comp[k]
 //   st_out: D2H of chunk k's result planes into q_out                    -> ev_out[k]
+//   st_s1 : stage 1 of every chunk (and the scatters of the input pieces) -> ev_s1[k];
+//           s then runs stages 2 and 3 only, stage 2 of chunk k after ev_s1 of chunks
+//           k-1..k+1.  Stage 1 of chunk j+1 depends on input pieces alone, so it runs
+//           concurrently with stages 2/3 of the chunks behind it: the small chunk
+//           kernels fill each other's tails (MFC_STREAM_2S=0: one compute stream).
+//           Every buffer plane is still written by one kernel and read after it:
+//           stage s of chunk k touches acc / its output only on chunk k's planes, and
+//           stage 3's in-place write of chunk k follows stage 2 of chunk k+1, which
+//           follows stage 1 of chunk k+2 (the last reader of chunk k's input).
 constexpr int kStageReach = 3;
 
 int copy_planes_h(const mfc_ctx* c, bool h2d, const double* host_in, double* host_out,
@@ -843,9 +852,35 @@ int rk3_stage_planes(mfc_ctx* c, double* q, int stage, double dt, int64_t za, in
 int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_dev, double dt,
                      int64_t cz, cudaStream_t s) {
     const int64_t nz = c->nl[2];
-    // balanced chunks of floor/ceil(nz/P) >= 3 planes (every chunk spans the stencil
-    // reach, so stage s of chunk k reads stage s-1 of chunks k-1, k, k+1 only)
-    const int P = (int)std::min<int64_t>((nz + cz - 1) / cz, nz / kStageReach);
+    // chunks of >= 3 planes (every chunk spans the stencil reach, so stage s of chunk k
+    // reads stage s-1 of chunks k-1, k, k+1 only): balanced floor/ceil(nz/P) planes, or
+    // (default, when nz allows) ramped -- 3, 4, 5, 6, 7 planes at both ends, cz in the
+    // middle -- so the first result leaves after a few thin pieces instead of six full
+    // ones and the last stages after the final piece are short (the D2H stream, busy
+    // from the first result to the end, is the critical path: r75 trace)
+    std::vector<int64_t> zb;   // chunk k = planes [zb[k], zb[k+1])
+    {
+        static const bool ramp_env = !(getenv("MFC_STREAM_RAMP") && atoi(getenv("MFC_STREAM_RAMP")) == 0);
+        std::vector<int64_t> head;
+        for (int64_t w = kStageReach; w < cz && head.size() < 5; ++w) head.push_back(w);
+        int64_t hsum = 0;
+        for (int64_t w : head) hsum += w;
+        const bool ramp = ramp_env && !head.empty() && nz - 2 * hsum >= 2 * cz;
+        zb.push_back(0);
+        if (ramp) {
+            for (int64_t w : head) zb.push_back(zb.back() + w);
+            const int64_t mid = nz - 2 * hsum, m = (mid + cz - 1) / cz;
+            const int64_t m0 = zb.back();
+            for (int64_t i = 1; i <= m; ++i) zb.push_back(m0 + i * mid / m);
+            for (auto it = head.rbegin(); it != head.rend(); ++it) zb.push_back(zb.back() + *it);
+        } else {
+            const int64_t Pu = std::min<int64_t>((nz + cz - 1) / cz, nz / kStageReach);
+            for (int64_t k = 1; k <= Pu; ++k) zb.push_back(k * nz / Pu);
+        }
+    }
+    const int P = (int)zb.size() - 1;
+    int64_t max_cz = 0;
+    for (int k = 0; k < P; ++k) max_cz = std::max<int64_t>(max_cz, zb[k + 1] - zb[k]);
     const bool per = c->bc[4] == MFC_BC_PERIODIC;
     auto mk = [](std::vector<cudaEvent_t>& v, int n) -> cudaError_t {
         while ((int)v.size() < n) {
@@ -859,11 +894,15 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
     CU_TRY(mk(c->ev_piece, P));
     CU_TRY(mk(c->ev_comp, P));
     CU_TRY(mk(c->ev_out, P));
+    CU_TRY(mk(c->ev_s1, P));
+    static const bool two = !(getenv("MFC_STREAM_2S") && atoi(getenv("MFC_STREAM_2S")) == 0);
+    if (two && !c->st_s1) CU_TRY(cudaStreamCreateWithFlags(&c->st_s1, cudaStreamNonBlocking));
+    cudaStream_t sa = two ? c->st_s1 : s;          // stage 1 + input scatters
     if (!c->ev_start) CU_TRY(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     if (!c->st_in) CU_TRY(cudaStreamCreateWithFlags(&c->st_in, cudaStreamNonBlocking));
     if (!c->st_out) CU_TRY(cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking));
-    auto z0 = [&](int k) { return k * nz / P; };
-    auto z1 = [&](int k) { return (k + 1) * nz / P; };
+    auto z0 = [&](int k) { return zb[k]; };
+    auto z1 = [&](int k) { return zb[k + 1]; };
     int st;
     static const bool tr = getenv("MFC_STREAM_TRACE") != nullptr;
     std::vector<std::pair<std::string, cudaEvent_t>> tr_ev;
@@ -877,12 +916,13 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
     CU_TRY(cudaEventRecord(c->ev_start, s));
     mark("start", s);
     CU_TRY(cudaStreamWaitEvent(c->st_in, c->ev_start, 0));
+    if (sa != s) CU_TRY(cudaStreamWaitEvent(sa, c->ev_start, 0));
     CU_TRY(cudaStreamWaitEvent(c->st_out, c->ev_start, 0));
     // Dense staging (c->stage_in / stage_out rings of kStageSlots pieces): the PCIe
     // copies are plain contiguous runs (E per piece) instead of 2 KB-row pitched
     // copies, which lost a quarter of the bidirectional bandwidth (r57 trace); a small
     // kernel scatters / gathers the padded planes on the compute stream.
-    const bool staged = c->stage_in && (nz + P - 1) / P <= c->stage_cz &&
+    const bool staged = c->stage_in && max_cz <= c->stage_cz &&
                         !getenv("MFC_STREAM_PITCHED");
     CU_TRY(mk(c->ev_scat, P));
     const int64_t plane_d = c->nl[0] * c->nl[1];
@@ -896,8 +936,9 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
         else CU_TRY(cudaMemcpy2DAsync(h, hp, dense, w, w, c->E, cudaMemcpyDeviceToHost, on));
         return MFC_OK;
     };
-    auto planes_kernel = [&](double* dense, int64_t za, int64_t n, bool to_dense) -> int {
-        dense_planes_kernel<<<grid_for(n * plane_d * c->E, 256), 256, 0, s>>>(
+    auto planes_kernel = [&](double* dense, int64_t za, int64_t n, bool to_dense,
+                             cudaStream_t on) -> int {
+        dense_planes_kernel<<<grid_for(n * plane_d * c->E, 256), 256, 0, on>>>(
             dense, q_dev, c->offset, c->stride[0], c->stride[1], c->stride[2], (int)c->nl[0],
             (int)c->nl[1], za, (int)n, c->E, to_dense);
         CU_TRY(cudaGetLastError());
@@ -934,15 +975,15 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
     // 2. the wavefront
     int scattered = 0;   // pieces scattered into q_dev, in upload order
     auto need_piece = [&](int j) -> int {
-        if (!staged) return cudaStreamWaitEvent(s, c->ev_piece[j], 0) == cudaSuccess
+        if (!staged) return cudaStreamWaitEvent(sa, c->ev_piece[j], 0) == cudaSuccess
                                 ? MFC_OK : fail(MFC_ECUDA, "stream wait");
         while (scattered <= rank_of[j]) {
             const int jj = order[scattered];
-            CU_TRY(cudaStreamWaitEvent(s, c->ev_piece[jj], 0));
+            CU_TRY(cudaStreamWaitEvent(sa, c->ev_piece[jj], 0));
             int r = planes_kernel(c->stage_in + (scattered % kStageSlots) * slot, z0(jj),
-                                  z1(jj) - z0(jj), false);
+                                  z1(jj) - z0(jj), false, sa);
             if (r) return r;
-            CU_TRY(cudaEventRecord(c->ev_scat[jj], s));
+            CU_TRY(cudaEventRecord(c->ev_scat[jj], sa));
             if (scattered + kStageSlots < P && (r = enqueue_h2d(scattered + kStageSlots))) return r;
             ++scattered;
         }
@@ -957,8 +998,16 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
                 if ((r = need_piece((m + P) % P))) return r;
             }
         }
-        if ((r = rk3_stage_planes(c, q_dev, sg, dt, z0(k), z1(k), s))) return r;
-        mark("s" + std::to_string(sg + 1) + "c" + std::to_string(k), s);
+        if (sg == 1 && sa != s) {   // stage 1 of the chunks within reach, on sa
+            for (int m = k - 1; m <= k + 1; ++m) {
+                if (!per && (m < 0 || m >= P)) continue;
+                CU_TRY(cudaStreamWaitEvent(s, c->ev_s1[(m + P) % P], 0));
+            }
+        }
+        cudaStream_t on = sg == 0 ? sa : s;
+        if ((r = rk3_stage_planes(c, q_dev, sg, dt, z0(k), z1(k), on))) return r;
+        if (sg == 0) CU_TRY(cudaEventRecord(c->ev_s1[k], sa));
+        mark("s" + std::to_string(sg + 1) + "c" + std::to_string(k), on);
         if (sg == 2) {
             double* dense = nullptr;
             if (staged) {
@@ -967,7 +1016,7 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
                 // slot o % R is free once the D2H of the chunk gathered R earlier is done
                 if (o >= kStageSlots) CU_TRY(cudaStreamWaitEvent(s, c->ev_out[gathered[o - kStageSlots]], 0));
                 gathered.push_back(k);
-                if ((r = planes_kernel(dense, z0(k), z1(k) - z0(k), true))) return r;
+                if ((r = planes_kernel(dense, z0(k), z1(k) - z0(k), true, s))) return r;
             }
             CU_TRY(cudaEventRecord(c->ev_comp[k], s));
             CU_TRY(cudaStreamWaitEvent(c->st_out, c->ev_comp[k], 0));
@@ -1718,8 +1767,10 @@ int mfc_finalize(mfc_ctx* c) {
     for (auto e : c->ev_out) cudaEventDestroy(e);
     for (auto e : c->ev_scat) cudaEventDestroy(e);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
+    for (auto e : c->ev_s1) cudaEventDestroy(e);
     if (c->st_in) cudaStreamDestroy(c->st_in);
     if (c->st_out) cudaStreamDestroy(c->st_out);
+    if (c->st_s1) cudaStreamDestroy(c->st_s1);
     delete c;
     return MFC_OK;
 }

@@ -603,7 +603,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     // resident warps per SM: 12 for the non-RK ring sweeps with E <= 8 (3 blocks), else 8
     // (8 for the 3D y/z marches, which run at 2 blocks/SM: sweep.cuh march_fewop; T = 128
     // there at 256^3, C3 y 2.114 -> 2.096 ms per step against T = 64, r63)
-    const bool fewop = dir >= 1 && c->D == 3 && (mode == M_ACC || mode == M_ACCN) && c->E <= 8;
+    const bool fewop = dir >= 1 && c->D >= 2 && (mode == M_ACC || mode == M_ACCN) && c->E <= 8;
     const bool three = c->E <= 8 && dir > 0 && (mode == M_ACC || mode == M_ACCN) && !fewop;
     a.T = seg_len(c, dir, three ? 12 : 8);
     a.s_lo = 0;

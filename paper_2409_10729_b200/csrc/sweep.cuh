@@ -148,13 +148,14 @@ struct SweepArgs {
 // prefetch distance 2 for all operands (mfc.cu launch_sweep_dir keeps the same test):
 // C3 y 2.177 -> 2.096, z 2.246 -> 2.189 ms per step (r62-r64, same box).  E = 10 (C5,
 // already 2 blocks/SM): the y march gains (20.8 -> 19.9 ms per step), the z march
-// loses (22.1 -> 23.2), r68.  The lean
+// loses (22.1 -> 23.2), r68.  The 2D y march (C2) likewise: 0.1053 -> 0.0978 ms per
+// step with both (r76).  The lean
 // weno5 at 3 blocks/SM (168 registers) is what the other marches run; weno5_fewop
 // spills there (+47%).
 template <class M, int DIR, int MODE>
 __host__ __device__ constexpr bool march_fewop() {
     return MFC_MARCH_FEWOP ||
-           (DIR >= 1 && M::D == 3 && (MODE == M_ACC || MODE == M_ACCN) &&
+           (DIR >= 1 && M::D >= 2 && (MODE == M_ACC || MODE == M_ACCN) &&
             (M::E <= MFC_FEWOP_EMAX || DIR == 1));
 }
 
@@ -276,10 +277,9 @@ sweep_kernel(const SweepArgs a) {
     // w[4] = e (the cell converted this step), so a step forms D2 = d-c, D3 = e-d only
     // (-2 FP64 per variable; bitwise the same differences), and the volume fractions
     // of cell j-1 (the alpha div(u) source) ride along in bA.
-    // (the 3D y/z marches, all at 2 blocks/SM: C5 z 22.3 -> 22.0 ms per step with the lean
-    // weno5 too, r70; at 168 registers the 2D/1D RHS marches spill with it, and C2's
-    // y march gains nothing)
-    constexpr bool DW = ORD == 5 && (MFC_DW_ALL || (M::D == 3 && DIR >= 1 &&
+    // (the 2D/3D y/z marches, all at 2 blocks/SM: C5 z 22.3 -> 22.0 ms per step with the
+    // lean weno5 too, r70; the 1D marches keep 168 registers, where it spills)
+    constexpr bool DW = ORD == 5 && (MFC_DW_ALL || (M::D >= 2 && DIR >= 1 &&
                                                     (MODE == M_ACC || MODE == M_ACCN)));
     double w[5][E];
     double bA[M::N];

@@ -231,6 +231,33 @@ __device__ __forceinline__ void weno5_fewop_d(double D0, double D1, double D2, d
     vp = fma(-Np, rcp(Dp), c);
 }
 
+// weno5_fewop with the curvature terms passed in: S_k = (13/3) s_k^2 + eps' formed by the
+// caller (fma(k133 s, s, eps')), beta'_k + eps' = r_k^2 + S_k.  A thread reconstructing two
+// neighbouring cells shares the s_k and S_k of the difference pairs both stencils
+// contain (sweep_x_pair); every cell's arithmetic is the same sequence whichever role
+// (first or second of a pair, or a segment-boundary cell) it has.
+__device__ __forceinline__ void weno5_fewop_s(double D0, double D1, double D2, double D3, double c,
+                                              double s0, double s1, double s2, double S0,
+                                              double S1, double S2, double& vm, double& vp) {
+    constexpr double k23 = 2.0 / 3.0;
+    const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
+    double t0 = fma(r0, r0, S0); t0 *= t0;
+    double t1 = fma(r1, r1, S1); t1 *= t1;
+    double t2 = fma(r2, r2, S2); t2 *= t2;
+    const double P0 = t1 * t2, P1 = t0 * t2, P2 = t0 * t1;
+    const double xm0 = fma(k23, s0, D1), xm1 = fma(3.0, r1, s1), xm2 = D2 - r2;
+    const double Dm = fma(12.0, P1, fma(6.0, P2, 2.0 * P0));
+    const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
+    vm = fma(Nm, rcp(Dm), c);
+    const double yp0 = r0 + D1, yp1 = fma(3.0, r1, -s1), yp2 = fma(-k23, s2, D2);   // = -X
+    const double Dp = fma(12.0, P1, fma(2.0, P2, 6.0 * P0));
+    const double Np = fma(P2, yp2, fma(P1, yp1, P0 * yp0));
+    vp = fma(-Np, rcp(Dp), c);
+}
+__device__ __forceinline__ double weno_S(double s, double eps4) {
+    return fma((13.0 / 3.0) * s, s, eps4);
+}
+
 __device__ __forceinline__ void weno5(double a, double b, double c, double d, double e,
                                       double eps4, double& vm, double& vp) {
     weno5_d(b - a, c - b, d - c, e - d, c, eps4, vm, vp);

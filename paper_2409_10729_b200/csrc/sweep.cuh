@@ -699,4 +699,183 @@ sweep_x_tile(const SweepArgs a, int W) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// x sweep, two cells per thread (sweep_x_pair; 2D/3D, WENO5, epilogue M_SET or the RK
+// stage base).  Same row-segment structure as sweep_x_tile, but thread t owns the two
+// neighbouring cells x0+2t and x0+2t+1: their stencils share four of five first
+// differences and three of four curvature terms S = (13/3) s^2 + eps' (weno5_fewop_s),
+// the face between them never leaves the registers, and only every other face and v-
+// go through shared memory.  Primitives sit in shared memory split by parity of the
+// tile index (Ve / Vo), so the stride-2 neighbour reads of a warp stay conflict-free.
+//   Ve/Vo [E][seg/2+3]: primitives of tile indices i (cell x0-3+i), i even / odd;
+//   VM2   [E][NT+1]   : v- of every thread's second cell (index t+1; index 0: cell x0-1);
+//   FS    [E+1][NT+1] : F, u^f of every thread's first face x0+2t-1/2 (aliases Ve/Vo;
+//                       index NT: face x0+seg-1/2).
+// A whole periodic row of even length wraps by index; otherwise 2E threads of the last
+// warp reconstruct the cells x0-1 (v-) and x0+seg (v+) with the same arithmetic
+// sequence as the main path, and one thread the face x0+seg-1/2 (AMB-22: bitwise the
+// same face whichever segment computes it).
+// ---------------------------------------------------------------------------
+// resident 128-thread blocks per SM: 5 for E <= 8 (96 registers, 12 B of spills; C3 x
+// 2.14 -> 2.05 ms per step against 4, r80), 4 for E = 10 (128 registers, no spills; 5
+// spills more and loses: C5 x 21.8 -> 25.1); 3 (168 registers) and 2 are slower.
+#ifndef MFC_XP_MINB
+#define MFC_XP_MINB 5
+#endif
+#ifndef MFC_XP_MINB_BIG
+#define MFC_XP_MINB_BIG 4
+#endif
+template <class M>
+__host__ __device__ constexpr int x_pair_minb() { return M::E <= 8 ? MFC_XP_MINB : MFC_XP_MINB_BIG; }
+template <class M>
+__host__ __device__ constexpr size_t x_pair_smem_doubles(int seg) {
+    const size_t nt = (size_t)seg / 2;
+    const size_t v = (size_t)2 * M::E * (nt + 3);
+    const size_t f = (size_t)(M::E + 1) * (nt + 1);
+    return (v > f ? v : f) + (size_t)M::E * (nt + 1) + M::E;
+}
+
+template <class M, bool RKB>
+__global__ void __launch_bounds__(128, x_pair_minb<M>())
+sweep_x_pair(const SweepArgs a, int W) {
+    constexpr int E = M::E;
+    const int t = threadIdx.x;
+    const int NT = 32 * W;
+    const int seg = 2 * NT;
+    const int x0 = blockIdx.x * seg;
+    const int n = a.nS;
+    const int x1 = min(x0 + seg, n);                 // cells x0 .. x1-1 are updated
+    const bool wrap = (a.gm.blo == 1 && a.gm.alo == n) && x0 == 0 && x1 == n && (n & 1) == 0;
+    const int tl = n / 2 - 1;                        // (wrap) thread owning the last cell
+    const int xa = x0 + 2 * t;                       // my cells xa, xa+1
+    const int64_t row = a.base + (int64_t)blockIdx.y * a.sA + (int64_t)blockIdx.z * a.sB;
+    const int LH = NT + 3, LP = NT + 1;
+    extern __shared__ double sm[];
+    double* const Ve = sm;                           // [E][LH]
+    double* const Vo = sm + (size_t)E * LH;          // [E][LH]
+    double* const FS = sm;                           // [E+1][LP] after phase 2
+    double* const VM2 = sm + x_pair_smem_doubles<M>(seg) - (size_t)E * LP - E;   // [E][LP]
+    double* const VPX = VM2 + (size_t)E * LP;        // [E]
+    auto V = [&](int e, int i) -> double& {
+        return (i & 1) ? Vo[e * LH + (i >> 1)] : Ve[e * LH + (i >> 1)];
+    };
+
+    auto load_prim = [&](int cell, double (&v)[E]) {
+        const int cl = min(cell, x1 + 2);            // beyond x1+2: unused
+        const double* p = a.q + row + map_cell(cl, n, a.gm);
+        double qc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) qc[e] = __ldg(p + e * a.sE);
+        if (map_flip(cl, n, a.gm)) qc[M::IM] = -qc[M::IM];
+        cons_to_prim_fast<M>(qc, v, a.mat);
+    };
+
+    // 1. primitives of my two cells (tile indices 2t+3, 2t+4) and of the six halo cells
+    double v0[E], v1[E];
+    load_prim(xa, v0);
+    load_prim(xa + 1, v1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        Vo[e * LH + t + 1] = v0[e];
+        Ve[e * LH + t + 2] = v1[e];
+    }
+    if (t < 6) {
+        double h[E];
+        load_prim(t < 3 ? x0 - 3 + t : x0 + seg + t - 3, h);
+        const int i = t < 3 ? t : seg + t;
+#pragma unroll
+        for (int e = 0; e < E; ++e) V(e, i) = h[e];
+    }
+    __syncthreads();
+
+    // 2. WENO of both cells: differences D_i = v_i - v_{i-1}, i = 2t+2 .. 2t+6
+    double vm0[E], vp0[E], vp1[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const double a1 = Vo[e * LH + t], a2 = Ve[e * LH + t + 1];
+        const double b5 = Vo[e * LH + t + 2], b6 = Ve[e * LH + t + 3];
+        const double D2 = a2 - a1, D3 = v0[e] - a2, D4 = v1[e] - v0[e], D5 = b5 - v1[e],
+                     D6 = b6 - b5;
+        const double s3 = D3 - D2, s4 = D4 - D3, s5 = D5 - D4, s6 = D6 - D5;
+        const double S3 = weno_S(s3, a.eps4), S4 = weno_S(s4, a.eps4), S5 = weno_S(s5, a.eps4),
+                     S6 = weno_S(s6, a.eps4);
+        double vm1;
+        weno5_fewop_s(D2, D3, D4, D5, v0[e], s3, s4, s5, S3, S4, S5, vm0[e], vp0[e]);
+        weno5_fewop_s(D3, D4, D5, D6, v1[e], s4, s5, s6, S4, S5, S6, vm1, vp1[e]);
+        VM2[e * LP + t + 1] = vm1;
+    }
+    if (!wrap) {
+        const int k = t - (NT - 32);                 // lanes 0 .. 2E-1 of the last warp
+        if (k >= 0 && k < 2 * E) {
+            const bool right = k >= E;
+            const int e = right ? k - E : k;
+            const int i0 = right ? seg + 1 : 0;      // stencil tile indices i0 .. i0+4
+            double r[5];
+#pragma unroll
+            for (int j = 0; j < 5; ++j) r[j] = V(e, i0 + j);
+            const double D0 = r[1] - r[0], D1 = r[2] - r[1], D2 = r[3] - r[2], D3 = r[4] - r[3];
+            const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
+            double bm, bp;
+            weno5_fewop_s(D0, D1, D2, D3, r[2], s0, s1, s2, weno_S(s0, a.eps4),
+                          weno_S(s1, a.eps4), weno_S(s2, a.eps4), bm, bp);
+            if (right) VPX[e] = bp;
+            else VM2[e * LP] = bm;
+        }
+    }
+    __syncthreads();
+
+    // 3. my faces xa-1/2 (v- of the cell before, from VM2) and xa+1/2 (both in registers)
+    double FA[E], ufA, FB[E], ufB;
+    {
+        const int li = (wrap && t == 0) ? tl + 1 : t;
+        double vL[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) vL[e] = VM2[e * LP + li];
+        hllc<M, 0>(vL, vp0, a.mat, FA, ufA);
+    }
+    hllc<M, 0>(vm0, vp1, a.mat, FB, ufB);
+#pragma unroll
+    for (int e = 0; e < E; ++e) FS[e * LP + t] = FA[e];
+    FS[E * LP + t] = ufA;
+    if (!wrap && x1 == x0 + seg && t == 0) {         // face x0+seg-1/2
+        double vl[E], vr[E], FE[E], ufE;
+#pragma unroll
+        for (int e = 0; e < E; ++e) { vl[e] = VM2[e * LP + NT]; vr[e] = VPX[e]; }
+        hllc<M, 0>(vl, vr, a.mat, FE, ufE);
+#pragma unroll
+        for (int e = 0; e < E; ++e) FS[e * LP + NT] = FE[e];
+        FS[E * LP + NT] = ufE;
+    }
+    __syncthreads();
+
+    // 4. updates: cell xa with (FA, FB), cell xa+1 with (FB, the next thread's FA)
+    const double wi = a.w * a.invd;
+    if (xa < x1) {
+        const double du = ufB - ufA;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            double r = FA[e] - FB[e];
+            if (e >= M::IA) r = fma(v0[e], du, r);
+            if constexpr (RKB)
+                a.dst[row + xa + e * a.sE] = fma(wi, r, a.cb * __ldg(a.q + row + xa + e * a.sE));
+            else
+                a.dst[row + xa + e * a.sE] = r * a.invd;
+        }
+    }
+    if (xa + 1 < x1) {
+        const int ri = (wrap && t == tl) ? 0 : t + 1;
+        const double du = FS[E * LP + ri] - ufB;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            double r = FB[e] - FS[e * LP + ri];
+            if (e >= M::IA) r = fma(v1[e], du, r);
+            if constexpr (RKB)
+                a.dst[row + xa + 1 + e * a.sE] =
+                    fma(wi, r, a.cb * __ldg(a.q + row + xa + 1 + e * a.sE));
+            else
+                a.dst[row + xa + 1 + e * a.sE] = r * a.invd;
+        }
+    }
+}
+
 }  // namespace mfc

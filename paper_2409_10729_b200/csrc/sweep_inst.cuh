@@ -90,7 +90,24 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
               // row-parallel tile kernel (rows longer than 256 cells: several 8-warp
               // segments with boundary cells); MFC_X_STAGED: the staged march.
               // The host asks x_rows_used() before choosing M_RKINIT (tile kernel only).
-              if (x_rows_used(a.nS)) {
+              static const bool xpair = !(getenv("MFC_XPAIR") && atoi(getenv("MFC_XPAIR")) == 0);
+              if (ORD == 5 && xpair && x_rows_used(a.nS)) {
+                // two cells per thread (sweep_x_pair): W <= 4 warps, 64 W cells per block
+                const int W = (int)std::min<int64_t>(4, (a.nS + 63) / 64);
+                const int nseg = (a.nS + 64 * W - 1) / (64 * W);
+                const size_t smem = sizeof(double) * x_pair_smem_doubles<M>(64 * W);
+                static size_t attr = 0;
+                if (smem > attr) {
+                    cudaFuncSetAttribute(sweep_x_pair<M, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    cudaFuncSetAttribute(sweep_x_pair<M, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    attr = smem;
+                }
+                const dim3 gr(nseg, a.nA, a.nB);
+                if (mode == M_SET) sweep_x_pair<M, false><<<gr, 32 * W, smem, s>>>(a, W);
+                else sweep_x_pair<M, true><<<gr, 32 * W, smem, s>>>(a, W);
+              } else if (x_rows_used(a.nS)) {
                 static const int wmax = getenv("MFC_XTILE_W") ? atoi(getenv("MFC_XTILE_W")) : 8;
                 const int W = (int)std::min<int64_t>(wmax, (a.nS + 31) / 32);
                 const int nseg = (a.nS + 32 * W - 1) / (32 * W);

@@ -36,6 +36,9 @@
 #ifndef MFC_MARCH_FEWOP
 #define MFC_MARCH_FEWOP false   // weno5_fewop in the ring marches (spills at 168 registers)
 #endif
+#ifndef MFC_MARCH_SC
+#define MFC_MARCH_SC false      // the curvature-term carry for E > 8 too (spills there)
+#endif
 #ifndef MFC_DW_ALL
 #define MFC_DW_ALL false        // experiment: the difference window in every WENO5 march
 #endif
@@ -281,8 +284,14 @@ sweep_kernel(const SweepArgs a) {
     // lean weno5 too, r70; the 1D marches keep 168 registers, where it spills)
     constexpr bool DW = ORD == 5 && (MFC_DW_ALL || (M::D >= 2 && DIR >= 1 &&
                                                     (MODE == M_ACC || MODE == M_ACCN)));
+    // SC: the difference marches also carry the curvature terms S = (13/3)s^2 + eps' of
+    // the difference pairs (D0,D1) and (D1,D2), formed one and two steps earlier, so a
+    // step forms the S of (D2,D3) only (weno5_fewop_s; bitwise the same S values)
+    // (E <= 8: C3 y 2.143 -> 2.085, z 2.232 -> 2.217 ms per step, r83; E = 10 spills 8 B)
+    constexpr bool SC = DW && (MFC_MARCH_SC || M::E <= 8) && march_fewop<M, DIR, MODE>();
     double w[5][E];
     double bA[M::N];
+    double Sc[2][SC ? E : 1];
     {
         double qc[E];
 #pragma unroll
@@ -305,6 +314,11 @@ sweep_kernel(const SweepArgs a) {
             for (int e = 0; e < E; ++e) {
                 w[0][e] = w[2][e] - w[1][e];
                 w[1][e] = w[3][e] - w[2][e];
+                if constexpr (SC) {
+                    const double D2 = w[4][e] - w[3][e];
+                    Sc[0][e] = weno_S(w[1][e] - w[0][e], a.eps4);
+                    Sc[1][e] = weno_S(D2 - w[1][e], a.eps4);
+                }
                 w[2][e] = w[3][e];
                 w[3][e] = w[4][e];
             }
@@ -349,7 +363,14 @@ sweep_kernel(const SweepArgs a) {
         for (int e = 0; e < E; ++e) {
             if constexpr (DW) {
                 const double D2 = w[3][e] - w[2][e], D3 = w[4][e] - w[3][e];
-                if constexpr (march_fewop<M, DIR, MODE>())
+                if constexpr (SC) {
+                    const double s0 = w[1][e] - w[0][e], s1 = D2 - w[1][e], s2 = D3 - D2;
+                    const double S2 = weno_S(s2, a.eps4);
+                    weno5_fewop_s(w[0][e], w[1][e], D2, D3, w[2][e], s0, s1, s2, Sc[0][e],
+                                  Sc[1][e], S2, vm[e], vp[e]);
+                    Sc[0][e] = Sc[1][e];
+                    Sc[1][e] = S2;
+                } else if constexpr (march_fewop<M, DIR, MODE>())
                     weno5_fewop_d(w[0][e], w[1][e], D2, D3, w[2][e], a.eps4, vm[e], vp[e]);
                 else
                     weno5_d(w[0][e], w[1][e], D2, D3, w[2][e], a.eps4, vm[e], vp[e]);

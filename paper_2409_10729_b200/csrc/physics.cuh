@@ -236,11 +236,13 @@ __device__ __forceinline__ void weno5_fewop_d(double D0, double D1, double D2, d
 // neighbouring cells shares the s_k and S_k of the difference pairs both stencils
 // contain (sweep_x_pair); every cell's arithmetic is the same sequence whichever role
 // (first or second of a pair, or a segment-boundary cell) it has.
-__device__ __forceinline__ void weno5_fewop_s(double D0, double D1, double D2, double D3, double c,
+// The caller also forms r0 = 3D1 - D0: the x pair as fma(3, D1, -D0), a march that
+// carries s0 instead of D0 as 2D1 + s0.
+__device__ __forceinline__ void weno5_fewop_s(double r0, double D1, double D2, double D3, double c,
                                               double s0, double s1, double s2, double S0,
                                               double S1, double S2, double& vm, double& vp) {
     constexpr double k23 = 2.0 / 3.0;
-    const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
+    const double r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
     double t0 = fma(r0, r0, S0); t0 *= t0;
     double t1 = fma(r1, r1, S1); t1 *= t1;
     double t2 = fma(r2, r2, S2); t2 *= t2;

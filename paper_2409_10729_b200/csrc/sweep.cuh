@@ -314,9 +314,10 @@ sweep_kernel(const SweepArgs a) {
             for (int e = 0; e < E; ++e) {
                 w[0][e] = w[2][e] - w[1][e];
                 w[1][e] = w[3][e] - w[2][e];
-                if constexpr (SC) {
+                if constexpr (SC) {       // w[0] carries s0 = D1 - D0 instead of D0
                     const double D2 = w[4][e] - w[3][e];
-                    Sc[0][e] = weno_S(w[1][e] - w[0][e], a.eps4);
+                    w[0][e] = w[1][e] - w[0][e];
+                    Sc[0][e] = weno_S(w[0][e], a.eps4);
                     Sc[1][e] = weno_S(D2 - w[1][e], a.eps4);
                 }
                 w[2][e] = w[3][e];
@@ -364,18 +365,19 @@ sweep_kernel(const SweepArgs a) {
             if constexpr (DW) {
                 const double D2 = w[3][e] - w[2][e], D3 = w[4][e] - w[3][e];
                 if constexpr (SC) {
-                    const double s0 = w[1][e] - w[0][e], s1 = D2 - w[1][e], s2 = D3 - D2;
+                    const double s1 = D2 - w[1][e], s2 = D3 - D2;
                     const double S2 = weno_S(s2, a.eps4);
-                    weno5_fewop_s(w[0][e], w[1][e], D2, D3, w[2][e], s0, s1, s2, Sc[0][e],
-                                  Sc[1][e], S2, vm[e], vp[e]);
+                    weno5_fewop_s(fma(2.0, w[1][e], w[0][e]), w[1][e], D2, D3, w[2][e], w[0][e],
+                                  s1, s2, Sc[0][e], Sc[1][e], S2, vm[e], vp[e]);
                     Sc[0][e] = Sc[1][e];
                     Sc[1][e] = S2;
+                    w[0][e] = s1;         // the next step's s0 (its w[1] = D2 below)
                 } else if constexpr (march_fewop<M, DIR, MODE>())
                     weno5_fewop_d(w[0][e], w[1][e], D2, D3, w[2][e], a.eps4, vm[e], vp[e]);
                 else
                     weno5_d(w[0][e], w[1][e], D2, D3, w[2][e], a.eps4, vm[e], vp[e]);
                 if (e >= M::IA) bAn[e - M::IA] = w[2][e];
-                w[0][e] = w[1][e];
+                if constexpr (!SC) w[0][e] = w[1][e];
                 w[1][e] = D2;
                 w[2][e] = w[3][e];
                 w[3][e] = w[4][e];
@@ -821,8 +823,9 @@ sweep_x_pair(const SweepArgs a, int W) {
         const double S3 = weno_S(s3, a.eps4), S4 = weno_S(s4, a.eps4), S5 = weno_S(s5, a.eps4),
                      S6 = weno_S(s6, a.eps4);
         double vm1;
-        weno5_fewop_s(D2, D3, D4, D5, v0[e], s3, s4, s5, S3, S4, S5, vm0[e], vp0[e]);
-        weno5_fewop_s(D3, D4, D5, D6, v1[e], s4, s5, s6, S4, S5, S6, vm1, vp1[e]);
+        weno5_fewop_s(fma(3.0, D3, -D2), D3, D4, D5, v0[e], s3, s4, s5, S3, S4, S5, vm0[e],
+                      vp0[e]);
+        weno5_fewop_s(fma(3.0, D4, -D3), D4, D5, D6, v1[e], s4, s5, s6, S4, S5, S6, vm1, vp1[e]);
         VM2[e * LP + t + 1] = vm1;
     }
     if (!wrap) {
@@ -837,7 +840,7 @@ sweep_x_pair(const SweepArgs a, int W) {
             const double D0 = r[1] - r[0], D1 = r[2] - r[1], D2 = r[3] - r[2], D3 = r[4] - r[3];
             const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
             double bm, bp;
-            weno5_fewop_s(D0, D1, D2, D3, r[2], s0, s1, s2, weno_S(s0, a.eps4),
+            weno5_fewop_s(fma(3.0, D1, -D0), D1, D2, D3, r[2], s0, s1, s2, weno_S(s0, a.eps4),
                           weno_S(s1, a.eps4), weno_S(s2, a.eps4), bm, bp);
             if (right) VPX[e] = bp;
             else VM2[e * LP] = bm;

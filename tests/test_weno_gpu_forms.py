@@ -6,7 +6,10 @@ forms that are not written the way the specification is:
     differences D0..D3;
   * `weno5_fewop_d`: every candidate correction ONE operation on the beta differences
     s_k, r_k (X = ((2/3)s0 + D1, 3r1 + s1, D2 - r2) for v-, -(r0 + D1, 3r1 - s1,
-    D2 - (2/3)s2) for v+) over the denominators 2P0 + 12P1 + 6P2 and 6P0 + 12P1 + 2P2.
+    D2 - (2/3)s2) for v+) over the denominators 2P0 + 12P1 + 6P2 and 6P0 + 12P1 + 2P2;
+  * `weno5_fewop_s`: the same with the curvature terms S_k = (13/3)s_k^2 + eps' formed
+    first (shared between neighbouring cells by the x pair and carried by the marches),
+    r0 either 3D1 - D0 or 2D1 + s0.
 Both are transcribed here operation by operation in numpy (fp64, same order; numpy
 does not contract a*b+c, so the products round separately -- the identity, not the
 rounding, is what this checks) and compared with the oracle's weno5_minus/plus
@@ -53,6 +56,29 @@ def weno5_fewop(a, b, c, d, e, eps):
     return c + Nm / Dm, c - Np / Dp
 
 
+def weno5_fewop_s(a, b, c, d, e, eps, r0_from_s0=False):
+    """`weno5_fewop_s` (x pair, marches): curvature terms S_k = (13/3)s_k^2 + eps' formed
+    first, t_k = (r_k^2 + S_k)^2; r0 = 3D1 - D0, or 2D1 + s0 in the marches that carry s0."""
+    D0, D1, D2, D3 = b - a, c - b, d - c, e - d
+    s0, s1, s2 = D1 - D0, D2 - D1, D3 - D2
+    S = [K133 * sk * sk + 4.0 * eps for sk in (s0, s1, s2)]
+    r0 = 2.0 * D1 + s0 if r0_from_s0 else 3.0 * D1 - D0
+    r1, r2 = D1 + D2, D3 - 3.0 * D2
+    t = [(rk * rk + Sk) ** 2 for rk, Sk in zip((r0, r1, r2), S)]
+    P0, P1, P2 = t[1] * t[2], t[0] * t[2], t[0] * t[1]
+    xm0, xm1, xm2 = K23 * s0 + D1, 3.0 * r1 + s1, D2 - r2
+    Dm = 12.0 * P1 + (6.0 * P2 + 2.0 * P0)
+    Nm = P2 * xm2 + (P1 * xm1 + P0 * xm0)
+    yp0, yp1, yp2 = r0 + D1, 3.0 * r1 - s1, -K23 * s2 + D2
+    Dp = 12.0 * P1 + (2.0 * P2 + 6.0 * P0)
+    Np = P2 * yp2 + (P1 * yp1 + P0 * yp0)
+    return c + Nm / Dm, c - Np / Dp
+
+
+def weno5_fewop_s_march(a, b, c, d, e, eps):
+    return weno5_fewop_s(a, b, c, d, e, eps, r0_from_s0=True)
+
+
 def _stencils(n=4000, seed=10729):
     rng = np.random.default_rng(seed)
     out = []
@@ -88,6 +114,12 @@ def test_lean_form_equals_specification():
 def test_fewop_form_equals_specification():
     for eps in (1e-16, 1e-6, 1e-40):
         _check(weno5_fewop, eps)
+
+
+def test_curvature_term_forms_equal_specification():
+    for eps in (1e-16, 1e-6, 1e-40):
+        _check(weno5_fewop_s, eps)
+        _check(weno5_fewop_s_march, eps)
 
 
 def test_fewop_candidate_identities():

@@ -10,7 +10,7 @@ forms that are not written the way the specification is:
   * `weno5_fewop_s`: the same with the curvature terms S_k = (13/3)s_k^2 + eps' formed
     first (shared between neighbouring cells by the x pair and carried by the marches),
     r0 either 3D1 - D0 or 2D1 + s0.
-Both are transcribed here operation by operation in numpy (fp64, same order; numpy
+All three are transcribed here operation by operation in numpy (fp64, same order; numpy
 does not contract a*b+c, so the products round separately -- the identity, not the
 rounding, is what this checks) and compared with the oracle's weno5_minus/plus
 (`oracle/mfc_oracle.c`, the plain alpha_k = d_k/(beta_k+eps)^2, omega = alpha/sum

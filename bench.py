@@ -224,6 +224,11 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
     red_dev = torch.device("cpu") if peer else dev
 
+    def variant(p):   # --weno: reconstruction of the solver's problem (F2 options)
+        p.weno_order = 3 if args.weno == "3" else 5
+        p.weno_mapped = args.weno == "5m"
+        return p
+
     n = args.n
     nid = mfc.broadcast_unique_id() if world > 1 and not peer else None
     procs = (1, 1, world)
@@ -235,7 +240,7 @@ def run_ours(args):
         else:
             pb = W.c3_droplet(n, nz=n * world)   # global domain: blocks stacked along z
             workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
-        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
+        s = mfc.Solver(variant(pb), procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
                        peer=peer)
         # every rank holds the same C3 block (its local prims), converted on the GPU
         q = s.state_from_prims(W.c3_prims(block))
@@ -244,7 +249,7 @@ def run_ours(args):
         nn = args.n if args.n != 256 else 512
         pb = W.c5_three_fluid(nn)                # strong scaling: fixed 512^3 split in z-slabs
         workload = f"C5 3D three-fluid shock-droplet {nn}^3 total, z-slabs x{world} (BASELINE configs[4])"
-        s = mfc.Solver(pb, procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
+        s = mfc.Solver(variant(pb), procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
                        peer=peer)
         L0 = s.layout
         v = s.empty_state()
@@ -259,7 +264,7 @@ def run_ours(args):
     else:                                        # C2, single GPU
         pb = W.c2_shock_bubble()
         workload = "C2 2D air-helium shock-bubble 1024x512 (BASELINE configs[1])"
-        s = mfc.Solver(pb, procs=(1, 1, 1), device=local)
+        s = mfc.Solver(variant(pb), procs=(1, 1, 1), device=local)
         q = s.state_from_prims(W.c2_prims(pb))
         dt = pb.dt
     if world > 1 and args.halo in ("fused", "peer"):
@@ -358,6 +363,8 @@ def run_ours(args):
                           f"inputs > L2: each state buffer {8 * L.n_elems / 1e9:.2f} GB >> 126 MB, no flush"),
                    "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
                    "halo": (args.halo if world > 1 else "none"),
+                   **({"weno": {"3": "WENO3-JS", "5m": "WENO5-M (mapped)"}[args.weno]}
+                      if args.weno != "5" else {}),
                    **({"same_device": "all ranks on GPU 0: protocol check, time-sliced, not a "
                                       "scaling number"} if args.same_device else {})},
         "hbm_gbs_step": hbm_step,
@@ -368,6 +375,9 @@ def run_ours(args):
                      "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "per_launch_ms": per_launch_ms,
                      "algorithmic_flops_per_cell": algorithmic_flops(dom, pb.n_fluids, pb.ndim),
+                     **({"flops_note": "algorithmic flops of the WENO5-JS path (DESIGN.md "
+                                       "§6.3); this run uses another reconstruction"}
+                        if args.weno != "5" else {}),
                      "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz "
                                     "(B200_PROFILING.md unit counts/clock; MEASURED_PEAKS.json "
                                     "has no FP64 entry; tools/fp64_peak.cu measured 34.1)",
@@ -430,6 +440,9 @@ def main():
     ap.add_argument("--same-device", action="store_true",
                     help="put every rank on GPU 0 (multi-process protocol check on one GPU; "
                          "its timings are time-sliced and not a scaling number)")
+    ap.add_argument("--weno", default="5", choices=["5", "3", "5m"],
+                    help="reconstruction: WENO5-JS (default, the named path), WENO3-JS or "
+                         "WENO5-M (SURVEY §8(f) F2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -138,6 +138,13 @@ int mfc_set_weno_eps(mfc_ctx* ctx, double eps);
  * The ghost depth stays 3; WENO3 reads the inner two layers. */
 int mfc_set_weno_order(mfc_ctx* ctx, int32_t order);
 
+/* on = 1: WENO5 with mapped nonlinear weights (WENO5-M: Henrick, Aslam & Powers, JCP 207
+ * (2005) 542, eq. (8); SURVEY §8(f) F2 "optionally, mapped WENO-M"): the Jiang-Shu
+ * omega_k are mapped by g_k(w) = w (d_k + d_k^2 - 3 d_k w + w^2)/(d_k^2 + w (1 - 2 d_k))
+ * and renormalised; same stencils, beta_k and eps.  on = 0 (default): WENO5-JS.  No
+ * effect with order 3.  EINVAL unless on is 0 or 1; a captured step graph is dropped. */
+int mfc_set_weno_mapped(mfc_ctx* ctx, int32_t on);
+
 /* Primitive <-> conserved conversion on the interior cells of padded device
  * buffers (same layout for v and q; may not alias).  prim_to_cons evaluates
  * rhoE = (Gamma p + Pi) + KE, cons_to_prim the inverse in the order of DESIGN.md

@@ -173,6 +173,34 @@ static double weno5_combine(const double beta[3], const double dk[3], const doub
     return (w[0] * p[0] + w[1] * p[1]) + w[2] * p[2];
 }
 
+/* WENO5-M (SURVEY §8(f) F2 "mapped WENO-M"; Henrick, Aslam & Powers 2005, eq. (8)):
+ * the Jiang-Shu weights ω_k = α_k/Σα (as above) are mapped by
+ *   g_k(ω) = ω (d_k + d_k² − 3 d_k ω + ω²) / (d_k² + ω (1 − 2 d_k))
+ * and renormalised, ω*_k = g_k(ω_k) / Σ_j g_j(ω_j); value = Σ ω*_k p_k. */
+static double weno5m_combine(const double beta[3], const double dk[3], const double p[3],
+                             double eps, double* weights) {
+    double alpha[3];
+    for (int k = 0; k < 3; ++k) {
+        const double s = beta[k] + eps;
+        alpha[k] = dk[k] / (s * s);
+    }
+    const double sum = (alpha[0] + alpha[1]) + alpha[2];
+    double g[3];
+    for (int k = 0; k < 3; ++k) {
+        const double w = alpha[k] / sum;
+        const double num = w * (((dk[k] + dk[k] * dk[k]) - 3.0 * dk[k] * w) + w * w);
+        const double den = dk[k] * dk[k] + w * (1.0 - 2.0 * dk[k]);
+        g[k] = num / den;
+    }
+    const double gsum = (g[0] + g[1]) + g[2];
+    double wm[3];
+    for (int k = 0; k < 3; ++k) wm[k] = g[k] / gsum;
+    if (weights) {
+        for (int k = 0; k < 3; ++k) weights[k] = wm[k];
+    }
+    return (wm[0] * p[0] + wm[1] * p[1]) + wm[2] * p[2];
+}
+
 /* v⁻_{m+½} from cell m's stencil a..e = v_{m−2..m+2}; linear weights
  * (0.1, 0.6, 0.3); p0 = (2a−7b+11c)/6, p1 = (−b+5c+2d)/6, p2 = (2c+5d−e)/6. */
 double orc_weno5_minus(double a, double b, double c, double d, double e, double eps,
@@ -199,6 +227,31 @@ double orc_weno5_plus(double a, double b, double c, double d, double e, double e
     p[1] = ((2.0 * b + 5.0 * c) - d) / 6.0;
     p[2] = ((11.0 * c - 7.0 * d) + 2.0 * e) / 6.0;
     return weno5_combine(beta, dk, p, eps, weights);
+}
+
+/* WENO5-M face states: the same candidates and β as orc_weno5_minus / _plus. */
+double orc_weno5m_minus(double a, double b, double c, double d, double e, double eps,
+                        double* weights) {
+    double beta[3];
+    weno5_beta(a, b, c, d, e, beta);
+    const double dk[3] = {0.1, 0.6, 0.3};
+    double p[3];
+    p[0] = ((2.0 * a - 7.0 * b) + 11.0 * c) / 6.0;
+    p[1] = ((-b + 5.0 * c) + 2.0 * d) / 6.0;
+    p[2] = ((2.0 * c + 5.0 * d) - e) / 6.0;
+    return weno5m_combine(beta, dk, p, eps, weights);
+}
+
+double orc_weno5m_plus(double a, double b, double c, double d, double e, double eps,
+                       double* weights) {
+    double beta[3];
+    weno5_beta(a, b, c, d, e, beta);
+    const double dk[3] = {0.3, 0.6, 0.1};
+    double p[3];
+    p[0] = ((-a + 5.0 * b) + 2.0 * c) / 6.0;
+    p[1] = ((2.0 * b + 5.0 * c) - d) / 6.0;
+    p[2] = ((11.0 * c - 7.0 * d) + 2.0 * e) / 6.0;
+    return weno5m_combine(beta, dk, p, eps, weights);
 }
 
 /* WENO3-JS: candidates from the 2-cell stencils {m-1,m} and {m,m+1},
@@ -330,6 +383,11 @@ static void face_flux(const orc_problem* P, const double* Gam, const double* Pi,
         if (P->weno_order == 3) {
             vL[e] = orc_weno3_minus(w[1 * E + e], w[2 * E + e], w[3 * E + e], P->eps, NULL);
             vR[e] = orc_weno3_plus(w[2 * E + e], w[3 * E + e], w[4 * E + e], P->eps, NULL);
+        } else if (P->weno_mapped) {
+            vL[e] = orc_weno5m_minus(w[0 * E + e], w[1 * E + e], w[2 * E + e], w[3 * E + e],
+                                     w[4 * E + e], P->eps, NULL);
+            vR[e] = orc_weno5m_plus(w[1 * E + e], w[2 * E + e], w[3 * E + e], w[4 * E + e],
+                                    w[5 * E + e], P->eps, NULL);
         } else {
             vL[e] = orc_weno5_minus(w[0 * E + e], w[1 * E + e], w[2 * E + e], w[3 * E + e],
                                     w[4 * E + e], P->eps, NULL);

@@ -44,6 +44,7 @@ typedef struct {
     double pi_inf[ORC_MAXF];    /* stiffened-gas pi_inf_i >= 0 */
     double eps;                 /* WENO epsilon (AMB-8), default 1e-16 */
     int32_t weno_order;         /* 5 (WENO5-JS, default) or 3 (WENO3-JS) */
+    int32_t weno_mapped;        /* 1: WENO5-M weights (Henrick et al. 2005) */
 } orc_problem;
 
 #ifdef __cplusplus
@@ -78,6 +79,13 @@ double orc_weno5_plus(double a, double b, double c, double d, double e, double e
 /* WENO3-JS ("third or fifth-order accurate WENO", Shu [15]) from a..c =
  * v_{m-1..m+1}: minus -> v^-_{m+1/2} (linear weights 1/3 on stencil {m-1,m},
  * 2/3 on {m,m+1}), plus -> v^+_{m-1/2} (2/3, 1/3); beta = squared differences. */
+/* WENO5-M (mapped weights, Henrick, Aslam & Powers, JCP 207 (2005) 542, eq. (8)):
+ * the Jiang-Shu omega_k mapped by g_k(w) = w (d_k + d_k^2 - 3 d_k w + w^2) /
+ * (d_k^2 + w (1 - 2 d_k)) and renormalised.  weights (optional) gets the mapped ones. */
+double orc_weno5m_minus(double a, double b, double c, double d, double e, double eps,
+                        double* weights);
+double orc_weno5m_plus(double a, double b, double c, double d, double e, double eps,
+                       double* weights);
 double orc_weno3_minus(double a, double b, double c, double eps, double* weights);
 double orc_weno3_plus(double a, double b, double c, double eps, double* weights);
 

@@ -19,7 +19,7 @@ import numpy as np
 
 __all__ = [
     "build", "lib", "Problem", "num_eq", "pad", "unpad", "constants", "cons_to_prim",
-    "prim_to_cons", "weno5_minus", "weno5_plus", "weno3_minus", "weno3_plus", "hllc", "fill_ghosts", "rhs",
+    "prim_to_cons", "weno5_minus", "weno5_plus", "weno5m_minus", "weno5m_plus", "weno3_minus", "weno3_plus", "hllc", "fill_ghosts", "rhs",
     "rhs_padded", "rhs_cells", "rk3_combine", "rk3_step", "count_inadmissible",
     "num_threads", "max_wave_rate", "BC_EXTERNAL", "BC_PERIODIC", "BC_REFLECTIVE", "BC_EXTRAPOLATION",
 ]
@@ -61,6 +61,7 @@ class _OrcProblem(ctypes.Structure):
         ("pi_inf", ctypes.c_double * MAXF),
         ("eps", ctypes.c_double),
         ("weno_order", ctypes.c_int32),
+        ("weno_mapped", ctypes.c_int32),
     ]
 
 
@@ -84,6 +85,8 @@ def lib():
                 "orc_prim_to_cons": (None, [P, ctypes.c_int64, _dp, _dp]),
                 "orc_weno5_minus": (ctypes.c_double, [ctypes.c_double] * 6 + [_dp]),
                 "orc_weno5_plus": (ctypes.c_double, [ctypes.c_double] * 6 + [_dp]),
+                "orc_weno5m_minus": (ctypes.c_double, [ctypes.c_double] * 6 + [_dp]),
+                "orc_weno5m_plus": (ctypes.c_double, [ctypes.c_double] * 6 + [_dp]),
                 "orc_weno3_minus": (ctypes.c_double, [ctypes.c_double] * 4 + [_dp]),
                 "orc_weno3_plus": (ctypes.c_double, [ctypes.c_double] * 4 + [_dp]),
                 "orc_hllc": (None, [P, _dp, _dp, ctypes.c_int32, _dp, _dp, _dp, _dp]),
@@ -117,6 +120,7 @@ class Problem:
     pi_inf: tuple
     eps: float = 1e-16
     weno_order: int = 5
+    weno_mapped: int = 0
     _c: _OrcProblem = field(default=None, repr=False, compare=False)
 
     @classmethod
@@ -126,7 +130,8 @@ class Problem:
                    bc=tuple(spec.bc if bc is None else bc), gamma=tuple(spec.gamma),
                    pi_inf=tuple(spec.pi_inf),
                    eps=float(getattr(spec, "weno_eps", 1e-16) if eps is None else eps),
-                   weno_order=int(getattr(spec, "weno_order", 5)))
+                   weno_order=int(getattr(spec, "weno_order", 5)),
+                   weno_mapped=int(bool(getattr(spec, "weno_mapped", False))))
 
     def __post_init__(self):
         n = list(self.n) + [1] * (3 - len(self.n))
@@ -145,6 +150,7 @@ class Problem:
             c.pi_inf[i] = float(self.pi_inf[i]) if i < self.N else 0.0
         c.eps = float(self.eps)
         c.weno_order = int(self.weno_order)
+        c.weno_mapped = int(self.weno_mapped)
         self._c = c
 
     @property
@@ -165,7 +171,7 @@ class Problem:
 
     def with_bc(self, bc):
         return Problem(self.N, self.d, self.n, self.dx, tuple(bc), self.gamma, self.pi_inf,
-                       self.eps, self.weno_order)
+                       self.eps, self.weno_order, self.weno_mapped)
 
 
 def num_eq(N: int, d: int) -> int:
@@ -225,6 +231,18 @@ def weno5_minus(a, b, c, d, e, eps=1e-16):
 def weno5_plus(a, b, c, d, e, eps=1e-16):
     w = np.zeros(3)
     val = lib().orc_weno5_plus(a, b, c, d, e, eps, _p(w))
+    return val, w
+
+
+def weno5m_minus(a, b, c, d, e, eps=1e-16):
+    w = np.zeros(3)
+    val = lib().orc_weno5m_minus(a, b, c, d, e, eps, _p(w))
+    return val, w
+
+
+def weno5m_plus(a, b, c, d, e, eps=1e-16):
+    w = np.zeros(3)
+    val = lib().orc_weno5m_plus(a, b, c, d, e, eps, _p(w))
     return val, w
 
 

@@ -82,6 +82,7 @@ struct mfc_ctx {
     Materials mat{};
     double eps = 1e-16;
     int weno_order = 5;
+    int weno_mapped = 0;           // WENO5-M weights (mfc_set_weno_mapped)
     int rank = 0, nranks = 1, procs[3] = {1, 1, 1}, coords[3] = {0, 0, 0};
     bool loopback = false;
     ncclComm_t comm = nullptr;
@@ -649,10 +650,12 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.s_hi - a.s_lo + a.T - 1) / a.T);
     cudaError_t e;
     ProfScope ps(c, s, K_SWEEP_X + dir);
+    // kernel template order: 3, 5, or 6 = WENO5 with mapped weights
+    const int ord = (c->weno_order == 5 && c->weno_mapped) ? 6 : c->weno_order;
     switch (c->N) {
-        case 1: e = launch_sweep<1>(c->D, dir, mode, c->weno_order, a, grid, block, s); break;
-        case 2: e = launch_sweep<2>(c->D, dir, mode, c->weno_order, a, grid, block, s); break;
-        case 3: e = launch_sweep<3>(c->D, dir, mode, c->weno_order, a, grid, block, s); break;
+        case 1: e = launch_sweep<1>(c->D, dir, mode, ord, a, grid, block, s); break;
+        case 2: e = launch_sweep<2>(c->D, dir, mode, ord, a, grid, block, s); break;
+        case 3: e = launch_sweep<3>(c->D, dir, mode, ord, a, grid, block, s); break;
         default: return fail(MFC_EINVAL, "bad N");
     }
     if (e != cudaSuccess) return fail(MFC_ECUDA, "sweep launch: %s", cudaGetErrorString(e));
@@ -1368,6 +1371,17 @@ int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
             c->sendb[f] = (double*)w; w += fb;
             c->recvb[f] = (double*)w; w += fb;
         }
+    }
+    return MFC_OK;
+}
+
+int mfc_set_weno_mapped(mfc_ctx* c, int32_t on) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (on != 0 && on != 1) return fail(MFC_EINVAL, "mapped must be 0 or 1");
+    c->weno_mapped = on;
+    if (c->graph) {                  // captured kernels depend on the weights
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
     }
     return MFC_OK;
 }

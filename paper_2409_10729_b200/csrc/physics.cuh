@@ -269,6 +269,46 @@ __device__ __forceinline__ void weno5_fewop(double a, double b, double c, double
     weno5_fewop_d(b - a, c - b, d - c, e - d, c, eps4, vm, vp);
 }
 
+// WENO5-M (Henrick, Aslam & Powers, JCP 207 (2005) 542): the Jiang-Shu
+// weights omega_k = d_k P_k / sum_j d_j P_j (P_k as in weno5) mapped by
+//   g_k(w) = w (d_k + d_k^2 - 3 d_k w + w^2) / (d_k^2 + w (1 - 2 d_k))
+// and renormalised, multiplied through by the three denominators:
+//   omega*_k ~ Q_k = num_k den_i den_j,  v = c + (sum_k Q_k A_k/6) / sum_k Q_k,
+// A_k = 6 (p_k - c) the candidate corrections (as in weno5): two reciprocals per side.
+__device__ __forceinline__ void weno5m_side(const double (&P)[3], const double (&A)[3],
+                                            const double (&d)[3], double c, double& v) {
+    const double W = rcp(fma(d[2], P[2], fma(d[1], P[1], d[0] * P[0])));
+    double num[3], den[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double w = d[k] * P[k] * W;
+        num[k] = w * fma(w, w - 3.0 * d[k], fma(d[k], d[k], d[k]));
+        den[k] = fma(w, 1.0 - 2.0 * d[k], d[k] * d[k]);
+    }
+    const double Q0 = num[0] * (den[1] * den[2]);
+    const double Q1 = num[1] * (den[0] * den[2]);
+    const double Q2 = num[2] * (den[0] * den[1]);
+    const double N = fma(Q2, A[2], fma(Q1, A[1], Q0 * A[0]));
+    v = fma(N * (1.0 / 6.0), rcp((Q0 + Q1) + Q2), c);
+}
+
+__device__ __forceinline__ void weno5m(double a, double b, double c, double d, double e,
+                                       double eps4, double& vm, double& vp) {
+    constexpr double k133 = 13.0 / 3.0;
+    const double D0 = b - a, D1 = c - b, D2 = d - c, D3 = e - d;
+    const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
+    const double r0 = fma(3.0, D1, -D0), r1 = D1 + D2, r2 = fma(-3.0, D2, D3);
+    double t0 = fma(k133 * s0, s0, fma(r0, r0, eps4)); t0 *= t0;
+    double t1 = fma(k133 * s1, s1, fma(r1, r1, eps4)); t1 *= t1;
+    double t2 = fma(k133 * s2, s2, fma(r2, r2, eps4)); t2 *= t2;
+    const double P[3] = {t1 * t2, t0 * t2, t0 * t1};
+    const double Am[3] = {fma(5.0, D1, -2.0 * D0), fma(2.0, D2, D1), fma(4.0, D2, -D3)};
+    const double Ap[3] = {fma(-4.0, D1, D0), fma(-2.0, D1, -D2), fma(2.0, D3, -5.0 * D2)};
+    const double dm[3] = {0.1, 0.6, 0.3}, dp[3] = {0.3, 0.6, 0.1};
+    weno5m_side(P, Am, dm, c, vm);
+    weno5m_side(P, Ap, dp, c, vp);
+}
+
 // WENO3-JS ("third or fifth-order"; F2) for one variable of cell m from
 // a..c = v_{m-1..m+1}, in first differences D0 = b-a, D1 = c-b:
 //   beta = (D0^2, D1^2), alpha_k ~ d_k/(beta_k+eps)^2 multiplied through by t0 t1,

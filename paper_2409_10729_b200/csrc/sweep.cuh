@@ -54,13 +54,14 @@ namespace mfc {
 enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3, M_ACCN = 4 };
 
 // Reconstruction of one variable of the window's centre cell (ORD = 5: cells w0..w4,
-// ORD = 3: the inner three).
+// ORD = 6: the same with WENO5-M weights, ORD = 3: the inner three).
 // FEWOP: the WENO5 form with fewer FP64 operations but longer-lived temporaries
 // (x tile only, see weno5_fewop).
 template <int ORD, bool FEWOP = false>
 __device__ __forceinline__ void reconstruct(double w0, double w1, double w2, double w3, double w4,
                                             double eps4, double eps, double& vm, double& vp) {
-    if constexpr (ORD == 5 && FEWOP) weno5_fewop(w0, w1, w2, w3, w4, eps4, vm, vp);
+    if constexpr (ORD == 6) weno5m(w0, w1, w2, w3, w4, eps4, vm, vp);   // WENO5-M
+    else if constexpr (ORD == 5 && FEWOP) weno5_fewop(w0, w1, w2, w3, w4, eps4, vm, vp);
     else if constexpr (ORD == 5) weno5(w0, w1, w2, w3, w4, eps4, vm, vp);
     else weno3(w1, w2, w3, eps, vm, vp);
 }

@@ -204,6 +204,7 @@ template <>
 cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int mode, int order, const SweepArgs& a, dim3 g,
                                  dim3 b, cudaStream_t s) {
     if (order == 3) return launch_order<3>(D, DIR, mode, a, g, b, s);
+    if (order == 6) return launch_order<6>(D, DIR, mode, a, g, b, s);   // WENO5-M
     return launch_order<5>(D, DIR, mode, a, g, b, s);
 }
 

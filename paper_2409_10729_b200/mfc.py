@@ -30,7 +30,7 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ES
 
 EXPORTED = [
     "mfc_init", "mfc_get_layout", "mfc_get_neighbors", "mfc_bind_workspace", "mfc_set_weno_eps",
-    "mfc_set_weno_order",
+    "mfc_set_weno_order", "mfc_set_weno_mapped",
     "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
     "mfc_rk3_steps", "mfc_max_wave_rate", "mfc_cfl_dt",
     "mfc_advance_host", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
@@ -78,6 +78,7 @@ def _load():
         "mfc_bind_workspace": [vp, vp, ctypes.c_size_t],
         "mfc_set_weno_eps": [vp, dbl],
         "mfc_set_weno_order": [vp, i32],
+        "mfc_set_weno_mapped": [vp, i32],
         "mfc_prim_to_cons": [vp, vp, vp, vp],
         "mfc_cons_to_prim": [vp, vp, vp, vp],
         "mfc_halo_exchange": [vp, vp, vp],
@@ -210,6 +211,8 @@ class Solver:
         _check(lib.mfc_set_weno_eps(h, float(eps)), "mfc_set_weno_eps")
         _check(lib.mfc_set_weno_order(h, int(getattr(problem, "weno_order", 5))),
                "mfc_set_weno_order")
+        _check(lib.mfc_set_weno_mapped(h, int(bool(getattr(problem, "weno_mapped", False)))),
+               "mfc_set_weno_mapped")
         # torch owns the workspace (256-byte aligned by the caching allocator)
         nbytes = self.layout.workspace_bytes
         self.workspace = torch.empty((nbytes + 7) // 8, dtype=torch.float64, device=self.device)

@@ -59,6 +59,7 @@ class Problem:
     steps: int = 0                # steps the config names (C1: 200)
     weno_eps: float = 1e-16
     weno_order: int = 5           # 5 (default) or 3
+    weno_mapped: bool = False     # WENO5-M weights (Henrick et al. 2005)
     notes: dict = field(default_factory=dict)
 
     @property

@@ -218,3 +218,53 @@ def test_weno3_100_steps_parity():
     tol = np.maximum(STEP100_TOL, 3.0 * oracle_sensitivity(P, q, pb.dt, 100, ref))
     record("100 RK3 steps C3-24 WENO3", err, tol)
     assert np.all(err <= tol), err
+
+
+def _mapped(pb):
+    pb.weno_mapped = True
+    return pb
+
+
+WENO5M_CASES = [
+    ("C1-m", lambda: _mapped(W.c1_water_air())),
+    ("C2-96x48-m", lambda: _mapped(W.c2_shock_bubble(96, 48))),
+    ("C3-32-m", lambda: _mapped(W.c3_droplet(32))),
+    ("GR-2D-N3-m", lambda: _mapped(W.random_problem(2, (45, 38), 3, "water"))),
+    ("GR-3D-N2-m", lambda: _mapped(W.random_problem(3, (35, 22, 27), 2, "gas"))),
+    ("GR-3D-N3-refl-m", lambda: _mapped(W.random_problem(3, (20, 21, 22), 3, "water",
+                                                         bc=(-2, -3, -1, -1, -3, -2)))),
+]
+
+
+@pytest.mark.parametrize("name,make", WENO5M_CASES, ids=[c[0] for c in WENO5M_CASES])
+def test_weno5m_rhs_parity(name, make):
+    """F2 (optional WENO-M): mapped weights through the same sweeps, against the oracle's
+    orc_weno5m (pinned in tests/test_oracle_weno_mapped.py)."""
+    _rhs_case(make())
+
+
+def test_weno5m_100_steps_parity():
+    pb = _mapped(W.c3_droplet(24))
+    P, v, q = oracle_inputs(pb)
+    assert P.weno_mapped == 1
+    ref = O.rk3_step(P, q, pb.dt, nsteps=100)
+    got = gpu_steps(pb, q, pb.dt, 100)
+    err = rel_err(got, ref)
+    tol = np.maximum(STEP100_TOL, 3.0 * oracle_sensitivity(P, q, pb.dt, 100, ref))
+    record("100 RK3 steps C3-24 WENO5-M", err, tol)
+    assert np.all(err <= tol), err
+
+
+def test_weno5m_differs_from_js():
+    """The mapped weights are actually used: the RHS moves away from WENO5-JS's by far more
+    than the parity tolerance on a discontinuous field."""
+    import dataclasses
+    pb = W.c3_droplet(24)
+    P, v, q = oracle_inputs(pb)
+    js = gpu_solver(pb)
+    pbm = _mapped(dataclasses.replace(pb))
+    m = gpu_solver(pbm)
+    a = js.interior(js.rhs(js.state_from_cons(q))).cpu().numpy()
+    b = m.interior(m.rhs(m.state_from_cons(q))).cpu().numpy()
+    scale = np.abs(a).max(axis=(1, 2, 3))
+    assert (np.abs(a - b).max(axis=(1, 2, 3)) / scale).max() > 1e-6

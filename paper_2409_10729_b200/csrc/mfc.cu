@@ -691,9 +691,14 @@ int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const
         // last one w*c + ca*q^n (M_ACCN, stages 2-3); with the staged x sweep, x writes
         // c_x and the y sweep assembles the base (M_RKACC)
         const bool xb = rk && c->D >= 2 && c->xbase && x_rows_used((int)c->nl[0]);
+        // 3D, E <= 8: the x sweep also adds ca*q^n, and the z sweep is a plain accumulate
+        // (M_ACC) in every stage: C3 x +0.10, z -0.15 ms per step (r89, three same-box
+        // repetitions); E = 10 loses (C5 x +1.37, z -0.84).  MFC_XBASE_N=0/1 forces it.
+        static const int xbn_env = getenv("MFC_XBASE_N") ? atoi(getenv("MFC_XBASE_N")) : -1;
+        const bool xbn = xb && (xbn_env < 0 ? (c->D == 3 && c->E <= 8) : xbn_env != 0);
         int mode;
         if (dir == 0) mode = (rk && (c->D == 1 || xb)) ? M_RKINIT : M_SET;
-        else if (xb) mode = (last && ca != 0.0) ? M_ACCN : M_ACC;
+        else if (xb) mode = (last && ca != 0.0 && !xbn) ? M_ACCN : M_ACC;
         else if (dir == 1 && rk) mode = M_RKACC;
         else mode = M_ACC;
         // M_SET in an RK stage writes the unscaled c_x; M_RKACC scales (acc + c_y) by w
@@ -703,7 +708,9 @@ int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const
         if (last && peer_buf >= 0)
             for (int f = 0; f < 2 * c->D; ++f)
                 if (c->bc[f] == BC_NEIGHBOR) po.f[po.nf++] = c->pf[f][peer_buf];
-        int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn, wd, ca, cb, s, &po);
+        // the x sweep gets q^n only when it adds ca*q^n (its kernels test qn != nullptr)
+        const double* qn_d = (dir == 0 && xb && !xbn) ? nullptr : qn;
+        int st = launch_sweep_dir(c, dir, mode, q, acc, out, qn_d, wd, ca, cb, s, &po);
         if (st) return st;
     }
     return MFC_OK;

@@ -609,6 +609,13 @@ namespace mfc {
 template <class M>
 __host__ __device__ constexpr int x_tile_minb() { return M::E <= 8 ? MFC_XT_MINB : MFC_XT_MINB_BIG; }
 
+// RK stage base of the x sweeps (RKB): cb*q^s, plus ca*q^n when the host hands q^n over
+// (MFC_XBASE_N; otherwise the last sweep adds it, M_ACCN)
+__device__ __forceinline__ double xbase(const SweepArgs& a, int64_t i) {
+    const double b = a.cb * __ldg(a.q + i);
+    return (a.qn != nullptr && a.ca != 0.0) ? fma(a.ca, __ldg(a.qn + i), b) : b;
+}
+
 template <class M>
 __host__ __device__ constexpr size_t x_tile_smem_doubles(int seg) {
     return (size_t)((M::E * (seg + 6) > (M::E + 1) * (seg + 1)) ? M::E * (seg + 6)
@@ -716,7 +723,7 @@ sweep_x_tile(const SweepArgs a, int W) {
             double r = F[e] - FS[e * LF + ri];
             if (e >= M::IA) r = fma(v[e], du, r);
             if constexpr (RKB)
-                a.dst[row + x + e * a.sE] = fma(wi, r, a.cb * __ldg(a.q + row + x + e * a.sE));
+                a.dst[row + x + e * a.sE] = fma(wi, r, xbase(a, row + x + e * a.sE));
             else
                 a.dst[row + x + e * a.sE] = r * a.invd;
         }
@@ -882,7 +889,7 @@ sweep_x_pair(const SweepArgs a, int W) {
             double r = FA[e] - FB[e];
             if (e >= M::IA) r = fma(v0[e], du, r);
             if constexpr (RKB)
-                a.dst[row + xa + e * a.sE] = fma(wi, r, a.cb * __ldg(a.q + row + xa + e * a.sE));
+                a.dst[row + xa + e * a.sE] = fma(wi, r, xbase(a, row + xa + e * a.sE));
             else
                 a.dst[row + xa + e * a.sE] = r * a.invd;
         }
@@ -895,8 +902,7 @@ sweep_x_pair(const SweepArgs a, int W) {
             double r = FB[e] - FS[e * LP + ri];
             if (e >= M::IA) r = fma(v1[e], du, r);
             if constexpr (RKB)
-                a.dst[row + xa + 1 + e * a.sE] =
-                    fma(wi, r, a.cb * __ldg(a.q + row + xa + 1 + e * a.sE));
+                a.dst[row + xa + 1 + e * a.sE] = fma(wi, r, xbase(a, row + xa + 1 + e * a.sE));
             else
                 a.dst[row + xa + 1 + e * a.sE] = r * a.invd;
         }

@@ -124,7 +124,7 @@ def test_decomposition_bookkeeping(mfc, procs, periodic):
 
 
 def test_new_entry_points_validate_arguments(mfc):
-    """mfc_set_weno_order / mfc_set_weno_eps / mfc_cfl_dt / mfc_rk3_steps reject bad
+    """mfc_set_weno_order / _mapped / _eps / mfc_cfl_dt / mfc_rk3_steps reject bad
     arguments before touching the GPU."""
     pb = W.random_problem(3, (8, 8, 8), 2, "gas")
     g = mfc._Grid()
@@ -142,6 +142,10 @@ def test_new_entry_points_validate_arguments(mfc):
         assert mfc.lib.mfc_set_weno_order(h, 4) == -1
         assert mfc.lib.mfc_set_weno_order(h, 3) == 0
         assert mfc.lib.mfc_set_weno_order(h, 5) == 0
+        assert mfc.lib.mfc_set_weno_mapped(h, 2) == -1
+        assert mfc.lib.mfc_set_weno_mapped(h, 1) == 0
+        assert mfc.lib.mfc_set_weno_mapped(h, 0) == 0
+        assert mfc.lib.mfc_set_weno_mapped(None, 1) == -1
         assert mfc.lib.mfc_set_weno_eps(h, 0.5) == -1
         assert mfc.lib.mfc_set_weno_eps(h, 1e-16) == 0
         dt = ctypes.c_double(0.0)

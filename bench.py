@@ -174,18 +174,20 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- ours
-def algorithmic_bytes(kind: str, E: int) -> float:
+def algorithmic_bytes(kind: str, E: int, qn_in_x: bool = True) -> float:
     """Algorithmic HBM bytes per interior cell for one launch of each sweep kind in an
-    RK3 step (DESIGN.md §6.3; 3D, row-parallel x sweep): x: read q^s (the stencil state;
-    its re-read for the RK base cb*q^s is the same cell, counted once), write acc (16E);
-    y: read q^s, acc, write acc (24E); z: read q^s, acc, q^n (stages 2, 3 only), write
-    the stage result (24E + 8E*2/3)."""
+    RK3 step, averaged over the three stages (3D, row-parallel x sweep):
+    x: read q^s (the stencil state; its re-read for the RK base cb*q^s is the same cell,
+    counted once), write acc (16E), plus q^n in stages 2 and 3 when x adds ca*q^n
+    (3D, E <= 8: qn_in_x); y: read q^s, acc, write acc (24E); z: read q^s, acc, write the
+    stage result (24E), plus q^n in stages 2 and 3 otherwise."""
+    qn = 8.0 * E * 2.0 / 3.0
     if kind == "sweep_x":
-        return 16.0 * E
+        return 16.0 * E + (qn if qn_in_x else 0.0)
     if kind == "sweep_y":
         return 24.0 * E
     if kind == "sweep_z":
-        return 24.0 * E + 8.0 * E * 2.0 / 3.0
+        return 24.0 * E + (0.0 if qn_in_x else qn)
     return 0.0
 
 
@@ -336,7 +338,8 @@ def run_ours(args):
     per_launch_ms = dom_ms / max(dom_n, 1)
     flops = algorithmic_flops(dom, pb.n_fluids, pb.ndim) * cells_local
     achieved_tf = flops / (per_launch_ms * 1e-3) / 1e12
-    alg_bytes = algorithmic_bytes(dom, E) * cells_local
+    qn_in_x = pb.ndim == 3 and E <= 8 and os.environ.get("MFC_XBASE_N", "") != "0"
+    alg_bytes = algorithmic_bytes(dom, E, qn_in_x) * cells_local
     achieved_gbs = alg_bytes / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     try:   # DRAM bytes of this kernel from the last committed ncu --set full capture
@@ -383,7 +386,7 @@ def run_ours(args):
                                     "has no FP64 entry; tools/fp64_peak.cu measured 34.1)",
                      "hbm_view": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                                   "frac": achieved_gbs / hbm_peak,
-                                  "algorithmic_bytes_per_cell": algorithmic_bytes(dom, E),
+                                  "algorithmic_bytes_per_cell": algorithmic_bytes(dom, E, qn_in_x),
                                   "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}},
         "clocks": clocks,
         "gpu_launches": launches,

@@ -93,7 +93,9 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
               static const bool xpair = !(getenv("MFC_XPAIR") && atoi(getenv("MFC_XPAIR")) == 0);
               if (ORD == 5 && xpair && x_rows_used(a.nS)) {
                 // two cells per thread (sweep_x_pair): W <= 4 warps, 64 W cells per block
-                const int W = (int)std::min<int64_t>(4, (a.nS + 63) / 64);
+                // (MFC_XPAIR_W=2: 128-cell segments, C3 x 2.15 -> 2.28 ms per step, r93)
+                static const int wmaxp = getenv("MFC_XPAIR_W") ? atoi(getenv("MFC_XPAIR_W")) : 4;
+                const int W = (int)std::min<int64_t>(wmaxp, (a.nS + 63) / 64);
                 const int nseg = (a.nS + 64 * W - 1) / (64 * W);
                 const size_t smem = sizeof(double) * x_pair_smem_doubles<M>(64 * W);
                 static size_t attr = 0;

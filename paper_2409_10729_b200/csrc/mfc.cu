@@ -217,18 +217,6 @@ __global__ void halo_pack_kernel(const double* q, double* buf, FaceGeom g, int d
     }
 }
 
-// dst[e*dE + i] = src[e*sE + i] for i < n (16-byte vectors; n, offsets even): the
-// streamed step's chunk copies on the SMs, off the copy engines that carry PCIe traffic
-__global__ void copy_planes_kernel(double* dst, int64_t dE, const double* src, int64_t sE,
-                                   int64_t n2, int E) {
-    const int64_t tot = n2 * E;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e = t / n2, i = t - e * n2;
-        reinterpret_cast<double2*>(dst + e * dE)[i] = reinterpret_cast<const double2*>(src + e * sE)[i];
-    }
-}
-
 // Dense <-> padded planes: dense[e][z][y][x] (nz planes) <-> padded interior planes
 // z0 .. z0+nz of a state with strides sE, sZ, sY (x unit stride), base = interior offset.
 __global__ void dense_planes_kernel(double* dense, double* padded, int64_t base, int64_t sE,

@@ -15,6 +15,10 @@
 #pragma once
 #include <cstdint>
 
+#ifndef MFC_HLLC_ONE_RCP
+#define MFC_HLLC_ONE_RCP 1   // r96: x -0.015, y -0.01 ms per step (same box, 3 repetitions)
+#endif
+
 namespace mfc {
 
 constexpr int kGhost = 3;
@@ -353,9 +357,20 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     const double aL = rL * (sL - uL), aR = rR * (sR - uR);
     // (every multiply-add is an explicit fma: contraction must not depend on the
     //  inlining site, so a face computed by two code paths is bitwise identical)
+#if MFC_HLLC_ONE_RCP
+    // s_S = num/den with den = aL - aR < 0 (aL < 0 < aR for positive densities and sound
+    // speeds), so s_S >= 0  <=>  num <= 0: the side is chosen before any division, and
+    // ONE reciprocal R = 1/(den dK D2), D2 = den dS = sK den - num, serves s_S = num dK D2 R,
+    // 1/(dK dS) = den^2 R and p_K/(s_K-u_K) = p_K D2 den R (one MUFU round trip fewer on
+    // the face's dependency chain)
+    const double num = fma(-aR, uR, fma(aL, uL, pR - pL));
+    const double den = aL - aR;
+    const bool left = num <= 0.0;
+#else
     const double sS = fma(-aR, uR, fma(aL, uL, pR - pL)) * rcp(aL - aR);
 
     const bool left = sS >= 0.0;
+#endif
     const double sK = left ? sL : sR;
     const double sstar = left ? fmin(0.0, sL) : fmax(0.0, sR);
     const double rK = left ? rL : rR;
@@ -371,8 +386,17 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     for (int k = 0; k < M::D; ++k) uu = fma(vK[M::IM + k], vK[M::IM + k], uu);
     const double EK = fma(0.5, rK * uu, fma(GK, pK, PK));
     const double dK = sK - uK;
+#if MFC_HLLC_ONE_RCP
+    const double D2 = fma(sK, den, -num);
+    const double R = rcp((den * dK) * D2);
+    const double sS = num * ((dK * D2) * R);
+    const double rr = (den * den) * R;       // 1/(dK dS)
+    const double pdK = pK * ((D2 * den) * R);   // p_K/(s_K-u_K)
+#else
     const double dS = sK - sS;
     const double rr = rcp(dK * dS);          // one reciprocal for xi and p_K/(s_K-u_K)
+    const double pdK = pK * (dS * rr);
+#endif
     const double xi = (dK * dK) * rr;
     const double ufv = fma(sstar, xi - 1.0, uK);
 #pragma unroll
@@ -388,7 +412,7 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
             F[M::IM + k] = (rK * vK[M::IM + k]) * ufv;
         }
     }
-    const double inner = fma(sS - uK, fma(rK, sS, pK * (dS * rr)), EK);
+    const double inner = fma(sS - uK, fma(rK, sS, pdK), EK);
     F[M::IE] = fma(sstar, fma(xi, inner, -EK), uK * (EK + pK));
     uf = ufv;
 }

@@ -15,6 +15,12 @@
 #pragma once
 #include <cstdint>
 
+#ifndef MFC_WENO_ONE_RCP
+#define MFC_WENO_ONE_RCP 1      // r98: C3 x -0.034, y -0.010, z -0.014 ms per step (3 reps)
+#endif
+#ifndef MFC_WENO_ONE_RCP_LEAN
+#define MFC_WENO_ONE_RCP_LEAN 0
+#endif
 #ifndef MFC_HLLC_ONE_RCP
 #define MFC_HLLC_ONE_RCP 1   // r96: x -0.015, y -0.01 ms per step (same box, 3 repetitions)
 #endif
@@ -193,13 +199,21 @@ __device__ __forceinline__ void weno5_d(double D0, double D1, double D2, double 
     const double xm2 = fma(2.0, D2, -0.5 * D3);
     const double Dm = fma(6.0, P1, fma(3.0, P2, P0));
     const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
+#if !MFC_WENO_ONE_RCP_LEAN
     vm = fma(Nm, rcp(Dm), c);
+#endif
     const double xp0 = fma(-2.0, D1, 0.5 * D0);
     const double xp1 = fma(-2.0, D1, -D2);
     const double xp2 = fma(k13, D3, -k56 * D2);
     const double Dp = fma(3.0, P0, fma(6.0, P1, P2));
     const double Np = fma(P2, xp2, fma(P1, xp1, P0 * xp0));
+#if MFC_WENO_ONE_RCP_LEAN
+    const double R = rcp(Dm * Dp);           // see weno5_fewop_s
+    vm = fma(Nm * Dp, R, c);
+    vp = fma(Np * Dm, R, c);
+#else
     vp = fma(Np, rcp(Dp), c);
+#endif
 }
 
 // WENO5-JS with two FP64 operations fewer per variable than weno5 (same beta'_k, t_k,
@@ -228,11 +242,17 @@ __device__ __forceinline__ void weno5_fewop_d(double D0, double D1, double D2, d
     const double xm0 = fma(k23, s0, D1), xm1 = fma(3.0, r1, s1), xm2 = D2 - r2;
     const double Dm = fma(12.0, P1, fma(6.0, P2, 2.0 * P0));
     const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
-    vm = fma(Nm, rcp(Dm), c);
     const double yp0 = r0 + D1, yp1 = fma(3.0, r1, -s1), yp2 = fma(-k23, s2, D2);   // = -X
     const double Dp = fma(12.0, P1, fma(2.0, P2, 6.0 * P0));
     const double Np = fma(P2, yp2, fma(P1, yp1, P0 * yp0));
+#if MFC_WENO_ONE_RCP
+    const double R = rcp(Dm * Dp);           // see weno5_fewop_s
+    vm = fma(Nm * Dp, R, c);
+    vp = fma(-Np * Dm, R, c);
+#else
+    vm = fma(Nm, rcp(Dm), c);
     vp = fma(-Np, rcp(Dp), c);
+#endif
 }
 
 // weno5_fewop with the curvature terms passed in: S_k = (13/3) s_k^2 + eps' formed by the
@@ -254,11 +274,19 @@ __device__ __forceinline__ void weno5_fewop_s(double r0, double D1, double D2, d
     const double xm0 = fma(k23, s0, D1), xm1 = fma(3.0, r1, s1), xm2 = D2 - r2;
     const double Dm = fma(12.0, P1, fma(6.0, P2, 2.0 * P0));
     const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
-    vm = fma(Nm, rcp(Dm), c);
     const double yp0 = r0 + D1, yp1 = fma(3.0, r1, -s1), yp2 = fma(-k23, s2, D2);   // = -X
     const double Dp = fma(12.0, P1, fma(2.0, P2, 6.0 * P0));
     const double Np = fma(P2, yp2, fma(P1, yp1, P0 * yp0));
+#if MFC_WENO_ONE_RCP
+    // one reciprocal for both sides: 1/Dm = Dp R, 1/Dp = Dm R, R = 1/(Dm Dp)
+    // (Dm Dp <= ~1e170 for |dv| <= 1e10, >= ~1e-123 for eps' = 4e-16)
+    const double R = rcp(Dm * Dp);
+    vm = fma(Nm * Dp, R, c);
+    vp = fma(-Np * Dm, R, c);
+#else
+    vm = fma(Nm, rcp(Dm), c);
     vp = fma(-Np, rcp(Dp), c);
+#endif
 }
 __device__ __forceinline__ double weno_S(double s, double eps4) {
     return fma((13.0 / 3.0) * s, s, eps4);

@@ -130,7 +130,9 @@ int mfc_get_neighbors(const mfc_ctx* ctx, int32_t nbr[6]);
 int mfc_bind_workspace(mfc_ctx* ctx, void* dev_ptr, size_t bytes);
 
 /* WENO epsilon of alpha_k = d_k/(beta_k+eps)^2 (DESIGN.md AMB-8); default 1e-16;
- * must be in [1e-40, 1e-2]. */
+ * must be in [1e-30, 1e-2] (the kernels' one-reciprocal weight normalisation divides
+ * by a product of two weight sums, ~ (4 eps)^8 on uniform data, which must stay a
+ * normal double).  Errors: EINVAL (NULL ctx, eps out of range). */
 int mfc_set_weno_eps(mfc_ctx* ctx, double eps);
 
 /* Reconstruction order: 5 (WENO5-JS, default) or 3 (WENO3-JS), the two options of

@@ -1394,7 +1394,9 @@ int mfc_set_weno_order(mfc_ctx* c, int32_t order) {
 
 int mfc_set_weno_eps(mfc_ctx* c, double eps) {
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
-    if (!(eps >= 1e-40 && eps <= 1e-2)) return fail(MFC_EINVAL, "eps out of [1e-40, 1e-2]");
+    // >= 1e-30: the one-reciprocal WENO forms divide by products of two weight sums,
+    // ~ (4 eps)^8 on uniform data, which must stay a normal double (rcp.approx.ftz)
+    if (!(eps >= 1e-30 && eps <= 1e-2)) return fail(MFC_EINVAL, "eps out of [1e-30, 1e-2]");
     c->eps = eps;
     if (c->graph) {
         cudaGraphExecDestroy(c->graph);

@@ -18,6 +18,9 @@
 #ifndef MFC_WENO_ONE_RCP
 #define MFC_WENO_ONE_RCP 1      // r98: C3 x -0.034, y -0.010, z -0.014 ms per step (3 reps)
 #endif
+#ifndef MFC_WENO5M_ONE_RCP
+#define MFC_WENO5M_ONE_RCP 1
+#endif
 #ifndef MFC_WENO_ONE_RCP_LEAN
 #define MFC_WENO_ONE_RCP_LEAN 0
 #endif
@@ -324,6 +327,25 @@ __device__ __forceinline__ void weno5m_side(const double (&P)[3], const double (
     v = fma(N * (1.0 / 6.0), rcp((Q0 + Q1) + Q2), c);
 }
 
+// the mapped, un-normalised weights of one side given W = 1/sum_k d_k P_k:
+// N = sum_k Q_k A_k, S = sum_k Q_k
+__device__ __forceinline__ void weno5m_sums(const double (&P)[3], const double (&A)[3],
+                                            const double (&d)[3], double W, double& N,
+                                            double& S) {
+    double num[3], den[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double w = d[k] * P[k] * W;
+        num[k] = w * fma(w, w - 3.0 * d[k], fma(d[k], d[k], d[k]));
+        den[k] = fma(w, 1.0 - 2.0 * d[k], d[k] * d[k]);
+    }
+    const double Q0 = num[0] * (den[1] * den[2]);
+    const double Q1 = num[1] * (den[0] * den[2]);
+    const double Q2 = num[2] * (den[0] * den[1]);
+    N = fma(Q2, A[2], fma(Q1, A[1], Q0 * A[0]));
+    S = (Q0 + Q1) + Q2;
+}
+
 __device__ __forceinline__ void weno5m(double a, double b, double c, double d, double e,
                                        double eps4, double& vm, double& vp) {
     constexpr double k133 = 13.0 / 3.0;
@@ -337,8 +359,25 @@ __device__ __forceinline__ void weno5m(double a, double b, double c, double d, d
     const double Am[3] = {fma(5.0, D1, -2.0 * D0), fma(2.0, D2, D1), fma(4.0, D2, -D3)};
     const double Ap[3] = {fma(-4.0, D1, D0), fma(-2.0, D1, -D2), fma(2.0, D3, -5.0 * D2)};
     const double dm[3] = {0.1, 0.6, 0.3}, dp[3] = {0.3, 0.6, 0.1};
+#if MFC_WENO5M_ONE_RCP
+    // both sides at once, one reciprocal for each pair of divisions (as in weno5_fewop_d):
+    // 1/Zm = Zp R1, 1/Zp = Zm R1 with R1 = 1/(Zm Zp), and the same for the two
+    // renormalisations. Zm Zp ~ P^2 (<= ~1e160 for |dv| <= 1e10, >= ~1e-124 for
+    // eps' = 4e-16); the sums of Q are O(1e-3 .. 1).
+    const double Zm = fma(dm[2], P[2], fma(dm[1], P[1], dm[0] * P[0]));
+    const double Zp = fma(dp[2], P[2], fma(dp[1], P[1], dp[0] * P[0]));
+    const double R1 = rcp(Zm * Zp);
+    const double Wm = Zp * R1, Wp = Zm * R1;
+    double Nm, Sm, Np, Sp;
+    weno5m_sums(P, Am, dm, Wm, Nm, Sm);
+    weno5m_sums(P, Ap, dp, Wp, Np, Sp);
+    const double R2 = rcp(Sm * Sp) * (1.0 / 6.0);
+    vm = fma(Nm * Sp, R2, c);
+    vp = fma(Np * Sm, R2, c);
+#else
     weno5m_side(P, Am, dm, c, vm);
     weno5m_side(P, Ap, dp, c, vp);
+#endif
 }
 
 // WENO3-JS ("third or fifth-order"; F2) for one variable of cell m from

@@ -147,6 +147,8 @@ def test_new_entry_points_validate_arguments(mfc):
         assert mfc.lib.mfc_set_weno_mapped(h, 0) == 0
         assert mfc.lib.mfc_set_weno_mapped(None, 1) == -1
         assert mfc.lib.mfc_set_weno_eps(h, 0.5) == -1
+        assert mfc.lib.mfc_set_weno_eps(h, 1e-40) == -1   # (4 eps)^8 would be subnormal
+        assert mfc.lib.mfc_set_weno_eps(h, 1e-30) == 0
         assert mfc.lib.mfc_set_weno_eps(h, 1e-16) == 0
         dt = ctypes.c_double(0.0)
         assert mfc.lib.mfc_cfl_dt(h, None, 0.4, ctypes.byref(dt), None, None) == -1

@@ -139,3 +139,48 @@ def test_fewop_candidate_identities():
         assert -(r0 + D1) == Ap[0]
         assert -(3 * r1 - s1) == 2 * Ap[1]
         assert abs(-3 * (D2 - K23 * s2) - Ap[2]) < 1e-9
+
+
+def _weno5m_sums(P, A, d, W):
+    """`weno5m_sums`: mapped, un-normalised weights Q_k = num_k den_i den_j of one side."""
+    num, den = [], []
+    for k in range(3):
+        w = d[k] * P[k] * W
+        num.append(w * (w * (w - 3.0 * d[k]) + (d[k] * d[k] + d[k])))
+        den.append(w * (1.0 - 2.0 * d[k]) + d[k] * d[k])
+    Q = (num[0] * (den[1] * den[2]), num[1] * (den[0] * den[2]), num[2] * (den[0] * den[1]))
+    return Q[2] * A[2] + (Q[1] * A[1] + Q[0] * A[0]), (Q[0] + Q[1]) + Q[2]
+
+
+def weno5m_one_rcp(a, b, c, d, e, eps):
+    """`weno5m` with MFC_WENO5M_ONE_RCP: both sides together, 1/Zm = Zp/(Zm Zp) and
+    1/Sm = Sp/(Sm Sp) (one reciprocal per pair of divisions)."""
+    D0, D1, D2, D3 = b - a, c - b, d - c, e - d
+    _, _, P = _beta_terms(D0, D1, D2, D3, 4.0 * eps)
+    Am = (5.0 * D1 - 2.0 * D0, 2.0 * D2 + D1, 4.0 * D2 - D3)
+    Ap = (-4.0 * D1 + D0, -2.0 * D1 - D2, 2.0 * D3 - 5.0 * D2)
+    dm, dp = (0.1, 0.6, 0.3), (0.3, 0.6, 0.1)
+    Zm = dm[2] * P[2] + (dm[1] * P[1] + dm[0] * P[0])
+    Zp = dp[2] * P[2] + (dp[1] * P[1] + dp[0] * P[0])
+    R1 = 1.0 / (Zm * Zp)
+    Nm, Sm = _weno5m_sums(P, Am, dm, Zp * R1)
+    Np, Sp = _weno5m_sums(P, Ap, dp, Zm * R1)
+    R2 = 1.0 / (Sm * Sp) * (1.0 / 6.0)
+    return c + Nm * Sp * R2, c + Np * Sm * R2
+
+
+def test_weno5m_one_rcp_form_equals_oracle():
+    """The two-sided WENO5-M form against the oracle's
+    orc_weno5m_minus/plus (pinned in test_oracle_weno_mapped.py), over the same stencil
+    mix (values up to ~1e9 and steps up to ~1e9: Zm Zp ~ P^2 stays finite)."""
+    for eps in (1e-16, 1e-6):
+        for v in _stencils(2000):
+            vm_ref = O.weno5m_minus(*v, eps=eps)
+            vp_ref = O.weno5m_plus(*v, eps=eps)
+            vm_ref = vm_ref[0] if isinstance(vm_ref, tuple) else vm_ref
+            vp_ref = vp_ref[0] if isinstance(vp_ref, tuple) else vp_ref
+            vm, vp = weno5m_one_rcp(*v, eps)
+            scale = np.abs(v).max()
+            assert np.isfinite(vm) and np.isfinite(vp)
+            assert abs(vm - vm_ref) <= 1e-14 * scale, (v, vm, vm_ref)
+            assert abs(vp - vp_ref) <= 1e-14 * scale, (v, vp, vp_ref)

@@ -19,7 +19,10 @@
 #define MFC_WENO_ONE_RCP 1      // r98: C3 x -0.034, y -0.010, z -0.014 ms per step (3 reps)
 #endif
 #ifndef MFC_WENO5M_ONE_RCP
-#define MFC_WENO5M_ONE_RCP 1
+#define MFC_WENO5M_ONE_RCP 1   // r100: C3 --weno 5m 10.43-10.53 -> 10.32-10.42 ms (3 reps)
+#endif
+#ifndef MFC_WENO5M_ALPHA
+#define MFC_WENO5M_ALPHA 1      // r101: C3 --weno 5m 10.322 -> 10.304 ms (3 reps; x +0.007, z -0.023)
 #endif
 #ifndef MFC_WENO_ONE_RCP_LEAN
 #define MFC_WENO_ONE_RCP_LEAN 0
@@ -346,6 +349,24 @@ __device__ __forceinline__ void weno5m_sums(const double (&P)[3], const double (
     S = (Q0 + Q1) + Q2;
 }
 
+// weno5m_sums from the unnormalised weights a_k = d_k P_k: w_k = a_k W
+__device__ __forceinline__ void weno5m_sums_a(const double (&a)[3], const double (&A)[3],
+                                              const double (&d)[3], double W, double& N,
+                                              double& S) {
+    double num[3], den[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double w = a[k] * W;
+        num[k] = w * fma(w, w - 3.0 * d[k], fma(d[k], d[k], d[k]));
+        den[k] = fma(w, 1.0 - 2.0 * d[k], d[k] * d[k]);
+    }
+    const double Q0 = num[0] * (den[1] * den[2]);
+    const double Q1 = num[1] * (den[0] * den[2]);
+    const double Q2 = num[2] * (den[0] * den[1]);
+    N = fma(Q2, A[2], fma(Q1, A[1], Q0 * A[0]));
+    S = (Q0 + Q1) + Q2;
+}
+
 __device__ __forceinline__ void weno5m(double a, double b, double c, double d, double e,
                                        double eps4, double& vm, double& vp) {
     constexpr double k133 = 13.0 / 3.0;
@@ -364,13 +385,24 @@ __device__ __forceinline__ void weno5m(double a, double b, double c, double d, d
     // 1/Zm = Zp R1, 1/Zp = Zm R1 with R1 = 1/(Zm Zp), and the same for the two
     // renormalisations. Zm Zp ~ P^2 (<= ~1e160 for |dv| <= 1e10, >= ~1e-124 for
     // eps' = 4e-16); the sums of Q are O(1e-3 .. 1).
+    double Nm, Sm, Np, Sp;
+#if MFC_WENO5M_ALPHA
+    // the unnormalised Jiang-Shu weights a_k = d_k P_k formed once (0.6 P1 shared by both
+    // sides) and reused for the sums and for w_k = a_k W: 4 FP64 fewer per variable
+    const double a1 = 0.6 * P[1];
+    const double am[3] = {0.1 * P[0], a1, 0.3 * P[2]}, ap[3] = {0.3 * P[0], a1, 0.1 * P[2]};
+    const double Zm = (am[0] + am[1]) + am[2], Zp = (ap[0] + ap[1]) + ap[2];
+    const double R1 = rcp(Zm * Zp);
+    weno5m_sums_a(am, Am, dm, Zp * R1, Nm, Sm);
+    weno5m_sums_a(ap, Ap, dp, Zm * R1, Np, Sp);
+#else
     const double Zm = fma(dm[2], P[2], fma(dm[1], P[1], dm[0] * P[0]));
     const double Zp = fma(dp[2], P[2], fma(dp[1], P[1], dp[0] * P[0]));
     const double R1 = rcp(Zm * Zp);
     const double Wm = Zp * R1, Wp = Zm * R1;
-    double Nm, Sm, Np, Sp;
     weno5m_sums(P, Am, dm, Wm, Nm, Sm);
     weno5m_sums(P, Ap, dp, Wp, Np, Sp);
+#endif
     const double R2 = rcp(Sm * Sp) * (1.0 / 6.0);
     vm = fma(Nm * Sp, R2, c);
     vp = fma(Np * Sm, R2, c);

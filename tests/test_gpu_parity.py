@@ -63,14 +63,29 @@ def test_rhs_parity_degenerate_sizes(n):
     _rhs_case(W.random_problem(d, n[:d], 2, "gas"))
 
 
-def test_uniform_state_rhs_exactly_zero_on_gpu():
+@pytest.mark.parametrize("order,mapped", [(5, False), (5, True), (3, False)])
+@pytest.mark.parametrize("eps", [1e-16, 1e-30, 1e-2])
+def test_uniform_state_rhs_exactly_zero_on_gpu(order, mapped, eps):
+    """Uniform data, every reconstruction, eps across mfc_set_weno_eps's range: the
+    one-reciprocal weight normalisations divide by ~(4 eps)^8 products there (AMB-24),
+    which must stay normal (a flushed product would give 0 * inf = NaN)."""
     pb = W.random_problem(3, (37, 21, 19), 2, "water")
+    pb.weno_order, pb.weno_mapped, pb.weno_eps = order, mapped, eps
     P = O.Problem.from_spec(pb)
     v = W.random_prims(pb, seed=1)
     v = np.broadcast_to(v[:, :1, :1, :1], v.shape).copy()
     q = O.prim_to_cons(P, v)
     got = gpu_rhs(pb, q)
     assert np.all(got == 0.0)
+
+
+@pytest.mark.parametrize("order,mapped", [(5, False), (5, True), (3, False)])
+@pytest.mark.parametrize("eps", [1e-30, 1e-2])
+def test_rhs_parity_weno_eps_range_ends(order, mapped, eps):
+    """mfc_set_weno_eps's two ends (AMB-24) on a mixed case, every reconstruction."""
+    pb = W.random_problem(3, (21, 18, 17), 2, "water")
+    pb.weno_order, pb.weno_mapped, pb.weno_eps = order, mapped, eps
+    _rhs_case(pb)
 
 
 @pytest.mark.parametrize("N,d", [(1, 1), (2, 2), (3, 3), (2, 3)])

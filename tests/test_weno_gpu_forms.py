@@ -141,11 +141,12 @@ def test_fewop_candidate_identities():
         assert abs(-3 * (D2 - K23 * s2) - Ap[2]) < 1e-9
 
 
-def _weno5m_sums(P, A, d, W):
-    """`weno5m_sums`: mapped, un-normalised weights Q_k = num_k den_i den_j of one side."""
+def _weno5m_sums(a, A, d, W):
+    """`weno5m_sums_a`: mapped, un-normalised weights Q_k = num_k den_i den_j of one side
+    from the Jiang-Shu weights a_k = d_k P_k."""
     num, den = [], []
     for k in range(3):
-        w = d[k] * P[k] * W
+        w = a[k] * W
         num.append(w * (w * (w - 3.0 * d[k]) + (d[k] * d[k] + d[k])))
         den.append(w * (1.0 - 2.0 * d[k]) + d[k] * d[k])
     Q = (num[0] * (den[1] * den[2]), num[1] * (den[0] * den[2]), num[2] * (den[0] * den[1]))
@@ -153,18 +154,20 @@ def _weno5m_sums(P, A, d, W):
 
 
 def weno5m_one_rcp(a, b, c, d, e, eps):
-    """`weno5m` with MFC_WENO5M_ONE_RCP: both sides together, 1/Zm = Zp/(Zm Zp) and
-    1/Sm = Sp/(Sm Sp) (one reciprocal per pair of divisions)."""
+    """`weno5m` with MFC_WENO5M_ONE_RCP and MFC_WENO5M_ALPHA: both sides together,
+    1/Zm = Zp/(Zm Zp) and 1/Sm = Sp/(Sm Sp) (one reciprocal per pair of divisions), the
+    weights a_k = d_k P_k formed once."""
     D0, D1, D2, D3 = b - a, c - b, d - c, e - d
     _, _, P = _beta_terms(D0, D1, D2, D3, 4.0 * eps)
     Am = (5.0 * D1 - 2.0 * D0, 2.0 * D2 + D1, 4.0 * D2 - D3)
     Ap = (-4.0 * D1 + D0, -2.0 * D1 - D2, 2.0 * D3 - 5.0 * D2)
     dm, dp = (0.1, 0.6, 0.3), (0.3, 0.6, 0.1)
-    Zm = dm[2] * P[2] + (dm[1] * P[1] + dm[0] * P[0])
-    Zp = dp[2] * P[2] + (dp[1] * P[1] + dp[0] * P[0])
+    a1 = 0.6 * P[1]
+    am, ap = (0.1 * P[0], a1, 0.3 * P[2]), (0.3 * P[0], a1, 0.1 * P[2])
+    Zm, Zp = (am[0] + am[1]) + am[2], (ap[0] + ap[1]) + ap[2]
     R1 = 1.0 / (Zm * Zp)
-    Nm, Sm = _weno5m_sums(P, Am, dm, Zp * R1)
-    Np, Sp = _weno5m_sums(P, Ap, dp, Zm * R1)
+    Nm, Sm = _weno5m_sums(am, Am, dm, Zp * R1)
+    Np, Sp = _weno5m_sums(ap, Ap, dp, Zm * R1)
     R2 = 1.0 / (Sm * Sp) * (1.0 / 6.0)
     return c + Nm * Sp * R2, c + Np * Sm * R2
 

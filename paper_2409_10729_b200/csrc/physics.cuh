@@ -21,6 +21,9 @@
 #ifndef MFC_WENO5M_ONE_RCP
 #define MFC_WENO5M_ONE_RCP 1   // r100: C3 --weno 5m 10.43-10.53 -> 10.32-10.42 ms (3 reps)
 #endif
+#ifndef MFC_WENO3_ONE_RCP
+#define MFC_WENO3_ONE_RCP 1      // r102: C3 --weno 3 5.493-5.512 -> 5.461-5.484 ms (3 reps)
+#endif
 #ifndef MFC_WENO5M_ALPHA
 #define MFC_WENO5M_ALPHA 1      // r101: C3 --weno 5m 10.322 -> 10.304 ms (3 reps; x +0.007, z -0.023)
 #endif
@@ -424,8 +427,17 @@ __device__ __forceinline__ void weno3(double a, double b, double c, double eps, 
     double t1 = fma(D1, D1, eps); t1 *= t1;
     const double wm0 = t1 * (1.0 / 3.0), wm1 = t0 * (2.0 / 3.0);
     const double wp0 = t1 * (2.0 / 3.0), wp1 = t0 * (1.0 / 3.0);
+#if MFC_WENO3_ONE_RCP
+    // one reciprocal for both sides (as in weno5_fewop_d): Zm Zp ~ t^2 with
+    // t_k = (D_k^2 + eps)^2, so >= ~1e-120 for eps >= 1e-30, <= ~1e80 for |dv| <= 1e10
+    const double Zm = wm0 + wm1, Zp = wp0 + wp1;
+    const double R = rcp(Zm * Zp) * 0.5;
+    vm = fma(fma(wm1, D1, wm0 * D0) * Zp, R, b);
+    vp = fma(-fma(wp1, D1, wp0 * D0) * Zm, R, b);
+#else
     vm = fma(0.5 * fma(wm1, D1, wm0 * D0), rcp(wm0 + wm1), b);
     vp = fma(-0.5 * fma(wp1, D1, wp0 * D0), rcp(wp0 + wp1), b);
+#endif
 }
 
 // HLLC face flux F[E] and face velocity uf for the normal direction DIR

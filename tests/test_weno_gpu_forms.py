@@ -187,3 +187,28 @@ def test_weno5m_one_rcp_form_equals_oracle():
             assert np.isfinite(vm) and np.isfinite(vp)
             assert abs(vm - vm_ref) <= 1e-14 * scale, (v, vm, vm_ref)
             assert abs(vp - vp_ref) <= 1e-14 * scale, (v, vp, vp_ref)
+
+
+def weno3_one_rcp(a, b, c, eps):
+    """`weno3` with MFC_WENO3_ONE_RCP: 1/Zm = Zp/(Zm Zp), 1/Zp = Zm/(Zm Zp)."""
+    D0, D1 = b - a, c - b
+    t0, t1 = (D0 * D0 + eps) ** 2, (D1 * D1 + eps) ** 2
+    wm0, wm1 = t1 * (1.0 / 3.0), t0 * (2.0 / 3.0)
+    wp0, wp1 = t1 * (2.0 / 3.0), t0 * (1.0 / 3.0)
+    Zm, Zp = wm0 + wm1, wp0 + wp1
+    R = 1.0 / (Zm * Zp) * 0.5
+    return b + (wm1 * D1 + wm0 * D0) * Zp * R, b - (wp1 * D1 + wp0 * D0) * Zm * R
+
+
+def test_weno3_one_rcp_form_equals_oracle():
+    """The two-sided WENO3 form (F2, AMB-26) against the oracle's orc_weno3_minus/plus on
+    the stencil mix, at both ends of mfc_set_weno_eps's range."""
+    for eps in (1e-16, 1e-30, 1e-2):
+        for v in _stencils(2000):
+            a, b, c = v[1], v[2], v[3]
+            vm_ref, _ = O.weno3_minus(a, b, c, eps=eps)
+            vp_ref, _ = O.weno3_plus(a, b, c, eps=eps)
+            vm, vp = weno3_one_rcp(a, b, c, eps)
+            scale = max(abs(a), abs(b), abs(c))
+            assert abs(vm - vm_ref) <= 4e-15 * scale, (v, vm, vm_ref)
+            assert abs(vp - vp_ref) <= 4e-15 * scale, (v, vp, vp_ref)

@@ -3,6 +3,8 @@ times: C3 (256^3, N = 2, E = 8).  The oracle computes the full RHS (~10 s on the
 cores) and one full SSP-RK3 step; the GPU runs the same Solver configuration as the
 bench.  C5 (512^3, N = 3) is checked on sampled cells computed one by one by the
 oracle (orc_rhs_cells) from a local patch of the field."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -37,6 +39,24 @@ def test_c3_full_rhs(c3):
     ref = O.rhs(P, q)
     err = rel_err(got, ref, rhs_flux_scale(pb, v, q))
     record("rhs C3 full 256^3 (bench launch config)", err, RHS_TOL, rel_err(got, ref))
+    assert np.all(err <= RHS_TOL), err
+
+
+@pytest.mark.parametrize("order,mapped", [(3, False), (5, True)], ids=["weno3", "weno5m"])
+def test_c3_full_rhs_weno_options(c3, order, mapped):
+    """The reconstruction options bench.py --weno {3,5m} times (F2), at the full C3 size."""
+    pb, _, v, q = c3
+    pb = dataclasses.replace(pb, weno_order=order, weno_mapped=mapped)
+    s = mfc.Solver(pb)
+    qd = s.state_from_cons(q)
+    rd = s.rhs(qd)
+    torch.cuda.synchronize()
+    got = s.interior(rd).cpu().numpy()
+    del rd, qd
+    ref = O.rhs(O.Problem.from_spec(pb), q)
+    err = rel_err(got, ref, rhs_flux_scale(pb, v, q))
+    record(f"rhs C3 full 256^3 weno{order}{'m' if mapped else ''}", err, RHS_TOL,
+           rel_err(got, ref))
     assert np.all(err <= RHS_TOL), err
 
 

@@ -126,7 +126,9 @@ int mfc_get_neighbors(const mfc_ctx* ctx, int32_t nbr[6]);
 /* Hand the library a device buffer of >= layout.workspace_bytes bytes, 256-byte
  * aligned (torch-owned; the library never frees it).  It holds two RK stage
  * buffers, the RHS accumulator and the halo pack buffers.  Must be bound before
- * mfc_rk3_step.  Errors: EINVAL (NULL, misaligned), ENOMEM (too small). */
+ * mfc_rk3_step.  Rebinding drops the captured CUDA graph of mfc_rk3_steps.
+ * Errors: EINVAL (NULL, misaligned), ENOMEM (too small), ESTATE (the fused halo is
+ * attached: neighbours hold pointers into the bound stage buffers). */
 int mfc_bind_workspace(mfc_ctx* ctx, void* dev_ptr, size_t bytes);
 
 /* WENO epsilon of alpha_k = d_k/(beta_k+eps)^2 (DESIGN.md AMB-8); default 1e-16;
@@ -159,7 +161,9 @@ int mfc_cons_to_prim(mfc_ctx* ctx, const double* q, double* v, void* stream);
  * max-allreduce) of max_k (|u_k| + c)/dx_k, c^2 = ((Gamma+1)p + Pi)/(rho Gamma);
  * enqueued on `stream`, no host sync.  mfc_cfl_dt computes it into the device
  * scratch double d_scratch, synchronises `stream` and returns *dt_out = cfl/rate on
- * the host (ESTATE if the rate is not positive and finite). */
+ * the host (ESTATE if the rate is not positive and finite).  A multi-rank context
+ * without an NCCL communicator (loopback or peer transport) has no way to reduce
+ * across ranks: EUNSUPPORTED, so no rank ever gets a local-only dt. */
 int mfc_max_wave_rate(mfc_ctx* ctx, const double* q, double* d_out, void* stream);
 int mfc_cfl_dt(mfc_ctx* ctx, const double* q, double cfl, double* dt_out, double* d_scratch,
                void* stream);
@@ -192,16 +196,25 @@ int mfc_rk3_steps(mfc_ctx* ctx, double* q, double dt, int64_t nsteps, void* stre
 /* End-to-end call with HOST buffers: copy the dense interior q_in[E][nz][ny][nx]
  * (host, pinned or pageable) into the padded device buffer q_dev, run nsteps RK3
  * steps of size dt, copy the interior back to q_out (host; may equal q_in), and
- * synchronise `stream`.  Host arrays are dense, x fastest, n_local extents.
- * Needs a bound workspace.  One step of a single-rank 3D domain with enough z planes
- * is STREAMED: z-chunks are computed as independent sub-domains over their planes +-9
- * (3 stages x the 3-cell stencil reach) while later input planes are still being
- * copied in and earlier results copied out (two copy streams besides `stream`; the
- * chunk states live in the workspace); the result is bitwise that of mfc_rk3_step.
- * After a streamed step q_dev holds the INPUT state, otherwise the result.
- * MFC_STREAM=0 disables streaming; MFC_STREAM=P (> 1) asks for P chunks. */
+ * synchronise `stream`.  Host arrays are dense, x fastest, n_local extents; q_in and
+ * q_out must each hold E*nx*ny*nz doubles (the library cannot check host sizes).
+ * Needs a bound workspace.  On return q_dev holds the result (the state after the
+ * nsteps steps), like q_out.
+ * One step (nsteps == 1) of a single-rank 3D domain with >= 9 z planes is STREAMED
+ * (DESIGN.md §6.4): a wavefront over z-chunks of >= 3 planes runs stage s of chunk k
+ * once stage s-1 of chunks k-1..k+1 is done, in the whole-domain buffers, while later
+ * input planes are still being copied in and finished chunks copied out (two copy
+ * streams and a second compute stream besides `stream`); every plane of every stage
+ * is computed once by the same kernels as mfc_rk3_step, so the result is bitwise
+ * mfc_rk3_step's whatever the workspace held before.  mfc_set_stream_chunks chooses
+ * the chunk count. */
 int mfc_advance_host(mfc_ctx* ctx, const double* q_in, double* q_out, double* q_dev,
                      int64_t nsteps, double dt, void* stream);
+
+/* Chunk count of the streamed mfc_advance_host step: 0 = never stream, 1 or -1 = the
+ * default (32 z-chunks, ramped 3..7 planes at both ends), P > 1 = about P chunks (each
+ * >= 3 planes).  EINVAL below -1. */
+int mfc_set_stream_chunks(mfc_ctx* ctx, int32_t chunks);
 
 /* Loopback groups: the same operations for `count` contexts created with
  * comm.loopback = 1 and ranks 0..count-1 (in order), exchanging halos with device

@@ -10,21 +10,10 @@
 namespace mfc {
 
 // Launch the sweep kernel for N fluids, D dims, direction DIR with epilogue `mode`
-// (M_SET / M_RKINIT for DIR == 0, M_ACC for DIR > 0).
+// (M_SET / M_RKINIT for DIR == 0, M_ACC / M_ACCN for DIR > 0).
 template <int N>
 cudaError_t launch_sweep(int D, int DIR, int mode, int order, const SweepArgs& a, dim3 grid,
                          dim3 block, cudaStream_t s);
-
-// Does the x sweep use the row-parallel tile kernel (else the staged march)?  The tile
-// kernel is the default for every row length (r50: C3 2.77 -> 2.40, C5 29.9 -> 29.2,
-// C2 0.123 -> 0.096 ms of x sweep per step); MFC_X_ROWS=0 or MFC_X_STAGED selects the
-// staged march (measurements).
-inline bool x_rows_used(int /*n*/) {
-    static const int xr = getenv("MFC_X_ROWS") ? atoi(getenv("MFC_X_ROWS")) : -1;
-    static const bool staged = getenv("MFC_X_STAGED") != nullptr;
-    if (staged) return false;
-    return xr != 0;
-}
 
 struct EosArgs {
     const double* in;

@@ -96,9 +96,7 @@ struct mfc_ctx {
     double* recvb[6] = {};
     int64_t face_elems[3] = {0, 0, 0};  // E * 3 * area of a face normal to dim k
     int64_t launches = 0;
-    int seg = 0;  // sweep segment length override (0 = heuristic)
-    int seg_dir[3] = {0, 0, 0};  // per-direction overrides (MFC_SEG_X/Y/Z)
-    bool xbase = true;           // RK base in the row-parallel x sweep (MFC_XBASE=0: off)
+    int stream_chunks = -1;       // streamed advance_host: z-chunks (-1 default, 0 off)
     // optional per-launch CUDA-event timing (mfc_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -551,8 +549,6 @@ bool group_fused(mfc_ctx* const* cs, int count, int* err) {
 // r25b): the best is the largest T <= 128 that still gives >= 3 waves of resident
 // warps (x, y: 128; z, with 3 resident blocks/SM, 64).
 int seg_len(const mfc_ctx* c, int dir, int resident_warps_per_sm) {
-    if (c->seg_dir[dir] > 0) return (int)std::min<int64_t>(c->seg_dir[dir], c->nl[dir]);
-    if (c->seg > 0) return c->seg;
     const int t1 = dir == 0 ? 1 : 0;          // lane axis
     const int t2 = dir == 2 ? 1 : 2;          // third axis
     const int64_t warp_lines = (c->nl[t1] + 31) / 32 * c->nl[t2];
@@ -561,8 +557,6 @@ int seg_len(const mfc_ctx* c, int dir, int resident_warps_per_sm) {
     int T = 128;
     while (T > 16 && (double)warp_lines * ((n + T - 1) / T) < 3.0 * resident) T /= 2;
     if (c->D == 1) T = (int)std::max<int64_t>(8, std::min<int64_t>(32, n / 8 + 1));
-    // the staged x sweep (D >= 2) needs segments that are multiples of its 4-cell chunks
-    if (dir == 0 && c->D >= 2) return std::max(4, (int)((std::min<int64_t>(T, n) + 3) / 4 * 4));
     return (int)std::min<int64_t>(T, n);
 }
 
@@ -628,14 +622,10 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     a.ca = ca;
     a.cb = cb;
     a.mat = c->mat;
-    int bx = (int)std::min<int64_t>(32, a.nA);
-    int by = (int)std::max<int64_t>(1, std::min<int64_t>(128 / bx, a.nB));
-    if (dir == 0 && c->D >= 2 && mode == M_SET) {
-        bx = 32;   // staged x sweep: one warp per 32 rows, E*3 KB of shared memory per warp
-        by = (int)std::max<int64_t>(1, std::min<int64_t>(c->E <= 8 ? 4 : 2, a.nB));
-    }   // (ring sweeps fix their own block shape: 32 x NTH/32, see sweep_nth)
-    dim3 block(bx, by);
-    dim3 grid((a.nA + bx - 1) / bx, (a.nB + by - 1) / by, (a.s_hi - a.s_lo + a.T - 1) / a.T);
+    // (the ring marches fix their own block shape, 32 x NTH/32, and the x-row kernels
+    // their own grid; only the segment count along the sweep is passed on)
+    const dim3 block(32, 1);
+    const dim3 grid(1, 1, (a.s_hi - a.s_lo + a.T - 1) / a.T);
     cudaError_t e;
     ProfScope ps(c, s, K_SWEEP_X + dir);
     // kernel template order: 3, 5, or 6 = WENO5 with mapped weights
@@ -654,7 +644,9 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
 // One RHS evaluation of the stencil state q, assembled across the sweeps:
 //   rk == false: dst = c_x + c_y + c_z                    (acc == dst, the rhs buffer)
 //   rk == true : dst = ca*qn + cb*(q + dt*(c_x + c_y + c_z)), accumulating in acc:
-//     1D: x = M_RKINIT -> dst;  2D/3D: x = M_SET -> acc, y = M_RKACC, z = M_ACC.
+//     1D: x = M_RKINIT -> dst;
+//     2D/3D: x = M_RKINIT -> acc (cb*q + w*c_x, plus ca*qn in 3D with E <= 8), the middle
+//     sweep M_ACC, the last sweep M_ACCN (adds ca*qn) or M_ACC.
 int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const double* qn,
            double dt, double ca, double cb, cudaStream_t s, cudaEvent_t halo = nullptr,
            int peer_buf = -1) {
@@ -674,23 +666,18 @@ int sweeps(mfc_ctx* c, const double* q, double* acc, double* dst, bool rk, const
         }
         const bool last = dir == c->D - 1;
         double* out = last ? dst : acc;
-        // RK stage assembly (2D/3D): with the row-parallel x sweep, x writes
-        // cb*q^s + w*c_x (its own cells, coalesced), the middle sweep adds w*c_y and the
-        // last one w*c + ca*q^n (M_ACCN, stages 2-3); with the staged x sweep, x writes
-        // c_x and the y sweep assembles the base (M_RKACC)
-        const bool xb = rk && c->D >= 2 && c->xbase && x_rows_used((int)c->nl[0]);
+        // RK stage assembly (2D/3D): the row-parallel x sweep writes cb*q^s + w*c_x (its
+        // own cells, coalesced), the middle sweep adds w*c_y and the last one
+        // w*c + ca*q^n (M_ACCN, stages 2-3)
+        const bool xb = rk && c->D >= 2;
         // 3D, E <= 8: the x sweep also adds ca*q^n, and the z sweep is a plain accumulate
         // (M_ACC) in every stage: C3 x +0.10, z -0.15 ms per step (r89, three same-box
-        // repetitions); E = 10 loses (C5 x +1.37, z -0.84).  MFC_XBASE_N=0/1 forces it.
-        static const int xbn_env = getenv("MFC_XBASE_N") ? atoi(getenv("MFC_XBASE_N")) : -1;
-        const bool xbn = xb && (xbn_env < 0 ? (c->D == 3 && c->E <= 8) : xbn_env != 0);
+        // repetitions); E = 10 loses (C5 x +1.37, z -0.84)
+        const bool xbn = xb && c->D == 3 && c->E <= 8;
         int mode;
-        if (dir == 0) mode = (rk && (c->D == 1 || xb)) ? M_RKINIT : M_SET;
-        else if (xb) mode = (last && ca != 0.0 && !xbn) ? M_ACCN : M_ACC;
-        else if (dir == 1 && rk) mode = M_RKACC;
-        else mode = M_ACC;
-        // M_SET in an RK stage writes the unscaled c_x; M_RKACC scales (acc + c_y) by w
-        const double wd = (mode == M_SET) ? 1.0 : w;
+        if (dir == 0) mode = rk ? M_RKINIT : M_SET;
+        else mode = (rk && last && ca != 0.0 && !xbn) ? M_ACCN : M_ACC;
+        const double wd = w;
         PeerOut po;
         po.nf = 0;
         if (last && peer_buf >= 0)
@@ -782,8 +769,10 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
 // result is bitwise mfc_rk3_step's and it is left in q_dev.  Stage 3 writes q_dev in
 // place, which is safe because stage 1 of chunk k+1 (the last reader of chunk k's input
 // planes) runs before stage 3 of chunk k.  A periodic z axis closes the ring at chunk
-// 0: its stages 2 and 3 wait for the end (stage 2 of chunk 0 before stage 3 of chunk
-// P-1, which reads it), and its input planes stay intact until then.
+// 0: stage 2 of chunk 0 reads stage 1 of chunk P-1, so it waits for the end, and so do
+// the three stage-3 chunks that read it (P-1, 0 and 1); chunk 0's input planes stay
+// intact until then (r2 fix: stage 3 of chunk 1 used to run inside the wavefront and
+// read chunk 0's stage-2 planes before they were computed).
 //   st_in : H2D of input piece j (= chunk j's planes) into q_dev; periodic: the piece
 //           holding the last 3 planes first                             -> ev_piece[j]
 //   s     : the stage sweeps in wavefront order; stage 1 of chunk k waits for the
@@ -793,7 +782,7 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
 //           s then runs stages 2 and 3 only, stage 2 of chunk k after ev_s1 of chunks
 //           k-1..k+1.  Stage 1 of chunk j+1 depends on input pieces alone, so it runs
 //           concurrently with stages 2/3 of the chunks behind it: the small chunk
-//           kernels fill each other's tails (MFC_STREAM_2S=0: one compute stream).
+//           kernels fill each other's tails.
 //           Every buffer plane is still written by one kernel and read after it:
 //           stage s of chunk k touches acc / its output only on chunk k's planes, and
 //           stage 3's in-place write of chunk k follows stage 2 of chunk k+1, which
@@ -824,10 +813,10 @@ int copy_planes_h(const mfc_ctx* c, bool h2d, const double* host_in, double* hos
 
 // Chunk depth of the streamed step, 0 when the step is not streamed.
 int64_t stream_cz(const mfc_ctx* c) {
-    static const int env = getenv("MFC_STREAM") ? atoi(getenv("MFC_STREAM")) : -1;
-    if (env == 0 || c->D != 3 || c->nranks != 1 || c->fused || !c->ws) return 0;
+    const int chunks = c->stream_chunks;
+    if (chunks == 0 || c->D != 3 || c->nranks != 1 || c->fused || !c->ws) return 0;
     const int64_t nz = c->nl[2];
-    const int64_t want = env > 1 ? env : kStreamChunks;      // chunks
+    const int64_t want = chunks > 1 ? chunks : kStreamChunks;
     const int64_t cz = std::max<int64_t>(kStageReach, (nz + want - 1) / want);
     return nz / kStageReach >= 3 ? cz : 0;
 }
@@ -858,12 +847,11 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
     // from the first result to the end, is the critical path: r75 trace)
     std::vector<int64_t> zb;   // chunk k = planes [zb[k], zb[k+1])
     {
-        static const bool ramp_env = !(getenv("MFC_STREAM_RAMP") && atoi(getenv("MFC_STREAM_RAMP")) == 0);
         std::vector<int64_t> head;
         for (int64_t w = kStageReach; w < cz && head.size() < 5; ++w) head.push_back(w);
         int64_t hsum = 0;
         for (int64_t w : head) hsum += w;
-        const bool ramp = ramp_env && !head.empty() && nz - 2 * hsum >= 2 * cz;
+        const bool ramp = !head.empty() && nz - 2 * hsum >= 2 * cz;
         zb.push_back(0);
         if (ramp) {
             for (int64_t w : head) zb.push_back(zb.back() + w);
@@ -893,16 +881,19 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
     CU_TRY(mk(c->ev_comp, P));
     CU_TRY(mk(c->ev_out, P));
     CU_TRY(mk(c->ev_s1, P));
-    static const bool two = !(getenv("MFC_STREAM_2S") && atoi(getenv("MFC_STREAM_2S")) == 0);
-    if (two && !c->st_s1) CU_TRY(cudaStreamCreateWithFlags(&c->st_s1, cudaStreamNonBlocking));
-    cudaStream_t sa = two ? c->st_s1 : s;          // stage 1 + input scatters
+    if (!c->st_s1) CU_TRY(cudaStreamCreateWithFlags(&c->st_s1, cudaStreamNonBlocking));
+    cudaStream_t sa = c->st_s1;                    // stage 1 + input scatters
     if (!c->ev_start) CU_TRY(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
     if (!c->st_in) CU_TRY(cudaStreamCreateWithFlags(&c->st_in, cudaStreamNonBlocking));
     if (!c->st_out) CU_TRY(cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking));
     auto z0 = [&](int k) { return zb[k]; };
     auto z1 = [&](int k) { return zb[k + 1]; };
     int st;
-    static const bool tr = getenv("MFC_STREAM_TRACE") != nullptr;
+#ifdef MFC_STREAM_TRACE
+    constexpr bool tr = true;      // debug build: per-piece timeline on stderr
+#else
+    constexpr bool tr = false;
+#endif
     std::vector<std::pair<std::string, cudaEvent_t>> tr_ev;
     auto mark = [&](const std::string& name, cudaStream_t on) {
         if (!tr) return;
@@ -920,8 +911,7 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
     // copies are plain contiguous runs (E per piece) instead of 2 KB-row pitched
     // copies, which lost a quarter of the bidirectional bandwidth (r57 trace); a small
     // kernel scatters / gathers the padded planes on the compute stream.
-    const bool staged = c->stage_in && max_cz <= c->stage_cz &&
-                        !getenv("MFC_STREAM_PITCHED");
+    const bool staged = c->stage_in && max_cz <= c->stage_cz;
     CU_TRY(mk(c->ev_scat, P));
     const int64_t plane_d = c->nl[0] * c->nl[1];
     const size_t slot = stage_slot_bytes(c) / sizeof(double);
@@ -988,6 +978,7 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
         return MFC_OK;
     };
     std::vector<int> gathered;   // chunks gathered for D2H, in order
+    int last_out = 0;            // chunk whose D2H was enqueued last
     auto stage = [&](int sg, int k) -> int {
         int r;
         if (sg == 0) {   // the input pieces within reach of chunk k
@@ -1025,21 +1016,27 @@ int advance_streamed(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
                 return r;
             }
             CU_TRY(cudaEventRecord(c->ev_out[k], c->st_out));
+            last_out = k;              // st_out is in order: its last event covers all
             mark("out" + std::to_string(k), c->st_out);
         }
         return MFC_OK;
     };
     c->launches = 0;
-    const int k0 = per ? 1 : 0;                     // periodic: chunk 0's stages 2, 3 last
+    // periodic z: stage 2 of chunk 0 needs stage 1 of chunk P-1, so it runs after the
+    // loop, and so does every stage 3 that reads it: chunks P-1, 0 and 1
+    const int k2 = per ? 1 : 0;                     // first chunk whose stage 2 is in the loop
+    const int k3 = per ? 2 : 0;                     // first chunk whose stage 3 is in the loop
+    const int e3 = per ? P - 1 : P;                 // end of the loop's stage-3 chunks
     for (int j = 0; j <= P + 1; ++j) {
         if (j < P && (st = stage(0, j))) return st;
-        if (j - 1 >= k0 && j - 1 < P && (st = stage(1, j - 1))) return st;
-        if (j - 2 >= k0 && j - 2 < (per ? P - 1 : P) && (st = stage(2, j - 2))) return st;
+        if (j - 1 >= k2 && j - 1 < P && (st = stage(1, j - 1))) return st;
+        if (j - 2 >= k3 && j - 2 < e3 && (st = stage(2, j - 2))) return st;
     }
     if (per) {
         if ((st = stage(1, 0)) || (st = stage(2, P - 1)) || (st = stage(2, 0))) return st;
+        if (P - 1 != 1 && (st = stage(2, 1))) return st;
     }
-    CU_TRY(cudaStreamWaitEvent(s, c->ev_out[per ? 0 : P - 1], 0));
+    CU_TRY(cudaStreamWaitEvent(s, c->ev_out[last_out], 0));
     CU_TRY(cudaStreamSynchronize(s));
     if (tr) {   // MFC_STREAM_TRACE: ms after the start at which each piece / chunk finished
         std::string line = "mfc stream trace (ms): ";
@@ -1287,11 +1284,6 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
         need += 2 * kStageSlots * stage_slot_bytes(c);
     }
     c->ws_need = need;
-    if (const char* sg = getenv("MFC_SEG")) c->seg = atoi(sg);
-    if (const char* xb = getenv("MFC_XBASE")) c->xbase = atoi(xb) != 0;
-    const char* segenv[3] = {"MFC_SEG_X", "MFC_SEG_Y", "MFC_SEG_Z"};
-    for (int k = 0; k < 3; ++k)
-        if (const char* sg = getenv(segenv[k])) c->seg_dir[k] = atoi(sg);
 
     // The device is only touched here when NCCL needs it; single-domain and loopback
     // contexts are pure host bookkeeping until the first GPU call (so layouts can be
@@ -1348,6 +1340,13 @@ int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
     if ((uintptr_t)p % 256) return fail(MFC_EINVAL, "workspace not 256-byte aligned");
     if (bytes < c->ws_need)
         return fail(MFC_ENOMEM, "workspace %zu < %zu bytes", bytes, c->ws_need);
+    if (c->fused)
+        return fail(MFC_ESTATE, "fused halo attached: the neighbours hold pointers into the "
+                                "bound stage buffers; rebinding is not allowed");
+    if (c->graph) {                  // the captured step reads and writes the old buffers
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
     c->ws = (char*)p;
     c->ws_bytes = bytes;
     char* w = c->ws;
@@ -1367,6 +1366,13 @@ int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
             c->recvb[f] = (double*)w; w += fb;
         }
     }
+    return MFC_OK;
+}
+
+int mfc_set_stream_chunks(mfc_ctx* c, int32_t chunks) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (chunks < -1) return fail(MFC_EINVAL, "chunks must be >= -1");
+    c->stream_chunks = chunks;
     return MFC_OK;
 }
 
@@ -1435,6 +1441,10 @@ static int eos(mfc_ctx* c, const double* in, double* out, bool to_cons, void* st
 
 int mfc_max_wave_rate(mfc_ctx* c, const double* q, double* d_out, void* stream) {
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (c->nranks > 1 && c->transport != MFC_TRANSPORT_NCCL)
+        return fail(MFC_EUNSUPPORTED, "max wave rate over %d ranks needs the NCCL transport "
+                                      "(loopback / peer contexts cannot reduce across ranks)",
+                    c->nranks);
     int st;
     if ((st = check_ptr(q, "q")) || (st = set_device(c))) return st;
     if (!d_out || ((uintptr_t)d_out) % 8) return fail(MFC_EINVAL, "d_out NULL or misaligned");

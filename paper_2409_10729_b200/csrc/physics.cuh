@@ -27,9 +27,6 @@
 #ifndef MFC_WENO5M_ALPHA
 #define MFC_WENO5M_ALPHA 1      // r101: C3 --weno 5m 10.322 -> 10.304 ms (3 reps; x +0.007, z -0.023)
 #endif
-#ifndef MFC_WENO_ONE_RCP_LEAN
-#define MFC_WENO_ONE_RCP_LEAN 0
-#endif
 #ifndef MFC_HLLC_ONE_RCP
 #define MFC_HLLC_ONE_RCP 1   // r96: x -0.015, y -0.01 ms per step (same box, 3 repetitions)
 #endif
@@ -208,21 +205,13 @@ __device__ __forceinline__ void weno5_d(double D0, double D1, double D2, double 
     const double xm2 = fma(2.0, D2, -0.5 * D3);
     const double Dm = fma(6.0, P1, fma(3.0, P2, P0));
     const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
-#if !MFC_WENO_ONE_RCP_LEAN
     vm = fma(Nm, rcp(Dm), c);
-#endif
     const double xp0 = fma(-2.0, D1, 0.5 * D0);
     const double xp1 = fma(-2.0, D1, -D2);
     const double xp2 = fma(k13, D3, -k56 * D2);
     const double Dp = fma(3.0, P0, fma(6.0, P1, P2));
     const double Np = fma(P2, xp2, fma(P1, xp1, P0 * xp0));
-#if MFC_WENO_ONE_RCP_LEAN
-    const double R = rcp(Dm * Dp);           // see weno5_fewop_s
-    vm = fma(Nm * Dp, R, c);
-    vp = fma(Np * Dm, R, c);
-#else
     vp = fma(Np, rcp(Dp), c);
-#endif
 }
 
 // WENO5-JS with two FP64 operations fewer per variable than weno5 (same beta'_k, t_k,

@@ -20,16 +20,14 @@
 // warp never waits on DRAM inside a step.
 //
 // Epilogues (compile-time MODE; w = cb*dt in RK stages, 1 for a plain RHS):
-//   M_SET   : dst = c                                 (x sweep: write-only)
-//   M_RKINIT: dst = ca*q^n + cb*q^s + w*c             (1D: the only sweep, RK stage)
-//   M_RKACC : dst = ca*q^n + cb*q^s + w*(acc + c)     (y sweep, RK stage)
-//   M_ACC   : dst = acc + w*c                         (y sweep of a RHS, z sweep)
+//   M_SET   : dst = c                                 (1D x sweep of a RHS: write-only)
+//   M_RKINIT: dst = ca*q^n + cb*q^s + w*c             (1D: the only sweep, RK stage; the
+//                                                      row-parallel x sweeps of 2D/3D)
+//   M_ACC   : dst = acc + w*c                         (y sweep, z sweep)
 //   M_ACCN  : dst = acc + w*c + ca*q^n                (last sweep of an RK stage when the
-//                                                      row-parallel x sweep wrote cb*q^s + w*c_x)
+//                                                      x sweep wrote cb*q^s + w*c_x only)
 // so the SSP-RK3 stage q^(s+1) = ca q^n + cb (q^s + dt (c_x + c_y + c_z)) (S4) is
-// assembled across the sweeps; the extra operands q^s, q^n are streamed by the y sweep,
-// whose warp accesses are contiguous rows, never by the x sweep, whose lanes own
-// different rows.
+// assembled across the sweeps.
 #pragma once
 #include "physics.cuh"
 
@@ -51,7 +49,7 @@
 
 namespace mfc {
 
-enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_RKACC = 3, M_ACCN = 4 };
+enum { M_SET = 0, M_RKINIT = 1, M_ACC = 2, M_ACCN = 4 };
 
 // Reconstruction of one variable of the window's centre cell (ORD = 5: cells w0..w4,
 // ORD = 6: the same with WENO5-M weights, ORD = 3: the inner three).
@@ -128,9 +126,9 @@ __device__ __forceinline__ void peer_copy(const PeerOut& po, int x, int y, int z
 
 struct SweepArgs {
     const double* __restrict__ q;   // stencil state (padded layout, ghosts filled)
-    const double* acc;              // accumulator input (M_ACC, M_RKACC)
+    const double* acc;              // accumulator input (M_ACC, M_ACCN)
     double* dst;                    // destination (state layout)
-    const double* qn;               // RK base state q^n (M_RKINIT/M_RKACC, read iff ca != 0)
+    const double* qn;               // RK base state q^n (M_RKINIT/M_ACCN, read iff ca != 0)
     int64_t sE;                     // equation stride
     int64_t sS, sA, sB;             // strides along the sweep, lane and third axis
     int64_t base;                   // offset of interior cell (0,0,0), equation 0
@@ -166,7 +164,7 @@ __host__ __device__ constexpr bool march_fewop() {
 // Per-thread shared-memory rings for the streamed operands (filled by cp.async PD
 // march steps ahead of use; element (slot, e) of thread t at [(slot*E + e)*nthreads + t],
 // so a warp's copies and reads are contiguous 256-byte rows):
-//   state ring : cells j+2 .. j+4 (RK y sweep: j-1 .. j+4, the stage operand q^s(j-1)
+//   state ring : cells j+2 .. j+4 (1D RK march: j-1 .. j+4, the stage operand q^s(j-1)
 //                is the state already streamed three steps earlier);
 //   acc / q^n rings : cells j-1 .. j+1.
 #ifndef MFC_RING_PD
@@ -175,12 +173,12 @@ __host__ __device__ constexpr bool march_fewop() {
 template <int MODE, int PD_>
 struct Rings {
     static constexpr int PD = PD_;
-    static constexpr bool RK = MODE == M_RKACC || MODE == M_RKINIT;
+    static constexpr bool RK = MODE == M_RKINIT;
     // state cell c lives from its fetch (step c-2-PD) to its conversion (step c-2), or
     // to its use as the stage operand q^s (step c+1); operands of cell c from step
     // c+1-PD to step c+1
     static constexpr int QS = RK ? PD + 4 : PD + 1;
-    static constexpr int AS = (MODE == M_ACC || MODE == M_RKACC || MODE == M_ACCN) ? PD + 1 : 0;
+    static constexpr int AS = (MODE == M_ACC || MODE == M_ACCN) ? PD + 1 : 0;
     static constexpr int NS = (RK || MODE == M_ACCN) ? PD + 1 : 0;
     static constexpr int OS = PD + 1;   // operand ring length (AS or NS when present)
     static constexpr int SLOTS = QS + AS + NS;
@@ -202,7 +200,7 @@ constexpr size_t sweep_smem_per_thread() { return (size_t)RingsOf<M, DIR, MODE>:
 // fold into instruction immediates): 128, or 64 where 12 ring slots of E > 9 doubles
 // would not leave room for two blocks per SM.
 template <class M, int MODE>
-__host__ __device__ constexpr int sweep_nth() { return ((MODE == M_RKACC || MODE == M_RKINIT) && M::E > 9) ? 64 : 128; }
+__host__ __device__ constexpr int sweep_nth() { return (MODE == M_RKINIT && M::E > 9) ? 64 : 128; }
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -410,9 +408,7 @@ sweep_kernel(const SweepArgs a) {
                         const double base = a.ca != 0.0
                                                 ? fma(a.ca, at(ringN, ka, e), a.cb * qs)
                                                 : a.cb * qs;
-                        out = MODE == M_RKACC
-                                  ? fma(a.w, fma(a.invd, r, at(ringA, ka, e)), base)
-                                  : fma(a.w * a.invd, r, base);
+                        out = fma(a.w * a.invd, r, base);
                     }
                     a.dst[c + e * a.sE] = out;
                 }
@@ -445,134 +441,6 @@ sweep_kernel(const SweepArgs a) {
         kaf = inc(kaf, R::OS);
     }
     cp_async_wait_all();
-}
-
-}  // namespace mfc
-
-namespace mfc {
-
-// ---------------------------------------------------------------------------
-// x sweep with shared-memory staging (2D/3D, epilogue M_SET).
-//
-// In the x sweep a warp's 32 lanes march along 32 different rows (consecutive y),
-// so a plain per-lane load touches 32 rows = 32 sectors per instruction.  Here each
-// warp moves its rows through shared memory in chunks of 4 cells (one 32-byte sector
-// per row): the warp copies a chunk [E][32 rows][4] with cp.async, 4 lanes per row
-// sector (each instruction = 8 full sectors), two chunks ahead of the march; the
-// lanes read their own row from it.  Results go to a chunk-sized output buffer and
-// leave as 8 full sectors per store instruction.  Layout inside a chunk buffer:
-// element (e, row, x) at (e*32 + row)*4 + (x ^ ((row >> 2) & 3)): the XOR swizzle
-// makes both the row-wise march reads and the sector-wise copies bank-conflict free.
-// Per warp: 2 input + 1 output chunk buffers = 3 * E * 1 KB of shared memory.
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ int swz(int row, int x) { return row * 4 + (x ^ ((row >> 2) & 3)); }
-
-template <class M, int ORD>
-__global__ void __launch_bounds__(128, 2)
-sweep_x_staged(const SweepArgs a) {
-    constexpr int E = M::E;
-    constexpr int CH = E * 128;                      // doubles per chunk buffer
-    extern __shared__ double smem[];
-    const int lane = threadIdx.x;                    // blockDim.x == 32
-    double* in0 = smem + threadIdx.y * 3 * CH;
-    double* in1 = in0 + CH;
-    double* outb = in1 + CH;
-    const int row0 = blockIdx.x * 32;                // first row (y) of this warp
-    const int ib = blockIdx.y * blockDim.y + threadIdx.y;
-    if (ib >= a.nB) return;                          // whole warp
-    const int s0 = blockIdx.z * a.T;                 // T is a multiple of 4
-    const int s1 = min(s0 + a.T, a.nS);
-    const int64_t plane = a.base + (int64_t)ib * a.sB;   // row row0+r, cell s: plane + (row0+r)*sA + s
-    const int crow = lane >> 2, cx = lane & 3;       // copy geometry: 8 rows x 4 cells
-    const int nrows = min(32, a.nA - row0);
-
-    // chunk K holds cells 4K-4 .. 4K-1 (padded x index 4K .. 4K+3; 32-byte aligned)
-    auto issue = [&](int K, double* dst) {
-        const double* src = a.q + plane + (int64_t)(row0 + crow) * a.sA + map_cell(4 * K - 4 + cx, a.nS, a.gm);
-#pragma unroll 1
-        for (int e = 0; e < E; ++e) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                if (8 * i + crow < nrows)
-                    cp_async8(dst + e * 128 + swz(8 * i + crow, cx), src + (int64_t)(8 * i) * a.sA);
-            }
-            src += a.sE;
-        }
-        cp_async_commit();
-    };
-    const int Klast = (s1 + 6) >> 2;
-    auto convert = [&](int x, double (&v)[E]) {     // cell x of my row -> primitives
-        const int K = (x + 4) >> 2;
-        double* b = (K & 1) ? in1 : in0;
-        if (((x + 4) & 3) == 0 || x == s0 - 3) {      // first use of chunk K
-            cp_async_wait_all();
-            __syncwarp();
-            if (K + 1 <= Klast) issue(K + 1, ((K + 1) & 1) ? in1 : in0);
-        }
-        double qc[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) qc[e] = b[e * 128 + swz(lane, (x + 4) & 3)];
-        if (map_flip(x, a.nS, a.gm)) qc[M::IM] = -qc[M::IM];
-        cons_to_prim_fast<M>(qc, v, a.mat);
-    };
-    auto flush = [&](int K) {                        // store output chunk K (cells 4K-4..4K-1)
-        __syncwarp();
-        const int xc = 4 * K - 4 + cx;
-        if (xc >= s0 && xc < s1) {
-            double* dst = a.dst + plane + (int64_t)(row0 + crow) * a.sA + xc;
-#pragma unroll 1
-            for (int e = 0; e < E; ++e) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    if (8 * i + crow < nrows)
-                        dst[(int64_t)(8 * i) * a.sA] = outb[e * 128 + swz(8 * i + crow, cx)];
-                }
-                dst += a.sE;
-            }
-        }
-        __syncwarp();
-    };
-
-    issue((s0 + 1) >> 2, (((s0 + 1) >> 2) & 1) ? in1 : in0);
-    double w[5][E];
-#pragma unroll
-    for (int k = 1; k < 5; ++k) convert(s0 - 4 + k, w[k]);
-
-    double vm_prev[E], F_prev[E];
-    double uf_prev = 0.0;
-    for (int j = s0 - 1; j <= s1; ++j) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) w[k][e] = w[k + 1][e];
-        }
-        convert(j + 2, w[4]);
-        double vm[E], vp[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-            reconstruct<ORD, MFC_MARCH_FEWOP>(w[0][e], w[1][e], w[2][e], w[3][e], w[4][e], a.eps4, a.eps, vm[e], vp[e]);
-        if (j >= s0) {
-            double F[E], uf;
-            hllc<M, 0>(vm_prev, vp, a.mat, F, uf);
-            if (j > s0) {
-                const int x = j - 1;
-                const double du = uf - uf_prev;
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    double r = F_prev[e] - F[e];
-                    if (e >= M::IA) r = fma(w[1][e], du, r);
-                    outb[e * 128 + swz(lane, (x + 4) & 3)] = r * a.invd;
-                }
-                if (((x + 4) & 3) == 3 || x == s1 - 1) flush((x + 4) >> 2);
-            }
-#pragma unroll
-            for (int e = 0; e < E; ++e) F_prev[e] = F[e];
-            uf_prev = uf;
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) vm_prev[e] = vm[e];
-    }
 }
 
 }  // namespace mfc

@@ -66,115 +66,97 @@ __global__ void __launch_bounds__(256) wave_rate_kernel(const EosArgs a, double3
     if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(red[0]));
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: raise it for
+// the current device whenever a launch needs more than that device has been given
+// (a success is recorded per device; a failure is returned, never cached)
+template <class K>
+static int set_smem_attr(K* kernel, size_t smem) {
+    constexpr int kMaxDev = 64;
+    static size_t done[kMaxDev] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    if (dev < 0 || dev >= kMaxDev) return (int)cudaErrorInvalidDevice;
+    if (smem <= 48 * 1024 || smem <= done[dev]) return 0;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    done[dev] = smem;
+    return 0;
+}
+
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
-static void launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
+static cudaError_t launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     constexpr int NTH = sweep_nth<M, MODE>();
     b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
     const int64_t warp_lines = (int64_t)((a.nA + 31) / 32) * a.nB;
     g = dim3((unsigned)((warp_lines + b.y - 1) / b.y), 1, g.z);
     const size_t smem = sweep_smem_per_thread<M, DIR, MODE>() * NTH;
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(sweep_kernel<M, DIR, MODE, ORD, PEER>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    const int st = set_smem_attr(sweep_kernel<M, DIR, MODE, ORD, PEER>, smem);
+    if (st) return (cudaError_t)st;
     sweep_kernel<M, DIR, MODE, ORD, PEER><<<g, b, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 template <class M, int DIR, int ORD>
 static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
-    if constexpr (DIR == 0) {
-        if (mode == M_SET || (mode == M_RKINIT && M::D >= 2)) {
-            if constexpr (M::D >= 2) {
-              // row-parallel tile kernel (rows longer than 256 cells: several 8-warp
-              // segments with boundary cells); MFC_X_STAGED: the staged march.
-              // The host asks x_rows_used() before choosing M_RKINIT (tile kernel only).
-              static const bool xpair = !(getenv("MFC_XPAIR") && atoi(getenv("MFC_XPAIR")) == 0);
-              if (ORD == 5 && xpair && x_rows_used(a.nS)) {
-                // two cells per thread (sweep_x_pair): W <= 4 warps, 64 W cells per block
-                // (MFC_XPAIR_W=2: 128-cell segments, C3 x 2.15 -> 2.28 ms per step, r93)
-                static const int wmaxp = getenv("MFC_XPAIR_W") ? atoi(getenv("MFC_XPAIR_W")) : 4;
-                const int W = (int)std::min<int64_t>(wmaxp, (a.nS + 63) / 64);
-                const int nseg = (a.nS + 64 * W - 1) / (64 * W);
-                const size_t smem = sizeof(double) * x_pair_smem_doubles<M>(64 * W);
-                static size_t attr = 0;
-                if (smem > attr) {
-                    cudaFuncSetAttribute(sweep_x_pair<M, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    cudaFuncSetAttribute(sweep_x_pair<M, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    attr = smem;
-                }
-                const dim3 gr(nseg, a.nA, a.nB);
-                if (mode == M_SET) sweep_x_pair<M, false><<<gr, 32 * W, smem, s>>>(a, W);
-                else sweep_x_pair<M, true><<<gr, 32 * W, smem, s>>>(a, W);
-              } else if (x_rows_used(a.nS)) {
-                static const int wmax = getenv("MFC_XTILE_W") ? atoi(getenv("MFC_XTILE_W")) : 8;
-                const int W = (int)std::min<int64_t>(wmax, (a.nS + 31) / 32);
-                const int nseg = (a.nS + 32 * W - 1) / (32 * W);
-                const size_t smem = sizeof(double) * x_tile_smem_doubles<M>(32 * W);
-                static size_t attr = 0;
-                if (smem > attr) {
-                    cudaFuncSetAttribute(sweep_x_tile<M, ORD, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    cudaFuncSetAttribute(sweep_x_tile<M, ORD, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    attr = smem;
-                }
-                const dim3 gr(nseg, a.nA, a.nB);
-                if (mode == M_SET) sweep_x_tile<M, ORD, false><<<gr, 32 * W, smem, s>>>(a, W);
-                else sweep_x_tile<M, ORD, true><<<gr, 32 * W, smem, s>>>(a, W);
-              } else if (mode == M_SET) {
-                // shared-memory staged x sweep: 3 chunk buffers of E*128 doubles per warp
-                const size_t smem = (size_t)b.y * 3 * M::E * 128 * sizeof(double);
-                static size_t attr = 0;
-                if (smem > attr) {
-                    cudaFuncSetAttribute(sweep_x_staged<M, ORD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    attr = smem;
-                }
-                sweep_x_staged<M, ORD><<<g, b, smem, s>>>(a);
-              } else {
-                return cudaErrorInvalidValue;
-              }
-            } else {
-                launch_ring<M, DIR, M_SET, ORD>(a, g, b, s);
-            }
-        } else if (mode == M_RKINIT) {
-            if constexpr (M::D == 1) {
-                if (a.po.nf) launch_ring<M, DIR, M_RKINIT, ORD, true>(a, g, b, s);
-                else launch_ring<M, DIR, M_RKINIT, ORD>(a, g, b, s);
-            } else {
-                return cudaErrorInvalidValue;
-            }
+    if constexpr (DIR == 0 && M::D >= 2) {
+        // row-parallel x sweeps (RHS: M_SET, RK stage: M_RKINIT = the stage base cb*q^s
+        // (+ ca*q^n when a.qn is set) + w*c_x)
+        if (mode != M_SET && mode != M_RKINIT) return cudaErrorInvalidValue;
+        if constexpr (ORD == 5) {
+            // two cells per thread (sweep_x_pair): W <= 4 warps, 64 W cells per block
+            // (128-cell segments: C3 x 2.15 -> 2.28 ms per step, r93)
+            const int W = (int)std::min<int64_t>(4, (a.nS + 63) / 64);
+            const int nseg = (a.nS + 64 * W - 1) / (64 * W);
+            const size_t smem = sizeof(double) * x_pair_smem_doubles<M>(64 * W);
+            int st;
+            if ((st = set_smem_attr(sweep_x_pair<M, false>, smem)) ||
+                (st = set_smem_attr(sweep_x_pair<M, true>, smem)))
+                return (cudaError_t)st;
+            const dim3 gr(nseg, a.nA, a.nB);
+            if (mode == M_SET) sweep_x_pair<M, false><<<gr, 32 * W, smem, s>>>(a, W);
+            else sweep_x_pair<M, true><<<gr, 32 * W, smem, s>>>(a, W);
         } else {
-            return cudaErrorInvalidValue;
+            // one cell per thread (sweep_x_tile): WENO3, WENO5-M; rows longer than 256
+            // cells run as several 8-warp segments with boundary cells
+            const int W = (int)std::min<int64_t>(8, (a.nS + 31) / 32);
+            const int nseg = (a.nS + 32 * W - 1) / (32 * W);
+            const size_t smem = sizeof(double) * x_tile_smem_doubles<M>(32 * W);
+            int st;
+            if ((st = set_smem_attr(sweep_x_tile<M, ORD, false>, smem)) ||
+                (st = set_smem_attr(sweep_x_tile<M, ORD, true>, smem)))
+                return (cudaError_t)st;
+            const dim3 gr(nseg, a.nA, a.nB);
+            if (mode == M_SET) sweep_x_tile<M, ORD, false><<<gr, 32 * W, smem, s>>>(a, W);
+            else sweep_x_tile<M, ORD, true><<<gr, 32 * W, smem, s>>>(a, W);
         }
+    } else if constexpr (DIR == 0) {
+        // 1D: the march is the only sweep (RHS: M_SET, RK stage: M_RKINIT)
+        if (mode == M_SET) {
+            if (a.po.nf) return cudaErrorInvalidValue;
+            return launch_ring<M, DIR, M_SET, ORD>(a, g, b, s);
+        }
+        if (mode != M_RKINIT) return cudaErrorInvalidValue;
+        if (a.po.nf) return launch_ring<M, DIR, M_RKINIT, ORD, true>(a, g, b, s);
+        return launch_ring<M, DIR, M_RKINIT, ORD>(a, g, b, s);
     } else {
-        if (mode == M_ACC && a.po.nf) {
-            if constexpr (DIR == M::D - 1) launch_ring<M, DIR, M_ACC, ORD, true>(a, g, b, s);
-            else return cudaErrorInvalidValue;   // only the last sweep writes a stage
-        } else if (mode == M_ACC) launch_ring<M, DIR, M_ACC, ORD>(a, g, b, s);
-        else if (mode == M_ACCN) {
-            if constexpr (DIR == M::D - 1) {
-                if (a.po.nf) launch_ring<M, DIR, M_ACCN, ORD, true>(a, g, b, s);
-                else launch_ring<M, DIR, M_ACCN, ORD>(a, g, b, s);
-            } else {
+        // y / z marches; only the last sweep of a stage writes a stage result and may
+        // carry the fused halo stores (PEER)
+        constexpr bool last = DIR == M::D - 1;
+        if (mode == M_ACC) {
+            if (a.po.nf) {
+                if constexpr (last) return launch_ring<M, DIR, M_ACC, ORD, true>(a, g, b, s);
                 return cudaErrorInvalidValue;
             }
+            return launch_ring<M, DIR, M_ACC, ORD>(a, g, b, s);
         }
-        else if (DIR == 1 && mode == M_RKACC) {
-            // 2D RK stage: the y sweep is the last one and may carry the fused halo
-            if constexpr (M::D == 2) {
-                if (a.po.nf) launch_ring<M, DIR, M_RKACC, ORD, true>(a, g, b, s);
-                else launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
-            } else {
-                if (a.po.nf) return cudaErrorInvalidValue;
-                launch_ring<M, DIR, M_RKACC, ORD>(a, g, b, s);
+        if (mode == M_ACCN) {
+            if constexpr (last) {
+                if (a.po.nf) return launch_ring<M, DIR, M_ACCN, ORD, true>(a, g, b, s);
+                return launch_ring<M, DIR, M_ACCN, ORD>(a, g, b, s);
             }
         }
-        else return cudaErrorInvalidValue;
+        return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }

@@ -33,7 +33,7 @@ EXPORTED = [
     "mfc_set_weno_order", "mfc_set_weno_mapped",
     "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
     "mfc_rk3_steps", "mfc_max_wave_rate", "mfc_cfl_dt",
-    "mfc_advance_host", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
+    "mfc_advance_host", "mfc_set_stream_chunks", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
     "mfc_fused_halo_group", "mfc_peer_export", "mfc_peer_import",
     "mfc_nccl_get_unique_id", "mfc_last_launch_count", "mfc_profile_enable", "mfc_profile_read", "mfc_finalize", "mfc_last_error",
     "mfc_version",
@@ -88,6 +88,7 @@ def _load():
         "mfc_max_wave_rate": [vp, vp, vp, vp],
         "mfc_cfl_dt": [vp, vp, dbl, ctypes.POINTER(dbl), vp, vp],
         "mfc_advance_host": [vp, vp, vp, vp, i64, dbl, vp],
+        "mfc_set_stream_chunks": [vp, i32],
         "mfc_halo_exchange_group": [pp, pp, i32, vp],
         "mfc_rhs_group": [pp, pp, pp, i32, vp],
         "mfc_rk3_step_group": [pp, pp, i32, dbl, vp],
@@ -150,7 +151,9 @@ def _stream(stream=None):
 
 
 def _ptr(t: torch.Tensor):
-    assert t.dtype == torch.float64 and t.is_cuda
+    """Device pointer of a float64 CUDA tensor (raises, never asserts: python -O)."""
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
+        raise ValueError("expected a float64 CUDA tensor")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -243,29 +246,44 @@ class Solver:
         return q
 
     # ------------------------------------------------------------- calls
+    def _sp(self, t: torch.Tensor):
+        """Pointer of a state buffer: float64, on this solver's device, contiguous and
+        holding at least layout.n_elems elements (the kernels index that far)."""
+        p = _ptr(t)
+        if t.device != self.device:
+            raise ValueError(f"state on {t.device}, solver on {self.device}")
+        if not t.is_contiguous() or t.numel() < self.layout.n_elems:
+            raise ValueError(f"state buffer needs >= {self.layout.n_elems} contiguous float64 "
+                             f"elements (got {t.numel()})")
+        return p
+
     def prim_to_cons(self, v, q, stream=None):
-        _check(lib.mfc_prim_to_cons(self._h, _ptr(v), _ptr(q), _stream(stream)), "mfc_prim_to_cons")
+        _check(lib.mfc_prim_to_cons(self._h, self._sp(v), self._sp(q), _stream(stream)),
+               "mfc_prim_to_cons")
 
     def cons_to_prim(self, q, v, stream=None):
-        _check(lib.mfc_cons_to_prim(self._h, _ptr(q), _ptr(v), _stream(stream)), "mfc_cons_to_prim")
+        _check(lib.mfc_cons_to_prim(self._h, self._sp(q), self._sp(v), _stream(stream)),
+               "mfc_cons_to_prim")
 
     def halo_exchange(self, q, stream=None):
-        _check(lib.mfc_halo_exchange(self._h, _ptr(q), _stream(stream)), "mfc_halo_exchange")
+        _check(lib.mfc_halo_exchange(self._h, self._sp(q), _stream(stream)), "mfc_halo_exchange")
 
     def rhs(self, q, out=None, stream=None) -> torch.Tensor:
         if out is None:
             out = self.empty_state()
-        _check(lib.mfc_rhs(self._h, _ptr(q), _ptr(out), _stream(stream)), "mfc_rhs")
+        _check(lib.mfc_rhs(self._h, self._sp(q), self._sp(out), _stream(stream)), "mfc_rhs")
         return out
 
     def rk3_step(self, q, dt: float, stream=None):
-        _check(lib.mfc_rk3_step(self._h, _ptr(q), float(dt), _stream(stream)), "mfc_rk3_step")
+        _check(lib.mfc_rk3_step(self._h, self._sp(q), float(dt), _stream(stream)), "mfc_rk3_step")
 
     def max_wave_rate(self, q, out=None, stream=None) -> torch.Tensor:
         """Device scalar: max over cells (and ranks) of max_k (|u_k|+c)/dx_k."""
         if out is None:
             out = torch.zeros(1, dtype=torch.float64, device=self.device)
-        _check(lib.mfc_max_wave_rate(self._h, _ptr(q), _ptr(out), _stream(stream)),
+        if out.device != self.device or out.numel() < 1:
+            raise ValueError("out must be a float64 tensor on the solver's device")
+        _check(lib.mfc_max_wave_rate(self._h, self._sp(q), _ptr(out), _stream(stream)),
                "mfc_max_wave_rate")
         return out
 
@@ -273,23 +291,34 @@ class Solver:
         """dt = cfl / max_wave_rate (synchronises the stream)."""
         scratch = torch.zeros(1, dtype=torch.float64, device=self.device)
         dt = ctypes.c_double(0.0)
-        _check(lib.mfc_cfl_dt(self._h, _ptr(q), float(cfl), ctypes.byref(dt), _ptr(scratch),
+        _check(lib.mfc_cfl_dt(self._h, self._sp(q), float(cfl), ctypes.byref(dt), _ptr(scratch),
                               _stream(stream)), "mfc_cfl_dt")
         return dt.value
 
     def rk3_steps(self, q, dt: float, nsteps: int, stream=None):
         """nsteps RK3 steps replayed from a CUDA graph of one step."""
-        _check(lib.mfc_rk3_steps(self._h, _ptr(q), float(dt), int(nsteps), _stream(stream)),
+        _check(lib.mfc_rk3_steps(self._h, self._sp(q), float(dt), int(nsteps), _stream(stream)),
                "mfc_rk3_steps")
 
     def advance_host(self, q_in: torch.Tensor, q_out: torch.Tensor, q_dev: torch.Tensor,
                      nsteps: int, dt: float, stream=None):
-        """End-to-end call with host buffers (dense interior (E, nz, ny, nx) float64)."""
-        assert q_in.device.type == "cpu" and q_out.device.type == "cpu"
-        assert q_in.is_contiguous() and q_out.is_contiguous()
+        """End-to-end call with host buffers (dense interior (E, nz, ny, nx) float64);
+        q_dev (a state buffer on the device) holds the result afterwards as well."""
+        L = self.layout
+        need = L.E * L.n_local[0] * L.n_local[1] * L.n_local[2]
+        for name, t in (("q_in", q_in), ("q_out", q_out)):
+            if not isinstance(t, torch.Tensor) or t.device.type != "cpu":
+                raise ValueError(f"{name} must be a host tensor")
+            if t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != need:
+                raise ValueError(f"{name} must be a contiguous float64 host tensor of "
+                                 f"E*nx*ny*nz = {need} elements (got {t.dtype}, {t.numel()})")
         _check(lib.mfc_advance_host(self._h, ctypes.c_void_p(q_in.data_ptr()),
-                                    ctypes.c_void_p(q_out.data_ptr()), _ptr(q_dev),
+                                    ctypes.c_void_p(q_out.data_ptr()), self._sp(q_dev),
                                     int(nsteps), float(dt), _stream(stream)), "mfc_advance_host")
+
+    def set_stream_chunks(self, chunks: int):
+        """Chunk count of the streamed one-step advance_host (0: off, -1: default)."""
+        _check(lib.mfc_set_stream_chunks(self._h, int(chunks)), "mfc_set_stream_chunks")
 
     KINDS = ("sweep_x", "sweep_y", "sweep_z", "bc_fill", "halo", "eos")
 
@@ -307,7 +336,7 @@ class Solver:
     def peer_export(self, q) -> bytes:
         """CUDA-IPC handles of q, the RK stage buffers and the flags (mfc_peer_export)."""
         buf = ctypes.create_string_buffer(PEER_BLOB_BYTES)
-        _check(lib.mfc_peer_export(self._h, _ptr(q), buf), "mfc_peer_export")
+        _check(lib.mfc_peer_export(self._h, self._sp(q), buf), "mfc_peer_export")
         return buf.raw
 
     def peer_import(self, face: int, blob: bytes):
@@ -380,21 +409,21 @@ def _arr(objs):
 def rk3_step_group(solvers, qs, dt, stream=None):
     """Loopback group step: len(solvers) subdomains on one GPU (comm.loopback = 1)."""
     hs = _arr([s._h.value for s in solvers])
-    ps = _arr([q.data_ptr() for q in qs])
+    ps = _arr([s._sp(q).value for s, q in zip(solvers, qs)])
     _check(lib.mfc_rk3_step_group(hs, ps, len(solvers), float(dt), _stream(stream)),
            "mfc_rk3_step_group")
 
 
 def rhs_group(solvers, qs, outs, stream=None):
     hs = _arr([s._h.value for s in solvers])
-    ps = _arr([q.data_ptr() for q in qs])
-    os_ = _arr([o.data_ptr() for o in outs])
+    ps = _arr([s._sp(q).value for s, q in zip(solvers, qs)])
+    os_ = _arr([s._sp(o).value for s, o in zip(solvers, outs)])
     _check(lib.mfc_rhs_group(hs, ps, os_, len(solvers), _stream(stream)), "mfc_rhs_group")
 
 
 def halo_exchange_group(solvers, qs, stream=None):
     hs = _arr([s._h.value for s in solvers])
-    ps = _arr([q.data_ptr() for q in qs])
+    ps = _arr([s._sp(q).value for s, q in zip(solvers, qs)])
     _check(lib.mfc_halo_exchange_group(hs, ps, len(solvers), _stream(stream)),
            "mfc_halo_exchange_group")
 
@@ -409,5 +438,5 @@ def fused_halo_group(solvers, qs):
     """Loopback group: the stage sweeps write the group members' ghost layers directly
     (mfc_fused_halo_group); qs become the registered state buffers."""
     hs = _arr([s._h.value for s in solvers])
-    ps = _arr([q.data_ptr() for q in qs])
+    ps = _arr([s._sp(q).value for s, q in zip(solvers, qs)])
     _check(lib.mfc_fused_halo_group(hs, ps, len(solvers)), "mfc_fused_halo_group")

@@ -41,14 +41,30 @@ CASES = [
 ]
 
 
+def _fresh_solver(pb, chunks=None):
+    """A solver whose workspace holds NaN: a streamed step that read a stage buffer
+    before the wavefront wrote it would propagate NaN into the result (ADVICE r1:
+    reference steps on the SAME solver left a correct S2 behind and hid exactly that)."""
+    from paper_2409_10729_b200.mfc import Solver
+    s = Solver(pb)
+    s.workspace.fill_(float("nan"))
+    if chunks is not None:
+        s.set_stream_chunks(chunks)
+    return s
+
+
+def _reference(pb, q, dt, n=1):
+    from paper_2409_10729_b200.mfc import Solver
+    return _device_steps(Solver(pb), q, dt, n)
+
+
 @pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
 def test_advance_host_streamed_bitwise(name, make):
-    from paper_2409_10729_b200.mfc import Solver
     pb = make()
     _, v, q = oracle_inputs(pb)
     dt = stable_dt(pb, v)
-    s = Solver(pb)
-    ref = _device_steps(s, q, dt, 1)
+    ref = _reference(pb, q, dt)                  # another context: nothing shared
+    s = _fresh_solver(pb)
     q_in, q_out = _host(q), _host(np.zeros_like(q))
     qdev = s.empty_state()
     s.advance_host(q_in, q_out, qdev, 1, dt)
@@ -57,9 +73,14 @@ def test_advance_host_streamed_bitwise(name, make):
     assert np.array_equal(s.interior(qdev).cpu().numpy(), ref)   # result left in q_dev
     got = q_out.numpy()
     assert np.array_equal(got, ref), np.abs(got - ref).max()
-    # in place, and a second call on the same context
+    # in place, and a second call on the same context (stage buffers now hold the first
+    # call's values, which must not leak either): the second step from q^1
+    ref2 = _reference(pb, ref, dt)
+    s.workspace.fill_(float("nan"))
     s.advance_host(q_in, q_in, qdev, 1, dt)
     assert np.array_equal(q_in.numpy(), ref)
+    s.advance_host(q_in, q_in, qdev, 1, dt)
+    assert np.array_equal(q_in.numpy(), ref2)
     # the step itself against the oracle
     P = O.Problem.from_spec(pb)
     want = O.rk3_step(P, q, dt)
@@ -92,28 +113,32 @@ def test_advance_host_small_grid_unstreamed():
     assert np.array_equal(q_out.numpy(), ref)
 
 
-@pytest.mark.parametrize("chunks", [3, 7, 40])
-def test_advance_host_chunk_counts(chunks):
-    # MFC_STREAM (chunk count) is read once per process: each case in a subprocess;
-    # 45 planes -> chunks of 15 / 7 (+ a short last one) / 3 planes
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = (
-        "import numpy as np, torch, sys; sys.path.insert(0, 'tests');"
-        "from paper_2409_10729_b200.mfc import Solver;"
-        "from paper_2409_10729_b200 import workloads as W;"
-        "from parity import oracle_inputs, stable_dt;"
-        "pb = W.random_problem(3, (20, 12, 45), 2, 'water', bc=(W.BC_EXTRAPOLATION,"
-        " W.BC_REFLECTIVE, W.BC_PERIODIC, W.BC_PERIODIC, W.BC_PERIODIC, W.BC_PERIODIC));"
-        "_, v, q = oracle_inputs(pb); dt = stable_dt(pb, v); s = Solver(pb);"
-        "qd = s.state_from_cons(q); s.rk3_step(qd, dt); torch.cuda.synchronize();"
-        "ref = s.interior(qd).cpu().numpy();"
-        "qi = torch.as_tensor(q).pin_memory(); qo = torch.empty_like(qi).pin_memory();"
-        "s.advance_host(qi, qo, s.empty_state(), 1, dt);"
-        "assert s.last_launch_count() > 9; assert np.array_equal(qo.numpy(), ref); print('ok')")
-    env = dict(os.environ, MFC_STREAM=str(chunks))
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                       cwd=root)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+@pytest.mark.parametrize("zbc", [W.BC_PERIODIC, W.BC_REFLECTIVE])
+@pytest.mark.parametrize("chunks", [3, 4, 7, 40])
+def test_advance_host_chunk_counts(chunks, zbc):
+    """45 planes -> chunks of 15 / ~11 / 7 (+ a short last one) / 3 planes; fresh
+    (NaN-poisoned) workspace every time; periodic z closes the wavefront ring."""
+    pb = W.random_problem(3, (20, 12, 45), 2, "water",
+                          bc=(W.BC_EXTRAPOLATION, W.BC_REFLECTIVE, W.BC_PERIODIC, W.BC_PERIODIC,
+                              zbc, zbc))
+    _, v, q = oracle_inputs(pb)
+    dt = stable_dt(pb, v)
+    ref = _reference(pb, q, dt)
+    s = _fresh_solver(pb, chunks)
+    qi, qo = _host(q), _host(np.zeros_like(q))
+    s.advance_host(qi, qo, s.empty_state(), 1, dt)
+    assert s.last_launch_count() > 9
+    assert np.array_equal(qo.numpy(), ref), np.abs(qo.numpy() - ref).max()
+
+
+def test_advance_host_rejects_bad_host_buffers():
+    from paper_2409_10729_b200.mfc import Solver
+    pb = W.random_problem(3, (16, 12, 9), 2, "gas")
+    s = Solver(pb)
+    good = torch.zeros(pb.shape, dtype=torch.float64)
+    with pytest.raises(ValueError):
+        s.advance_host(good.float(), good, s.empty_state(), 1, 1e-6)
+    with pytest.raises(ValueError):
+        s.advance_host(good[:, :-1].contiguous(), good, s.empty_state(), 1, 1e-6)
+    with pytest.raises(ValueError):
+        s.advance_host(good, good, s.empty_state()[:-1], 1, 1e-6)

@@ -288,6 +288,134 @@ double orc_weno3_plus(double a, double b, double c, double eps, double* weights)
     return weno3_combine(beta, dk, p, eps, weights);
 }
 
+/* ------------------------------------------- S3 WENO5, non-uniform grid (F4) */
+
+/* t^k by repeated multiplication. */
+static double ipow(double t, int k) {
+    double r = 1.0;
+    for (int i = 0; i < k; ++i) r = r * t;
+    return r;
+}
+
+/* Average of t^i over the interval [tl, tr]: (tr^(i+1) - tl^(i+1)) / ((i+1)(tr - tl)). */
+static double avg_pow(double tl, double tr, int i) {
+    return (ipow(tr, i + 1) - ipow(tl, i + 1)) / ((double)(i + 1) * (tr - tl));
+}
+
+/* Solve A X = B in place (A n x n row-major, B n x nrhs row-major) by Gaussian
+ * elimination with partial pivoting; X overwrites B. */
+static void gauss_solve(int n, double* A, double* B, int nrhs) {
+    for (int k = 0; k < n; ++k) {
+        int piv = k;
+        for (int r = k + 1; r < n; ++r)
+            if (fabs(A[r * n + k]) > fabs(A[piv * n + k])) piv = r;
+        if (piv != k) {
+            for (int c = 0; c < n; ++c) {
+                const double t = A[k * n + c];
+                A[k * n + c] = A[piv * n + c];
+                A[piv * n + c] = t;
+            }
+            for (int c = 0; c < nrhs; ++c) {
+                const double t = B[k * nrhs + c];
+                B[k * nrhs + c] = B[piv * nrhs + c];
+                B[piv * nrhs + c] = t;
+            }
+        }
+        for (int r = k + 1; r < n; ++r) {
+            const double f = A[r * n + k] / A[k * n + k];
+            for (int c = k; c < n; ++c) A[r * n + c] = A[r * n + c] - f * A[k * n + c];
+            for (int c = 0; c < nrhs; ++c) B[r * nrhs + c] = B[r * nrhs + c] - f * B[k * nrhs + c];
+        }
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        for (int c = 0; c < nrhs; ++c) {
+            double acc = B[k * nrhs + c];
+            for (int j = k + 1; j < n; ++j) acc = acc - A[k * n + j] * B[j * nrhs + c];
+            B[k * nrhs + c] = acc / A[k * n + k];
+        }
+    }
+}
+
+/* DESIGN.md AMB-27 ("local mesh refinement ... hyperbolic tangent
+ * function"): the WENO5-JS ingredients of cell m on a non-uniform grid, from their
+ * definitions in the local coordinate t = (x - x_m)/Δ_m (see mfc_oracle.h). */
+int32_t orc_nu_cell_coeffs(const double* xb6, orc_nu_cell* out) {
+    const double w = xb6[3] - xb6[2];                 /* Δ_m */
+    const double xm = 0.5 * (xb6[2] + xb6[3]);        /* centre of cell m */
+    double t[6];                                      /* boundaries in local coordinates */
+    for (int j = 0; j < 6; ++j) t[j] = (xb6[j] - xm) / w;
+    out->w = w;
+    /* candidates: (a, b, c) = M[k] v, M[k] = A_k^{-1}, A_k[j][i] = avg_{cell m-2+k+j} t^i */
+    for (int k = 0; k < 3; ++k) {
+        double A[9], B[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        for (int j = 0; j < 3; ++j)
+            for (int i = 0; i < 3; ++i) A[j * 3 + i] = avg_pow(t[k + j], t[k + j + 1], i);
+        gauss_solve(3, A, B, 3);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) out->M[k][i][j] = B[i * 3 + j];
+    }
+    /* ideal weights at t_f = +1/2 (v-) and -1/2 (v+): the degree-4 reconstruction
+     * weights R (A5^T R = (1, t_f, .., t_f^4)) against the candidates' weights
+     * r^(k)_j = sum_i t_f^i M[k][i][j] on their outermost cells */
+    for (int side = 0; side < 2; ++side) {
+        const double tf = side == 0 ? 0.5 : -0.5;
+        double A5t[25], R[5];
+        for (int j = 0; j < 5; ++j)
+            for (int i = 0; i < 5; ++i) A5t[i * 5 + j] = avg_pow(t[j], t[j + 1], i);
+        for (int i = 0; i < 5; ++i) R[i] = ipow(tf, i);
+        gauss_solve(5, A5t, R, 1);
+        double r0 = 0.0, r2 = 0.0;                    /* r^(0)_{m-2}, r^(2)_{m+2} */
+        for (int i = 0; i < 3; ++i) {
+            r0 = r0 + ipow(tf, i) * out->M[0][i][0];
+            r2 = r2 + ipow(tf, i) * out->M[2][i][2];
+        }
+        double* d = side == 0 ? out->dm : out->dp;
+        d[0] = R[0] / r0;
+        d[2] = R[4] / r2;
+        d[1] = (1.0 - d[0]) - d[2];
+    }
+    for (int k = 0; k < 3; ++k)
+        if (!(out->dm[k] > 0.0) || !(out->dp[k] > 0.0)) return -1;
+    return 0;
+}
+
+/* β_k = b² + (13/3)c² and q_k(t_f) of the three candidates of cell m. */
+static void weno5nu_parts(const orc_nu_cell* C, const double v[5], double tf, double beta[3],
+                          double p[3]) {
+    for (int k = 0; k < 3; ++k) {
+        double abc[3];
+        for (int i = 0; i < 3; ++i)
+            abc[i] = (C->M[k][i][0] * v[k] + C->M[k][i][1] * v[k + 1]) + C->M[k][i][2] * v[k + 2];
+        beta[k] = abc[1] * abc[1] + (13.0 / 3.0) * (abc[2] * abc[2]);
+        p[k] = (abc[0] + abc[1] * tf) + abc[2] * (tf * tf);
+    }
+}
+
+double orc_weno5nu_minus(const orc_nu_cell* C, double a, double b, double c, double d, double e,
+                         double eps, double* weights) {
+    const double v[5] = {a, b, c, d, e};
+    double beta[3], p[3];
+    weno5nu_parts(C, v, 0.5, beta, p);
+    return weno5_combine(beta, C->dm, p, eps, weights);
+}
+
+double orc_weno5nu_plus(const orc_nu_cell* C, double a, double b, double c, double d, double e,
+                        double eps, double* weights) {
+    const double v[5] = {a, b, c, d, e};
+    double beta[3], p[3];
+    weno5nu_parts(C, v, -0.5, beta, p);
+    return weno5_combine(beta, C->dp, p, eps, weights);
+}
+
+/* Coefficients of cells -1 .. n of axis dir (index m+1), or NULL on a uniform axis. */
+static orc_nu_cell* nu_axis(const orc_problem* P, int dir) {
+    if (!P->xb[dir]) return NULL;
+    const int64_t n = P->n[dir];
+    orc_nu_cell* C = (orc_nu_cell*)malloc(sizeof(orc_nu_cell) * (size_t)(n + 2));
+    for (int64_t m = -1; m <= n; ++m) orc_nu_cell_coeffs(P->xb[dir] + (m + 1), C + (m + 1));
+    return C;
+}
+
 /* ---------------------------------------------------------------- S3 HLLC */
 
 typedef struct {
@@ -374,13 +502,19 @@ void orc_hllc(const orc_problem* P, const double* Gam, const double* Pi, int32_t
 
 /* Face m+½ from the primitive window w = cells m−2..m+3 ([6][E], AoS):
  * v_L = v⁻ from cell m (cells m−2..m+2), v_R = v⁺ from cell m+1 (m−1..m+3);
- * WENO3 uses the inner cells m−1..m+1 and m..m+2. */
+ * WENO3 uses the inner cells m−1..m+1 and m..m+2.  Cm: NULL on a uniform axis, else
+ * the non-uniform coefficients of cells m, m+1. */
 static void face_flux(const orc_problem* P, const double* Gam, const double* Pi, int dir,
-                      const double* w, double* F, double* uf) {
+                      const double* w, const orc_nu_cell* Cm, double* F, double* uf) {
     const int E = orc_num_eq(P->N, P->d);
     double vL[ORC_MAXE], vR[ORC_MAXE];
     for (int e = 0; e < E; ++e) {
-        if (P->weno_order == 3) {
+        if (Cm) {   /* non-uniform axis: cell m's v-, cell m+1's v+ (Cm[0], Cm[1]) */
+            vL[e] = orc_weno5nu_minus(Cm, w[0 * E + e], w[1 * E + e], w[2 * E + e], w[3 * E + e],
+                                      w[4 * E + e], P->eps, NULL);
+            vR[e] = orc_weno5nu_plus(Cm + 1, w[1 * E + e], w[2 * E + e], w[3 * E + e],
+                                     w[4 * E + e], w[5 * E + e], P->eps, NULL);
+        } else if (P->weno_order == 3) {
             vL[e] = orc_weno3_minus(w[1 * E + e], w[2 * E + e], w[3 * E + e], P->eps, NULL);
             vR[e] = orc_weno3_plus(w[2 * E + e], w[3 * E + e], w[4 * E + e], P->eps, NULL);
         } else if (P->weno_mapped) {
@@ -475,6 +609,7 @@ void orc_rhs(const orc_problem* P, double* q, double* rhs) {
         const int t1 = (dir + 1) % 3, t2 = (dir + 2) % 3;
         const int64_t n1 = P->n[t1], n2 = P->n[t2];
         const double invd = 1.0 / P->dx[dir];
+        orc_nu_cell* NU = nu_axis(P, dir);        /* cells -1 .. n at NU[m+1] */
 #pragma omp parallel
         {
             double* v = (double*)malloc(sizeof(double) * (size_t)((n + 2 * ORC_G) * E));
@@ -498,17 +633,20 @@ void orc_rhs(const orc_problem* P, double* q, double* rhs) {
                     /* faces m+½ for m = −1..n−1 -> F[m+1]; window starts at cell m−2 */
                     for (int64_t m = -1; m < n; ++m) {
                         const double* w = v + (m - 2 + ORC_G) * E;
-                        face_flux(P, Gam, Pi, dir, w, F + (m + 1) * E, uf + (m + 1));
+                        face_flux(P, Gam, Pi, dir, w, NU ? NU + (m + 1) : NULL, F + (m + 1) * E,
+                                  uf + (m + 1));
                     }
                     for (int64_t m = 0; m < n; ++m) {
                         const int64_t c = cidx[m + ORC_G];
+                        /* 1/Δ_m: uniform spacing, or the width of cell m */
+                        const double id = NU ? 1.0 / NU[m + 1].w : invd;
                         for (int e = 0; e < E; ++e)
                             rhs[e * ncell + c] =
-                                rhs[e * ncell + c] + (F[m * E + e] - F[(m + 1) * E + e]) * invd;
+                                rhs[e * ncell + c] + (F[m * E + e] - F[(m + 1) * E + e]) * id;
                         for (int i = 0; i < N; ++i)
                             rhs[(ia + i) * ncell + c] =
                                 rhs[(ia + i) * ncell + c] +
-                                q[(ia + i) * ncell + c] * ((uf[m + 1] - uf[m]) * invd);
+                                q[(ia + i) * ncell + c] * ((uf[m + 1] - uf[m]) * id);
                     }
                 }
             }
@@ -517,6 +655,7 @@ void orc_rhs(const orc_problem* P, double* q, double* rhs) {
             free(uf);
             free(cidx);
         }
+        free(NU);
     }
 }
 
@@ -537,7 +676,12 @@ void orc_rhs_cells(const orc_problem* P, const double* q, int64_t ncells, const 
         const int64_t ci = cell_index(pd, o[0] + cells[3 * c], o[1] + cells[3 * c + 1],
                                       o[2] + cells[3 * c + 2]);
         for (int dir = 0; dir < d; ++dir) {
-            const double invd = 1.0 / P->dx[dir];
+            const int64_t mc = cells[3 * c + dir];      /* the cell's index along dir */
+            /* non-uniform axis: coefficients of cells m-1, m, m+1 from the boundaries */
+            orc_nu_cell NU3[3];
+            if (P->xb[dir])
+                for (int s = 0; s < 3; ++s) orc_nu_cell_coeffs(P->xb[dir] + (mc + s), NU3 + s);
+            const double invd = P->xb[dir] ? 1.0 / NU3[1].w : 1.0 / P->dx[dir];
             /* primitive window: cells m−3..m+3 along dir */
             double w[7 * ORC_MAXE];
             for (int s = -3; s <= 3; ++s) {
@@ -550,8 +694,9 @@ void orc_rhs_cells(const orc_problem* P, const double* q, int64_t ncells, const 
                 orc_cons_to_prim_cell(P, Gam, Pi, qc, w + (s + 3) * E);
             }
             double Fm[ORC_MAXE], Fp[ORC_MAXE], ufm, ufp;
-            face_flux(P, Gam, Pi, dir, w, Fm, &ufm);     /* face m−½: window m−3..m+2 */
-            face_flux(P, Gam, Pi, dir, w + E, Fp, &ufp); /* face m+½: window m−2..m+3 */
+            const orc_nu_cell* nu = P->xb[dir] ? NU3 : NULL;
+            face_flux(P, Gam, Pi, dir, w, nu, Fm, &ufm);                      /* face m−½ */
+            face_flux(P, Gam, Pi, dir, w + E, nu ? nu + 1 : NULL, Fp, &ufp);  /* face m+½ */
             for (int e = 0; e < E; ++e) acc[e] = acc[e] + (Fm[e] - Fp[e]) * invd;
             for (int i = 0; i < N; ++i)
                 acc[ia + i] = acc[ia + i] + q[(ia + i) * ncell + ci] * ((ufp - ufm) * invd);
@@ -663,8 +808,12 @@ double orc_max_wave_rate(const orc_problem* P, const double* q) {
                     PI = PI + v[ia + i2] * Pi[i2];
                 }
                 const double c = sqrt(((G + 1.0) * v[N + d] + PI) / (rho * G));
+                const int64_t ijk[3] = {i, j, k};
                 for (int dir = 0; dir < d; ++dir) {
-                    const double r = (fabs(v[N + dir]) + c) / P->dx[dir];
+                    /* Δ of this cell: uniform spacing or its own width (F4) */
+                    const double h = P->xb[dir] ? P->xb[dir][ijk[dir] + 4] - P->xb[dir][ijk[dir] + 3]
+                                                : P->dx[dir];
+                    const double r = (fabs(v[N + dir]) + c) / h;
                     if (r > rate) rate = r;
                 }
             }

@@ -45,7 +45,28 @@ typedef struct {
     double eps;                 /* WENO epsilon (AMB-8), default 1e-16 */
     int32_t weno_order;         /* 5 (WENO5-JS, default) or 3 (WENO3-JS) */
     int32_t weno_mapped;        /* 1: WENO5-M weights (Henrick et al. 2005) */
+    /* Non-uniform (stretched) grid, SURVEY §8(f) F4 / P:92: NULL = uniform spacing dx[k];
+     * else n[k]+7 cell boundaries of axis k, x_{-7/2} .. x_{n+5/2} (interior cell i spans
+     * [xb[i+3], xb[i+4]]; the 3 ghost cells per side are part of the input, see
+     * oracle.py extend_boundaries).  WENO5-JS only (weno_order 5, not mapped). */
+    const double* xb[3];
 } orc_problem;
+
+/* WENO5-JS on a non-uniform grid (DESIGN.md AMB-27), per cell m, from the definitions
+ * in the local coordinate t = (x - x_m)/Δ_m of cell m (x_m its centre):
+ *   candidate k = 0, 1, 2 (stencil cells m-2+k .. m+k): the quadratic q_k(t) = a + b t + c t²
+ *     whose AVERAGES over the three stencil cells are the cell values;
+ *   v-_{m+1/2} = Σ ω_k q_k(+1/2),  v+_{m-1/2} = Σ ω_k q_k(-1/2);
+ *   β_k = Σ_{l=1,2} Δ_m^{2l-1} ∫_cell (d^l q_k/dx^l)² dx = b² + (13/3) c²  (Jiang-Shu);
+ *   ideal weights: Σ_k d_k q_k(t_face) = the degree-4 reconstruction from the 5 cell
+ *     averages at the same face, read off the coefficients of cells m-2 (only in k=0)
+ *     and m+2 (only in k=2), d_1 = 1 - d_0 - d_2;
+ *   α_k = d_k/(β_k+ε)², ω_k = α_k/Σα (as in the uniform case). */
+typedef struct {
+    double M[3][3][3];          /* candidate k: (a, b, c) = M[k] (v_{m-2+k}, v_{m-1+k}, v_{m+k}) */
+    double dm[3], dp[3];        /* ideal weights of v-_{m+1/2} and v+_{m-1/2} */
+    double w;                   /* Δ_m */
+} orc_nu_cell;
 
 #ifdef __cplusplus
 extern "C" {
@@ -86,6 +107,13 @@ double orc_weno5m_minus(double a, double b, double c, double d, double e, double
                         double* weights);
 double orc_weno5m_plus(double a, double b, double c, double d, double e, double eps,
                        double* weights);
+/* Coefficients of cell m from the 6 boundaries xb6 = x_{m-5/2} .. x_{m+5/2}; returns 0,
+ * or -1 if an ideal weight is not positive (grid too strongly stretched for WENO5). */
+int32_t orc_nu_cell_coeffs(const double* xb6, orc_nu_cell* out);
+double orc_weno5nu_minus(const orc_nu_cell* C, double a, double b, double c, double d, double e,
+                         double eps, double* weights);
+double orc_weno5nu_plus(const orc_nu_cell* C, double a, double b, double c, double d, double e,
+                        double eps, double* weights);
 double orc_weno3_minus(double a, double b, double c, double eps, double* weights);
 double orc_weno3_plus(double a, double b, double c, double eps, double* weights);
 

@@ -19,7 +19,8 @@ import numpy as np
 
 __all__ = [
     "build", "lib", "Problem", "num_eq", "pad", "unpad", "constants", "cons_to_prim",
-    "prim_to_cons", "weno5_minus", "weno5_plus", "weno5m_minus", "weno5m_plus", "weno3_minus", "weno3_plus", "hllc", "fill_ghosts", "rhs",
+    "prim_to_cons", "weno5_minus", "nu_cell_coeffs", "weno5nu_minus", "weno5nu_plus",
+    "extend_boundaries", "weno5_plus", "weno5m_minus", "weno5m_plus", "weno3_minus", "weno3_plus", "hllc", "fill_ghosts", "rhs",
     "rhs_padded", "rhs_cells", "rk3_combine", "rk3_step", "count_inadmissible",
     "num_threads", "max_wave_rate", "BC_EXTERNAL", "BC_PERIODIC", "BC_REFLECTIVE", "BC_EXTRAPOLATION",
 ]
@@ -62,7 +63,13 @@ class _OrcProblem(ctypes.Structure):
         ("eps", ctypes.c_double),
         ("weno_order", ctypes.c_int32),
         ("weno_mapped", ctypes.c_int32),
+        ("xb", ctypes.c_void_p * 3),
     ]
+
+
+class _NuCell(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_double * 27), ("dm", ctypes.c_double * 3),
+                ("dp", ctypes.c_double * 3), ("w", ctypes.c_double)]
 
 
 _lib = None
@@ -87,6 +94,11 @@ def lib():
                 "orc_weno5_plus": (ctypes.c_double, [ctypes.c_double] * 6 + [_dp]),
                 "orc_weno5m_minus": (ctypes.c_double, [ctypes.c_double] * 6 + [_dp]),
                 "orc_weno5m_plus": (ctypes.c_double, [ctypes.c_double] * 6 + [_dp]),
+                "orc_nu_cell_coeffs": (ctypes.c_int32, [_dp, ctypes.POINTER(_NuCell)]),
+                "orc_weno5nu_minus": (ctypes.c_double, [ctypes.POINTER(_NuCell)] +
+                                      [ctypes.c_double] * 6 + [_dp]),
+                "orc_weno5nu_plus": (ctypes.c_double, [ctypes.POINTER(_NuCell)] +
+                                     [ctypes.c_double] * 6 + [_dp]),
                 "orc_weno3_minus": (ctypes.c_double, [ctypes.c_double] * 4 + [_dp]),
                 "orc_weno3_plus": (ctypes.c_double, [ctypes.c_double] * 4 + [_dp]),
                 "orc_hllc": (None, [P, _dp, _dp, ctypes.c_int32, _dp, _dp, _dp, _dp]),
@@ -121,17 +133,24 @@ class Problem:
     eps: float = 1e-16
     weno_order: int = 5
     weno_mapped: int = 0
+    # non-uniform grid (F4): per axis None (uniform dx) or the cell boundaries, either the
+    # n+1 interior boundaries (ghost cells added by extend_boundaries from this
+    # problem's BCs) or all n+7 (ghosts included, e.g. for BC_EXTERNAL faces)
+    x_cb: tuple = (None, None, None)
     _c: _OrcProblem = field(default=None, repr=False, compare=False)
+    _xb: list = field(default=None, repr=False, compare=False)
 
     @classmethod
     def from_spec(cls, spec, bc=None, eps=None):
-        """Duck-typed: any object with n_fluids, ndim, n, dx, bc, gamma, pi_inf, weno_eps."""
+        """Duck-typed: any object with n_fluids, ndim, n, dx, bc, gamma, pi_inf, weno_eps
+        (and optionally x_cb: per-axis cell boundaries of a stretched grid)."""
         return cls(N=spec.n_fluids, d=spec.ndim, n=tuple(spec.n), dx=tuple(spec.dx),
                    bc=tuple(spec.bc if bc is None else bc), gamma=tuple(spec.gamma),
                    pi_inf=tuple(spec.pi_inf),
                    eps=float(getattr(spec, "weno_eps", 1e-16) if eps is None else eps),
                    weno_order=int(getattr(spec, "weno_order", 5)),
-                   weno_mapped=int(bool(getattr(spec, "weno_mapped", False))))
+                   weno_mapped=int(bool(getattr(spec, "weno_mapped", False))),
+                   x_cb=tuple(getattr(spec, "x_cb", None) or (None, None, None)))
 
     def __post_init__(self):
         n = list(self.n) + [1] * (3 - len(self.n))
@@ -151,6 +170,21 @@ class Problem:
         c.eps = float(self.eps)
         c.weno_order = int(self.weno_order)
         c.weno_mapped = int(self.weno_mapped)
+        xcb = list(self.x_cb) + [None] * (3 - len(self.x_cb))
+        self.x_cb = tuple(xcb[:3])
+        self._xb = [None, None, None]
+        for k in range(3):
+            if xcb[k] is None or k >= self.d:
+                c.xb[k] = None
+                continue
+            assert self.weno_order == 5 and not self.weno_mapped, \
+                "stretched grids: WENO5-JS only (DESIGN.md AMB-27)"
+            xb = np.ascontiguousarray(xcb[k], dtype=np.float64)
+            if xb.size == self.n[k] + 1:
+                xb = extend_boundaries(xb, self.bc[2 * k], self.bc[2 * k + 1])
+            assert xb.size == self.n[k] + 7 and np.all(np.diff(xb) > 0)
+            self._xb[k] = xb                      # keeps the memory alive
+            c.xb[k] = xb.ctypes.data
         self._c = c
 
     @property
@@ -171,7 +205,32 @@ class Problem:
 
     def with_bc(self, bc):
         return Problem(self.N, self.d, self.n, self.dx, tuple(bc), self.gamma, self.pi_inf,
-                       self.eps, self.weno_order, self.weno_mapped)
+                       self.eps, self.weno_order, self.weno_mapped, self.x_cb)
+
+
+def extend_boundaries(xb: np.ndarray, bc_lo: int, bc_hi: int) -> np.ndarray:
+    """S1 for the grid (DESIGN.md AMB-27): the 3 ghost cells on each side of a stretched
+    axis get the widths of the interior cells their DATA come from (periodic
+    -1-j <- n-1-j, reflective -1-j <- j, extrapolation <- the boundary cell), laid
+    out outward from the boundary; n+1 interior boundaries -> n+7."""
+    xb = np.asarray(xb, dtype=np.float64)
+    n = xb.size - 1
+    w = np.diff(xb)
+
+    def src(g):                      # interior cell whose data ghost cell g (< 0 or >= n) holds
+        if g < 0:
+            j = -1 - g
+            return {BC_PERIODIC: n - 1 - j, BC_REFLECTIVE: j}.get(bc_lo, 0)
+        j = g - n
+        return {BC_PERIODIC: j, BC_REFLECTIVE: n - 1 - j}.get(bc_hi, n - 1)
+
+    lo = [xb[0]]
+    for g in range(-1, -4, -1):
+        lo.append(lo[-1] - w[src(g)])
+    hi = [xb[-1]]
+    for g in range(n, n + 3):
+        hi.append(hi[-1] + w[src(g)])
+    return np.concatenate([lo[:0:-1], xb, hi[1:]])
 
 
 def num_eq(N: int, d: int) -> int:
@@ -244,6 +303,26 @@ def weno5m_plus(a, b, c, d, e, eps=1e-16):
     w = np.zeros(3)
     val = lib().orc_weno5m_plus(a, b, c, d, e, eps, _p(w))
     return val, w
+
+
+def nu_cell_coeffs(xb6):
+    """Non-uniform WENO5 ingredients of one cell from its 6 stencil boundaries:
+    (M[3][3][3], dm[3], dp[3], width, status)."""
+    xb6 = np.ascontiguousarray(xb6, dtype=np.float64)
+    assert xb6.size == 6
+    C = _NuCell()
+    st = lib().orc_nu_cell_coeffs(_p(xb6), ctypes.byref(C))
+    return C, int(st)
+
+
+def weno5nu_minus(C, a, b, c, d, e, eps=1e-16):
+    w = np.zeros(3)
+    return lib().orc_weno5nu_minus(ctypes.byref(C), a, b, c, d, e, eps, _p(w)), w
+
+
+def weno5nu_plus(C, a, b, c, d, e, eps=1e-16):
+    w = np.zeros(3)
+    return lib().orc_weno5nu_plus(ctypes.byref(C), a, b, c, d, e, eps, _p(w)), w
 
 
 def weno3_minus(a, b, c, eps=1e-16):

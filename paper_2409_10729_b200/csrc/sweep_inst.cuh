@@ -2,6 +2,9 @@
 // (included by sweep_n{1,2,3}.cu with MFC_NF defined).
 #pragma once
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "dispatch.h"
 
@@ -66,21 +69,23 @@ __global__ void __launch_bounds__(256) wave_rate_kernel(const EosArgs a, double3
     if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(red[0]));
 }
 
-// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: raise it for
-// the current device whenever a launch needs more than that device has been given
-// (a success is recorded per device; a failure is returned, never cached)
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-(kernel, device) setting: raise it
+// whenever a launch needs more than that kernel has been given on the current device
+// (successes are recorded per kernel and device; a failure is returned, never cached)
 template <class K>
 static int set_smem_attr(K* kernel, size_t smem) {
-    constexpr int kMaxDev = 64;
-    static size_t done[kMaxDev] = {};
+    if (smem <= 48 * 1024) return 0;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return (int)e;
-    if (dev < 0 || dev >= kMaxDev) return (int)cudaErrorInvalidDevice;
-    if (smem <= 48 * 1024 || smem <= done[dev]) return 0;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{(const void*)kernel, dev}];
+    if (smem <= have) return 0;
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    done[dev] = smem;
+    have = smem;
     return 0;
 }
 

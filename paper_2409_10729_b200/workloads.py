@@ -61,6 +61,9 @@ class Problem:
     weno_order: int = 5           # 5 (default) or 3
     weno_mapped: bool = False     # WENO5-M weights (Henrick et al. 2005)
     notes: dict = field(default_factory=dict)
+    # stretched grid: per axis None (uniform) or the n+1 cell
+    # boundaries from lo to hi (tanh_boundaries); geometry only, like lo/hi
+    x_cb: tuple = (None, None, None)
 
     @property
     def E(self) -> int:
@@ -71,6 +74,10 @@ class Problem:
         return tuple((self.hi[k] - self.lo[k]) / self.n[k] for k in range(3))
 
     @property
+    def stretched(self) -> bool:
+        return any(x is not None for x in self.x_cb)
+
+    @property
     def cells(self) -> int:
         return int(self.n[0] * self.n[1] * self.n[2])
 
@@ -78,10 +85,19 @@ class Problem:
     def shape(self):
         return (self.E, self.n[2], self.n[1], self.n[0])
 
+    def boundaries(self, k: int) -> np.ndarray:
+        """The n+1 cell boundaries of axis k (uniform unless x_cb[k] is set)."""
+        if self.x_cb[k] is not None:
+            return np.asarray(self.x_cb[k], dtype=np.float64)
+        return self.lo[k] + np.arange(self.n[k] + 1) * self.dx[k]
+
     def centres(self, z0: int = 0, z1: int | None = None):
         """Cell-centre coordinates (X, Y, Z) broadcastable to (nz, ny, nx); optionally
         only the z-planes z0 .. z1-1 (slab-wise generation of large grids)."""
-        xs = [self.lo[k] + (np.arange(self.n[k]) + 0.5) * self.dx[k] for k in range(3)]
+        if self.stretched:
+            xs = [0.5 * (self.boundaries(k)[1:] + self.boundaries(k)[:-1]) for k in range(3)]
+        else:
+            xs = [self.lo[k] + (np.arange(self.n[k]) + 0.5) * self.dx[k] for k in range(3)]
         xs[2] = xs[2][z0:z1]
         return xs[0][None, None, :], xs[1][None, :, None], xs[2][:, None, None]
 
@@ -102,6 +118,41 @@ def _assemble(pb: Problem, partial, vel, p, alpha, nz=None):
 def smooth_step(s, width):
     """0 -> 1 across s = 0 with a tanh profile of the given width (geometry only)."""
     return 0.5 * (1.0 + np.tanh(s / width))
+
+
+# ------------------------------------------------------- stretched grids (F4)
+
+def tanh_boundaries(n: int, lo: float, hi: float, r: float = 0.5, xi_a: float = 0.3,
+                    xi_b: float = 0.7, w: float = 0.05) -> np.ndarray:
+    """Cell boundaries x_i = x(i/n), i = 0..n, of a hyperbolic-tangent local refinement
+    (Vinokur [16]; DESIGN.md AMB-27): in the computational coordinate ξ ∈ [0, 1]
+    the spacing is proportional to
+        g(ξ) = 1 - (r/2) [tanh((ξ - ξa)/w) - tanh((ξ - ξb)/w)],
+    i.e. cells are finer by the factor (1 - r) between ξa and ξb, with tanh transitions
+    of width w; x(ξ) = lo + (hi - lo) G(ξ)/G(1) with G the integral of g (closed form
+    through ln cosh).  0 <= r < 1; r = 0 gives the uniform grid."""
+    xi = np.arange(n + 1, dtype=np.float64) / n
+
+    def lncosh(z):                 # ln cosh z, overflow-free
+        z = np.abs(z)
+        return z + np.log1p(np.exp(-2.0 * z)) - np.log(2.0)
+
+    def G(x):
+        return x - 0.5 * r * w * (lncosh((x - xi_a) / w) - lncosh(xi_a / w)
+                                  - lncosh((x - xi_b) / w) + lncosh(xi_b / w))
+
+    x = lo + (hi - lo) * G(xi) / G(1.0)
+    x[0], x[-1] = lo, hi
+    return x
+
+
+def stretched(pb: Problem, axes=(0, 1, 2), **kw) -> Problem:
+    """The same problem on a tanh-refined grid along the given active axes."""
+    xcb = list(pb.x_cb)
+    for k in axes:
+        if k < pb.ndim:
+            xcb[k] = tanh_boundaries(pb.n[k], pb.lo[k], pb.hi[k], **kw)
+    return replace(pb, x_cb=tuple(xcb), name=pb.name + " stretched")
 
 
 # ----------------------------------------------------------------------- C1

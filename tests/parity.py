@@ -3,24 +3,24 @@ oracle (CPU, fp64) and through libmfc (GPU, via the C ABI) and compare with the
 metric of DESIGN.md AMB-17:
 
     per equation e:  max_cells |gpu_e - cpu_e| / scale_e  <= tol
-    RHS:   scale_e = max( max_cells |cpu_e| ,  Phi_e / dx_min )
-    state: scale_e = max_cells |cpu_e|
+    RHS, flux-scaled: scale_e = max( max_cells |cpu_e| ,  Phi_e / dx_min )
+    RHS, strict:      scale_e = max_cells |cpu_e|
+    state:            scale_e = max_cells |cpu_e|
     (and gpu == 0 exactly wherever the oracle's whole output e is identically 0).
 
 Phi_e is the magnitude of equation e's face flux (a_max = max(|u| + c)):
     partial densities, volume fractions: max|q_e| * a_max
     every momentum component:           max(rho) * a_max^2   (bounds rho u^2 + p)
     energy:                             (max|rhoE| + max|p|) * a_max
-Rounding in any correct implementation of the flux is relative to Phi_e, so a
-component whose RHS is tiny or identically 0 in exact arithmetic (the air partial
-density at rest in C1: oracle round-off 1.2e-10 against Phi/dx = 7.5e6; the zero
-tangential momenta of C2/C3, where p is uniform along the sweep) is not compared
-against its own round-off noise.
-
-After many steps a shock problem can be ill-conditioned: the oracle perturbed by
-1 ulp of its own input moves by `oracle_sensitivity` (C1: 2.1e-10 after 100 steps);
-no implementation with a different rounding order can be closer than that, so the
-100-step bound is max(1e-10, 3 * that sensitivity) (DESIGN.md AMB-17).
+Rounding in any correct implementation of the flux difference is relative to
+Phi_e / dx, so the flux-scaled error is asserted <= 1e-12 for every equation, and the
+STRICT error (the north star's "1e-12 relative" read literally) for every equation
+whose RHS is not itself a cancellation of much larger fluxes: cond_e =
+(Phi_e/dx) / max|cpu_e| <= COND_STRICT.  An equation above that (the air partial
+density at rest in C1, the zero tangential momenta of C2/C3/C5 where p is uniform
+along the sweep, alpha of a single fluid) has an exact RHS that is ~0 and an oracle
+RHS that is rounding noise of size ~eps * Phi_e/dx; its strict error is recorded in
+the parity log (per equation, with cond_e) and listed in DESIGN.md, not asserted.
 """
 from __future__ import annotations
 
@@ -31,15 +31,24 @@ from paper_2409_10729_b200 import workloads as W
 
 RHS_TOL = 1e-12       # BASELINE.json north_star: per RHS evaluation
 STEP100_TOL = 1e-10   # BASELINE.json north_star: after 100 RK3 steps
+COND_STRICT = 1e2     # strict 1e-12 asserted where the RHS is >= 1 % of its flux scale
+FLUX_ULPS = 64 * np.finfo(float).eps   # and every equation within 64 ulp of its flux scale
 
 # achieved errors, written to $MFC_PARITY_LOG by tests/conftest.py at session end
 RECORD = {}
 
 
-def record(name: str, err, tol, strict=None):
+def record(name: str, err, tol, strict=None, cond=None):
     RECORD[name] = {"max_err": float(np.max(err)), "tol": float(np.max(tol)),
-                    "per_eq": [float(x) for x in np.atleast_1d(err)],
-                    **({"strict_max_err": float(np.max(strict))} if strict is not None else {})}
+                    "per_eq": [float(x) for x in np.atleast_1d(err)]}
+    if strict is not None:
+        RECORD[name]["strict_per_eq"] = [float(x) for x in np.atleast_1d(strict)]
+        RECORD[name]["strict_max_err"] = float(np.max(strict))
+    if cond is not None:
+        RECORD[name]["cond_per_eq"] = [float(x) for x in np.atleast_1d(cond)]
+        wc = np.atleast_1d(cond) <= COND_STRICT
+        RECORD[name]["strict_max_err_well_conditioned"] = (
+            float(np.max(np.atleast_1d(strict)[wc])) if wc.any() else 0.0)
 
 
 def rel_err(gpu: np.ndarray, cpu: np.ndarray, floor=None) -> np.ndarray:
@@ -56,6 +65,54 @@ def rel_err(gpu: np.ndarray, cpu: np.ndarray, floor=None) -> np.ndarray:
         else:
             out[e] = diff / scale
     return out
+
+
+def check_rhs(name: str, pb, v: np.ndarray, q: np.ndarray, got: np.ndarray, ref: np.ndarray,
+              tol: float = RHS_TOL):
+    """The RHS parity assertion of AMB-17: flux-scaled error <= tol for every equation,
+    strict error <= tol for every well-conditioned equation; both recorded per equation."""
+    phi = rhs_flux_scale(pb, v, q)
+    flux = rel_err(got, ref, phi)
+    strict = rel_err(got, ref)
+    mx = np.abs(ref).reshape(ref.shape[0], -1).max(axis=1)
+    cond = np.where(mx > 0, phi / np.where(mx > 0, mx, 1.0), np.inf)
+    record(name, flux, tol, strict, cond)
+    assert np.all(flux <= tol), (name, "flux-scaled", flux)
+    assert np.all(flux <= FLUX_ULPS), (name, "flux-scaled > 64 ulp", flux)
+    wc = cond <= COND_STRICT
+    assert np.all(strict[wc] <= tol), (name, "strict (well-conditioned)", strict, cond)
+    return flux, strict, cond
+
+
+def state_err(pb, got: np.ndarray, ref: np.ndarray) -> tuple:
+    """State metric after k steps (AMB-17): max|gpu_e - cpu_e| / max|cpu_e| per equation,
+    except that the momentum components are one vector and share its scale
+    max_k max|cpu_(rho u_k)| (a tangential momentum that is identically 0 in exact
+    arithmetic -- C3 before the shock reaches the droplet -- is otherwise compared as
+    round-off against round-off).  Returns (metric, strict per-component errors)."""
+    strict = rel_err(got, ref)
+    N, d = pb.n_fluids, pb.ndim
+    mom = np.abs(ref[N:N + d]).max()
+    err = strict.copy()
+    for e in range(N, N + d):
+        diff = np.abs(got[e] - ref[e]).max()
+        err[e] = 0.0 if diff == 0.0 else (diff / mom if mom > 0 else np.inf)
+    return err, strict
+
+
+def check_against_oracle(name: str, pb, v, q, rhs_gpu=None, state_gpu=None, dt=0.0,
+                         nsteps=0):
+    """A gathered multi-rank result (decomposed, fused-halo, IPC) against the ORACLE on
+    the whole domain, not only against the GPU's own single-domain run: the RHS under
+    check_rhs, the state after nsteps RK3 steps under the 1e-10 state metric."""
+    P = O.Problem.from_spec(pb)
+    if rhs_gpu is not None:
+        check_rhs("rhs " + name, pb, v, q, rhs_gpu, O.rhs(P, q))
+    if state_gpu is not None:
+        ref = O.rk3_step(P, q, dt, nsteps=nsteps)
+        err, strict = state_err(pb, state_gpu, ref)
+        record(f"{nsteps} RK3 steps " + name, err, STEP100_TOL, strict)
+        assert np.all(err <= STEP100_TOL), (name, err)
 
 
 def oracle_inputs(pb: W.Problem, seed: int = W.SEED):
@@ -117,17 +174,6 @@ def rhs_flux_scale(pb: W.Problem, v: np.ndarray, q: np.ndarray) -> np.ndarray:
         else:
             phi[e] = np.abs(q[e]).max() * amax
     return phi / dxm
-
-
-def oracle_sensitivity(P, q, dt, nsteps, ref, trials=2, seed=0):
-    """Max per-equation deviation of the oracle from itself when its input is
-    perturbed by +-1 ulp (random signs), after nsteps RK3 steps."""
-    rng = np.random.default_rng(seed)
-    worst = np.zeros(q.shape[0])
-    for _ in range(trials):
-        qp = q * (1.0 + rng.choice([-1.0, 1.0], q.shape) * np.finfo(float).eps)
-        worst = np.maximum(worst, rel_err(O.rk3_step(P, qp, dt, nsteps), ref))
-    return worst
 
 
 def stable_dt(pb: W.Problem, v: np.ndarray, cfl: float = 0.3) -> float:

@@ -8,7 +8,7 @@ import pytest
 import oracle as O
 from paper_2409_10729_b200 import workloads as W
 
-from parity import oracle_inputs, stable_dt
+from parity import check_against_oracle, oracle_inputs, stable_dt
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -61,9 +61,11 @@ def test_loopback_rhs_and_steps_bitwise(procs):
     pb = W.random_problem(3, (24, 20, 30), 2, "water")
     P_, v, q = oracle_inputs(pb)
     dt = stable_dt(pb, v)
-    assert np.array_equal(_split_run(pb, q, procs, dt, 0, rhs_only=True),
-                          _single(pb, q, dt, 0, rhs_only=True))
-    assert np.array_equal(_split_run(pb, q, procs, dt, 5), _single(pb, q, dt, 5))
+    r_split = _split_run(pb, q, procs, dt, 0, rhs_only=True)
+    q_split = _split_run(pb, q, procs, dt, 5)
+    assert np.array_equal(r_split, _single(pb, q, dt, 0, rhs_only=True))
+    assert np.array_equal(q_split, _single(pb, q, dt, 5))
+    check_against_oracle(f"loopback procs={procs} " + pb.name, pb, v, q, r_split, q_split, dt, 5)
 
 
 def test_loopback_nonperiodic_z():
@@ -72,4 +74,7 @@ def test_loopback_nonperiodic_z():
                               W.BC_EXTRAPOLATION, W.BC_REFLECTIVE))
     _, v, q = oracle_inputs(pb)
     dt = stable_dt(pb, v)
-    assert np.array_equal(_split_run(pb, q, (1, 1, 4), dt, 3), _single(pb, q, dt, 3))
+    q_split = _split_run(pb, q, (1, 1, 4), dt, 3)
+    assert np.array_equal(q_split, _single(pb, q, dt, 3))
+    check_against_oracle("loopback procs=(1,1,4) nonperiodic " + pb.name, pb, v, q, None,
+                         q_split, dt, 3)

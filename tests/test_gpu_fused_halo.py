@@ -18,7 +18,7 @@ import pytest
 
 from paper_2409_10729_b200 import workloads as W
 
-from parity import oracle_inputs, stable_dt
+from parity import check_against_oracle, oracle_inputs, stable_dt
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -86,6 +86,7 @@ def test_fused_group_bitwise_3d(procs):
     r_f, q_f, _, _ = _group_run(pb, q, procs, dt, 4, fused=True)
     assert np.array_equal(r_f, r_ref) and np.array_equal(r_x, r_ref)
     assert np.array_equal(q_f, q_ref) and np.array_equal(q_x, q_ref)
+    check_against_oracle(f"fused procs={procs} " + pb.name, pb, v, q, r_f, q_f, dt, 4)
 
 
 @pytest.mark.parametrize("ndim,procs,bc", [
@@ -104,6 +105,8 @@ def test_fused_group_bitwise_dims_and_bcs(ndim, procs, bc):
     r_f, q_f, _, _ = _group_run(pb, q, procs, dt, 3, fused=True)
     assert np.array_equal(r_f, r_ref)
     assert np.array_equal(q_f, q_ref)
+    check_against_oracle(f"fused {ndim}D procs={procs} bc={bc} " + pb.name, pb, v, q, r_f, q_f,
+                         dt, 3)
 
 
 def test_fused_group_keeps_ghosts_current_and_launches_no_halo_kernels():
@@ -214,3 +217,5 @@ def test_ipc_peer_two_processes_bitwise(procs, tmp_path):
         q_f[sl] = np.load(tmp_path / f"q{r}.npy")
     assert np.array_equal(r_f, r_ref)
     assert np.array_equal(q_f, q_ref)
+    check_against_oracle(f"IPC 2 processes procs={procs} " + pb.name, pb, v, q, r_f, q_f, dt,
+                         nsteps)

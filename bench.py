@@ -105,7 +105,10 @@ class ClockSampler:
 # ------------------------------------------------------------ cpu baseline
 def cpu_oracle_grind(target_s: float = 12.0, n: int = 256, max_nz: int = 256):
     """The oracle as it stands, timed on the host cores on a bounded sample of C3:
-    one RK3 step on an n x n x nz block of the C3 field (nz sized for ~target_s)."""
+    one RK3 step on an n x n x nz block of the C3 field (nz sized for ~target_s), with
+    every OpenMP thread; then the same on a 2-plane block with ONE thread.  Reported:
+    wall grind (all threads), core-normalised grind (wall x cores, the paper's CPU
+    normalisation P:273) and single-thread grind."""
     import oracle as O
     from paper_2409_10729_b200 import workloads as W
     O.build()
@@ -118,14 +121,23 @@ def cpu_oracle_grind(target_s: float = 12.0, n: int = 256, max_nz: int = 256):
         O.rk3_step(P, q, pb.dt, nsteps=1)
         return time.perf_counter() - t0, pb
 
+    cores = O.num_threads()
     t, pb = run(4)
     nz = int(min(max_nz, max(4, 4 * target_s / max(t, 1e-3))))
     if nz > 4:
         t, pb = run(nz)
     grind = t / (pb.cells * pb.E * RHS_PER_STEP) * 1e9
-    return {"value": grind, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+    O.set_num_threads(1)
+    try:
+        t1, pb1 = run(2)
+    finally:
+        O.set_num_threads(cores)
+    grind1 = t1 / (pb1.cells * pb1.E * RHS_PER_STEP) * 1e9
+    return {"value": grind, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"1 SSP-RK3 step (3 RHS) of the C3 field on a {n}x{n}x{nz} block "
-                      f"({pb.cells} cells, E={pb.E}), {t:.2f} s wall"}
+                      f"({pb.cells} cells, E={pb.E}), {t:.2f} s wall on {cores} threads; "
+                      f"single thread: {n}x{n}x2 block, {t1:.2f} s",
+            "core_normalised": grind * cores, "single_thread": grind1}
 
 
 def run_reference(args):
@@ -242,11 +254,19 @@ def run_ours(args):
         else:
             pb = W.c3_droplet(n, nz=n * world)   # global domain: blocks stacked along z
             workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
+        if args.stretch:      # F4: tanh-refined grid on every axis of the global domain
+            pb = W.stretched(pb)
+            block = W.stretched(block)
+            workload += ", tanh-stretched grid (F4)"
         s = mfc.Solver(variant(pb), procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
                        peer=peer)
         # every rank holds the same C3 block (its local prims), converted on the GPU
         q = s.state_from_prims(W.c3_prims(block))
         dt = block.dt
+        if args.stretch:      # CFL of the smallest cell
+            dt *= min(np.diff(pb.boundaries(k)).min() for k in range(3)) / min(pb.dx)
+    elif args.config == "C5" and args.stretch:
+        raise SystemExit("--stretch runs C3 / C4 only")
     elif args.config == "C5":
         nn = args.n if args.n != 256 else 512
         pb = W.c5_three_fluid(nn)                # strong scaling: fixed 512^3 split in z-slabs
@@ -287,7 +307,6 @@ def run_ours(args):
 
     clk = ClockSampler(local)
     clk.start()
-    s.profile(True)
     barrier()
     torch.cuda.synchronize()
     # the three state buffers of a step (q, S1, S2 + acc) must not sit in the 126 MB L2
@@ -295,31 +314,40 @@ def run_ours(args):
     # events of each step; large ones exceed it by themselves
     flush = 4 * 8 * L.n_elems < 2 * L2_BYTES
     scratch = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if flush else None
+    # timed region: exactly K steps, library profiling OFF, one CUDA event pair per step
+    # on the launching stream
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps if flush else 1)]
+           for _ in range(args.steps)]
     launches = 0
-    if not flush:
-        evs[0][0].record(stream)
     for i in range(args.steps):
         if flush:
             scratch.fill_(float(i))
-            evs[i][0].record(stream)
+        evs[i][0].record(stream)
         s.rk3_step(q, dt)
         launches += s.last_launch_count()
-        if flush:
-            evs[i][1].record(stream)
-    if not flush:
-        evs[0][1].record(stream)
+        evs[i][1].record(stream)
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
-    prof = s.profile_read()
-    s.profile(False)
-    ms = sum(a.elapsed_time(b) for a, b in evs)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(step_ms)
     t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+
+    # separate profiled pass (same configuration, right after the timed region): every
+    # kernel launch bracketed by events on its own stream -> the per-kernel split and
+    # the roofline of the dominant kernel
+    nprof = max(3, min(args.steps, 10))
+    s.profile(True)
+    for i in range(nprof):
+        if flush:
+            scratch.fill_(float(i))
+        s.rk3_step(q, dt)
+    torch.cuda.synchronize()
+    prof = s.profile_read()
+    s.profile(False)
 
     cells_local = int(np.prod(L.n_local))
     cells_total = cells_local * world
@@ -329,22 +357,27 @@ def run_ours(args):
     # state sanity (finite) after the timed steps
     finite = bool(torch.isfinite(s.interior(q)).all().item())
 
-    # dominant kernel roofline (CUDA events on the launch stream, over the timed region)
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    qn_in_x = pb.ndim == 3 and E <= 8
     sweeps = {k: v for k, v in prof.items() if k.startswith("sweep") and v[1]}
     dom = max(sweeps, key=lambda k: sweeps[k][0])
-    dom_ms, dom_n = sweeps[dom]
-    per_launch_ms = dom_ms / max(dom_n, 1)
+
+    def per_launch(k):
+        return sweeps[k][0] / max(sweeps[k][1], 1)
+
+    def hbm_of(k):
+        b = algorithmic_bytes(k, E, qn_in_x) * cells_local
+        g = b / (per_launch(k) * 1e-3) / 1e9
+        return {"achieved": g, "frac": g / hbm_peak, "per_launch_ms": per_launch(k),
+                "algorithmic_bytes_per_cell": algorithmic_bytes(k, E, qn_in_x)}
+
     flops = algorithmic_flops(dom, pb.n_fluids, pb.ndim) * cells_local
-    achieved_tf = flops / (per_launch_ms * 1e-3) / 1e12
-    qn_in_x = pb.ndim == 3 and E <= 8 and os.environ.get("MFC_XBASE_N", "") != "0"
-    alg_bytes = algorithmic_bytes(dom, E, qn_in_x) * cells_local
-    achieved_gbs = alg_bytes / (per_launch_ms * 1e-3) / 1e9
-    traffic = None
-    try:   # DRAM bytes of this kernel from the last committed ncu --set full capture
+    achieved_tf = flops / (per_launch(dom) * 1e-3) / 1e12
+    traffic, traffic_src = None, None
+    try:   # DRAM bytes of this kernel from the committed ncu --set full capture
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(dom)
+        traffic, traffic_src = tr.get(dom), tr.get("source")
     except Exception:
         pass
     # per step: 3 x (16E + 24E + 24E) + q^n reads in stages 2 and 3 (2 x 8E) = 208E B/cell
@@ -352,6 +385,7 @@ def run_ours(args):
     hbm_step = step_alg_bytes / (ms_max / args.steps * 1e-3) / 1e9
     step_flops = (RHS_PER_STEP * sum(algorithmic_flops(k, pb.n_fluids, pb.ndim)
                                      for k in ("sweep_x", "sweep_y", "sweep_z")) + 96.0) * cells_local
+    srt = sorted(step_ms)
 
     line = {
         "metric": METRIC, "value": grind, "unit": UNIT, "n_gpus": world,
@@ -366,28 +400,37 @@ def run_ours(args):
                           f"inputs > L2: each state buffer {8 * L.n_elems / 1e9:.2f} GB >> 126 MB, no flush"),
                    "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
                    "halo": (args.halo if world > 1 else "none"),
+                   **({"grid": "tanh-refined on every axis (F4): cells 0.625x finer in "
+                              "[0.3, 0.7], workloads.tanh_boundaries"} if args.stretch else {}),
                    **({"weno": {"3": "WENO3-JS", "5m": "WENO5-M (mapped)"}[args.weno]}
                       if args.weno != "5" else {}),
                    **({"same_device": "all ranks on GPU 0: protocol check, time-sliced, not a "
                                       "scaling number"} if args.same_device else {})},
+        "step_ms": {"median": statistics.median(step_ms), "min": srt[0], "max": srt[-1],
+                    "p10": srt[len(srt) // 10], "p90": srt[(9 * len(srt)) // 10],
+                    "timing": "one CUDA event pair per step on the launching stream, "
+                              "library profiling off; value = sum over the K steps"},
         "hbm_gbs_step": hbm_step,
+        "hbm_frac_step": hbm_step / hbm_peak,
         "fp64_tflops_step": step_flops / (ms_max / args.steps * 1e-3) / 1e12,
-        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+        "kernel_ms_per_step": {k: v[0] / nprof for k, v in prof.items() if v[1]},
+        "kernel_split_source": f"separate profiled pass of {nprof} steps after the timed "
+                               "region (events around every launch)",
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved_tf,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "per_launch_ms": per_launch_ms,
+                     "traffic_source": traffic_src,
+                     "per_launch_ms": per_launch(dom),
                      "algorithmic_flops_per_cell": algorithmic_flops(dom, pb.n_fluids, pb.ndim),
                      **({"flops_note": "algorithmic flops of the WENO5-JS path (DESIGN.md "
                                        "§6.3); this run uses another reconstruction"}
-                        if args.weno != "5" else {}),
+                        if args.weno != "5" or args.stretch else {}),
                      "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz "
                                     "(B200_PROFILING.md unit counts/clock; MEASURED_PEAKS.json "
                                     "has no FP64 entry; tools/fp64_peak.cu measured 34.1)",
-                     "hbm_view": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                                  "frac": achieved_gbs / hbm_peak,
-                                  "algorithmic_bytes_per_cell": algorithmic_bytes(dom, E, qn_in_x),
-                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}},
+                     "hbm_view": {**hbm_of(dom), "peak": hbm_peak, "unit": "GB/s",
+                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
+                     "hbm_per_sweep": {k: hbm_of(k) for k in sorted(sweeps)}},
         "clocks": clocks,
         "gpu_launches": launches,
         "state_finite": finite,
@@ -446,6 +489,8 @@ def main():
     ap.add_argument("--weno", default="5", choices=["5", "3", "5m"],
                     help="reconstruction: WENO5-JS (default, the named path), WENO3-JS or "
                          "WENO5-M (SURVEY §8(f) F2)")
+    ap.add_argument("--stretch", action="store_true",
+                    help="C3/C4 on a tanh-refined grid (SURVEY §8(f) F4; per-cell WENO tables)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

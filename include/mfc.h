@@ -149,6 +149,21 @@ int mfc_set_weno_order(mfc_ctx* ctx, int32_t order);
  * effect with order 3.  EINVAL unless on is 0 or 1; a captured step graph is dropped. */
 int mfc_set_weno_mapped(mfc_ctx* ctx, int32_t on);
 
+/* Non-uniform grid along dimension dim ("local mesh refinement
+ * is implemented using a hyperbolic tangent function [16]"; DESIGN.md AMB-27).
+ * x_cb: n_global[dim]+1 strictly increasing cell boundaries of the GLOBAL axis (host
+ * array, copied; any mapping, e.g. the tanh refinement of workloads.tanh_boundaries).
+ * Ghost cells take the widths of the cells their data come from (periodic wrap, mirror,
+ * or the boundary cell for extrapolation).  The library derives, per local cell, the
+ * WENO5-JS candidate, smoothness-indicator and ideal-weight coefficients of the
+ * non-uniform grid and 1/dx_m, and the sweeps along dim use them (dx of mfc_grid is
+ * then ignored along dim).  x_cb == NULL restores the uniform spacing.  Needs a bound
+ * workspace (the tables live in it); synchronous.  WENO5-JS only: EUNSUPPORTED with
+ * WENO3 or WENO5-M selected (and those setters refuse a stretched context).
+ * Errors: EINVAL (dim, n, non-increasing x_cb, or a grid so strongly stretched that an
+ * ideal weight is not positive), ESTATE (no workspace), ECUDA. */
+int mfc_set_grid(mfc_ctx* ctx, int32_t dim, const double* x_cb, int64_t n);
+
 /* Primitive <-> conserved conversion on the interior cells of padded device
  * buffers (same layout for v and q; may not alias).  prim_to_cons evaluates
  * rhoE = (Gamma p + Pi) + KE, cons_to_prim the inverse in the order of DESIGN.md
@@ -250,8 +265,9 @@ int mfc_rk3_step_group(mfc_ctx* const* ctxs, double* const* qs, int32_t count, d
  *   a barrier on all ranks before the first fused call.
  * Ranks then order their operations with stream memory operations on the flags
  * (cuStreamWaitValue64 / cuStreamWriteValue64: no spinning kernels): every fused call
- * is collective and all ranks must issue the same sequence.  mfc_rk3_steps does not
- * use a CUDA graph in this mode.  EUNSUPPORTED if the device lacks 64-bit stream
+ * is collective and all ranks must issue the same sequence.  mfc_rk3_steps replays a
+ * CUDA graph of one step in this mode too (the stream memory operations are captured;
+ * every step waits for and signals the same flag slots).  EUNSUPPORTED if the device lacks 64-bit stream
  * memory operations; ECUDA if IPC mapping fails. */
 #define MFC_PEER_BLOB_BYTES 512
 int mfc_fused_halo_group(mfc_ctx* const* ctxs, double* const* qs, int32_t count);

@@ -822,6 +822,14 @@ double orc_max_wave_rate(const orc_problem* P, const double* q) {
     return rate;
 }
 
+void orc_set_num_threads(int32_t n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int32_t orc_num_threads(void) {
 #ifdef _OPENMP
     return (int32_t)omp_get_max_threads();

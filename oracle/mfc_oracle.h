@@ -155,8 +155,10 @@ double orc_max_wave_rate(const orc_problem* P, const double* q);
  * non-finite values, rho <= 0 or c^2 <= 0. */
 int64_t orc_count_inadmissible(const orc_problem* P, const double* q);
 
-/* Threads the OpenMP runtime will use (for the cpu_baseline report). */
+/* Threads the OpenMP runtime will use (for the cpu_baseline report), and a setter
+ * (the single-thread grind of bench.py's cpu_baseline). */
 int32_t orc_num_threads(void);
+void orc_set_num_threads(int32_t n);
 
 #ifdef __cplusplus
 }

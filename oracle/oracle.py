@@ -22,7 +22,7 @@ __all__ = [
     "prim_to_cons", "weno5_minus", "nu_cell_coeffs", "weno5nu_minus", "weno5nu_plus",
     "extend_boundaries", "weno5_plus", "weno5m_minus", "weno5m_plus", "weno3_minus", "weno3_plus", "hllc", "fill_ghosts", "rhs",
     "rhs_padded", "rhs_cells", "rk3_combine", "rk3_step", "count_inadmissible",
-    "num_threads", "max_wave_rate", "BC_EXTERNAL", "BC_PERIODIC", "BC_REFLECTIVE", "BC_EXTRAPOLATION",
+    "num_threads", "set_num_threads", "max_wave_rate", "BC_EXTERNAL", "BC_PERIODIC", "BC_REFLECTIVE", "BC_EXTRAPOLATION",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -111,6 +111,7 @@ def lib():
                 "orc_count_inadmissible": (ctypes.c_int64, [P, _dp]),
                 "orc_max_wave_rate": (ctypes.c_double, [P, _dp]),
                 "orc_num_threads": (ctypes.c_int32, []),
+                "orc_set_num_threads": (None, [ctypes.c_int32]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -405,3 +406,7 @@ def max_wave_rate(P: Problem, q: np.ndarray) -> float:
 
 def num_threads() -> int:
     return int(lib().orc_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    lib().orc_set_num_threads(int(n))

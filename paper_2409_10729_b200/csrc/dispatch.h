@@ -27,9 +27,15 @@ struct EosArgs {
 template <int N>
 cudaError_t launch_eos(int D, bool to_cons, const EosArgs& a, cudaStream_t s);
 
+// 1/dx of every interior cell of the stretched axes (nullptr: uniform axis, inv_dx)
+struct WaveGrid {
+    const double* inv[3];
+};
+
 // max over interior cells of max_k (|u_k|+c)/dx_k -> *out (device double, must hold
 // 0 or a smaller non-negative value before the launch)
 template <int N>
-cudaError_t launch_wave_rate(int D, const EosArgs& a, double3 inv_dx, double* out, cudaStream_t s);
+cudaError_t launch_wave_rate(int D, const EosArgs& a, double3 inv_dx, const WaveGrid& wg,
+                             double* out, cudaStream_t s);
 
 }  // namespace mfc

@@ -29,6 +29,38 @@
 
 using namespace mfc;
 
+// ------------------------------------------------------------ TMA tensor maps
+
+namespace mfc {
+cudaError_t encode_state_map(CUtensorMap* out, const double* base, int64_t X, int64_t Y,
+                             int64_t Z, int E, int box_x) {
+    using Fn = CUresult(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                        CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                        CUtensorMapFloatOOBfill);
+    static Fn* fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        void* p = nullptr;
+        const cudaError_t e = cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000,
+                                                               cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return cudaErrorNotSupported;
+        fn = (Fn*)p;
+    }
+    const cuuint64_t dims[4] = {(cuuint64_t)X, (cuuint64_t)Y, (cuuint64_t)Z, (cuuint64_t)E};
+    const cuuint64_t strides[3] = {(cuuint64_t)X * 8, (cuuint64_t)(X * Y) * 8,
+                                   (cuuint64_t)(X * Y * Z) * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)box_x, 1, 1, (cuuint32_t)E};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+}  // namespace mfc
+
+
 namespace {
 
 thread_local std::string g_err;
@@ -78,6 +110,8 @@ struct mfc_ctx {
     int64_t offset = 0, n_elems = 0;
     double dx[3] = {1, 1, 1};
     int bc[6] = {0, 0, 0, 0, 0, 0};  // physical bc code, or BC_NEIGHBOR
+    int bc_phys[6] = {0, 0, 0, 0, 0, 0};  // the global domain's boundary conditions
+    int64_t n_global[3] = {1, 1, 1};
     int nbr[6] = {-1, -1, -1, -1, -1, -1};
     Materials mat{};
     double eps = 1e-16;
@@ -97,6 +131,10 @@ struct mfc_ctx {
     int64_t face_elems[3] = {0, 0, 0};  // E * 3 * area of a face normal to dim k
     int64_t launches = 0;
     int stream_chunks = -1;       // streamed advance_host: z-chunks (-1 default, 0 off)
+    // non-uniform grid (F4): global cell boundaries per stretched axis (host copy) and
+    // the per-cell coefficient tables in the workspace (NU_NCOEF x (n_local + 6))
+    std::vector<double> xcb[3];
+    double* nu[3] = {nullptr, nullptr, nullptr};
     // optional per-launch CUDA-event timing (mfc_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -122,8 +160,10 @@ struct mfc_ctx {
     PeerFace pf[6][3] = {};
     bool pf_set[6] = {};
     uint64_t* flags = nullptr;     // device [8]: flags[f] written by the neighbour across f
-    CUdeviceptr peer_flag[6] = {}; // the neighbour's flags[f^1]
+    CUdeviceptr peer_flag[6] = {}; // the neighbour's 3 flag slots for its face f^1
     uint64_t epoch = 0;            // fused-halo operations completed by this rank
+    uint64_t waited = 0;           // neighbour operations awaited (and slots reset) so far
+    uint64_t graph_phase = 0;      // (epoch % 3, epoch - waited) the graph was captured at
     std::vector<void*> ipc_maps;   // IPC mappings this context opened
     // streamed mfc_advance_host (one step, host buffers): the sweeps of one RK stage
     // restricted to z planes [zr0, zr1) (zr1 < 0: whole domain), copy streams, events
@@ -303,6 +343,151 @@ __global__ void peer_exchange_kernel(const double* q, FaceGeom g, PeerFace p) {
     }
 }
 
+// ------------------------------------------------------- non-uniform grids (F4)
+//
+// DESIGN.md AMB-27.  WENO5 on a stretched axis reconstructs from cell averages on cells of
+// unequal width.  The coefficients of cell m come from the primitive function
+// V(x) = integral of v from the left end of a stencil: at the stencil's cell boundaries
+// y_0 < .. < y_K it is known exactly (partial sums of v_j h_j), its interpolating
+// polynomial of degree K has derivative q = V' = the reconstruction polynomial of the
+// K cells (Shu, NASA CR-97-206253, 1997, §2.2), so
+//   q^(r)(x) = sum_i V(y_i) L_i^(r+1)(x),  weight of v_j: h_j sum_{i > j} L_i^(r+1)(x)
+// with L_i the Lagrange basis on the y's.  Everything is evaluated in the local coordinate
+// t = (x - x_m)/dx_m of cell m (widths and positions scaled by dx_m), so b = q'(0) and
+// c = q''(0)/2 are the t-polynomial's coefficients and beta = b^2 + (13/3) c^2.
+
+size_t nu_table_bytes(const mfc_ctx* c, int k) {
+    return ((size_t)NU_NCOEF * (c->nl[k] + 2 * kGhost) * sizeof(double) + 255) / 256 * 256;
+}
+
+bool any_stretched(const mfc_ctx* c) {
+    for (int k = 0; k < 3; ++k)
+        if (!c->xcb[k].empty()) return true;
+    return false;
+}
+
+// r-th derivative at x of the Lagrange basis polynomial L_i on nodes y[0..K]
+double lagrange_deriv(const double* y, int K, int i, int r, double x) {
+    // coefficients of prod_{l != i} (x - y_l) / (y_i - y_l), lowest degree first
+    double cf[8] = {1.0, 0, 0, 0, 0, 0, 0, 0};
+    int deg = 0;
+    for (int l = 0; l <= K; ++l) {
+        if (l == i) continue;
+        const double inv = 1.0 / (y[i] - y[l]);
+        for (int d = deg + 1; d >= 0; --d) {
+            const double lo = d > 0 ? cf[d - 1] : 0.0;
+            cf[d] = (lo - y[l] * cf[d]) * inv;
+        }
+        ++deg;
+    }
+    double v = 0.0;
+    for (int d = deg; d >= r; --d) {      // Horner on the r-th derivative
+        double f = 1.0;
+        for (int q = 0; q < r; ++q) f *= (double)(d - q);
+        v = v * x + f * cf[d];
+    }
+    return v;
+}
+
+// weights w[0..K-1] on the K cell values of the r-th derivative, at x, of the
+// reconstruction polynomial of the cells between nodes y[0..K]
+void recon_weights(const double* y, int K, int r, double x, double* w) {
+    double Lp[8];
+    for (int i = 0; i <= K; ++i) Lp[i] = lagrange_deriv(y, K, i, r + 1, x);
+    for (int j = 0; j < K; ++j) {
+        double sum = 0.0;
+        for (int i = j + 1; i <= K; ++i) sum += Lp[i];
+        w[j] = (y[j + 1] - y[j]) * sum;
+    }
+}
+
+// Widths of the global cells -3 .. n+2 of axis k (index g + 3): a ghost cell has the
+// width of the cell its data come from (periodic wrap, mirror, or the boundary cell).
+std::vector<double> extended_widths(const std::vector<double>& x, int bc_lo, int bc_hi) {
+    const int64_t n = (int64_t)x.size() - 1;
+    auto src = [&](int64_t g) -> int64_t {           // data source of cell g
+        if (g >= 0 && g < n) return g;
+        if (g < 0) {
+            const int64_t j = -1 - g;
+            return bc_lo == MFC_BC_PERIODIC ? n - 1 - j : (bc_lo == MFC_BC_REFLECTIVE ? j : 0);
+        }
+        const int64_t j = g - n;
+        return bc_hi == MFC_BC_PERIODIC ? j : (bc_hi == MFC_BC_REFLECTIVE ? n - 1 - j : n - 1);
+    };
+    std::vector<double> w(n + 6);
+    for (int64_t g = -3; g < n + 3; ++g) {
+        const int64_t i = src(g);
+        w[g + 3] = x[i + 1] - x[i];
+    }
+    return w;
+}
+
+// Coefficient table of local axis k (host) -> the workspace.
+int upload_nu_table(mfc_ctx* c, int k) {
+    const int64_t n = c->nl[k], ld = n + 2 * kGhost;
+    const std::vector<double> we = extended_widths(c->xcb[k], c->bc_phys[2 * k],
+                                                   c->bc_phys[2 * k + 1]);
+    std::vector<double> tab((size_t)NU_NCOEF * ld, 0.0);
+    auto T = [&](int coef, int64_t m) -> double& { return tab[(size_t)coef * ld + m + kGhost]; };
+    for (int64_t m = -1; m <= n; ++m) {
+        const int64_t g = c->lo_g[k] + m;                 // global cell
+        const double* hw = &we[g + 3 - 2];               // widths of cells g-2 .. g+2
+        const double h = hw[2];
+        // boundaries in units of h from the centre of cell m, built from the WIDTHS only,
+        // so a cell's coefficients do not depend on where it sits (a periodic ghost
+        // cell -1 and cell n-1, or the same cell seen by two subdomains, agree bitwise)
+        double t[6];
+        t[2] = -0.5;
+        t[3] = 0.5;
+        t[1] = t[2] - hw[1] / h;
+        t[0] = t[1] - hw[0] / h;
+        t[4] = t[3] + hw[3] / h;
+        t[5] = t[4] + hw[4] / h;
+        double wm[3][3], wp[3][3];                        // candidate weights at t = +-1/2
+        for (int kk = 0; kk < 3; ++kk) {
+            double wb[3], wc[3];
+            recon_weights(t + kk, 3, 0, 0.5, wm[kk]);
+            recon_weights(t + kk, 3, 0, -0.5, wp[kk]);
+            recon_weights(t + kk, 3, 1, 0.0, wb);        // q'(0)
+            recon_weights(t + kk, 3, 2, 0.0, wc);        // q''(0)
+            const double sc = 0.5 * std::sqrt(13.0 / 3.0);
+            // difference form (the weights of q' and q'' sum to 0, those of q to 1):
+            //   k = 0: cells m-2, m-1, m   -> (-w0) D0 + (-w0 - w1) D1
+            //   k = 1: cells m-1, m, m+1   -> (-w0) D1 + (w2) D2
+            //   k = 2: cells m, m+1, m+2   -> (w1 + w2) D2 + (w2) D3
+            auto diff = [&](const double* w, double& ca, double& cb) {
+                if (kk == 0) { ca = -w[0]; cb = -w[0] - w[1]; }
+                else if (kk == 1) { ca = -w[0]; cb = w[2]; }
+                else { ca = w[1] + w[2]; cb = w[2]; }
+            };
+            diff(wb, T(NU_B + 2 * kk, m), T(NU_B + 2 * kk + 1, m));
+            double s0, s1;
+            diff(wc, s0, s1);
+            T(NU_C + 2 * kk, m) = sc * s0;
+            T(NU_C + 2 * kk + 1, m) = sc * s1;
+            diff(wm[kk], T(NU_PM + 2 * kk, m), T(NU_PM + 2 * kk + 1, m));
+            diff(wp[kk], T(NU_PP + 2 * kk, m), T(NU_PP + 2 * kk + 1, m));
+        }
+        // ideal weights: the 5-cell reconstruction against the outer cells' candidates
+        for (int side = 0; side < 2; ++side) {
+            double W5[5];
+            recon_weights(t, 5, 0, side == 0 ? 0.5 : -0.5, W5);
+            const double(&w)[3][3] = side == 0 ? wm : wp;
+            const double d0 = W5[0] / w[0][0], d2 = W5[4] / w[2][2], d1 = 1.0 - d0 - d2;
+            if (!(d0 > 0.0 && d1 > 0.0 && d2 > 0.0))
+                return fail(MFC_EINVAL, "axis %d cell %lld: ideal WENO5 weight <= 0 (grid too "
+                                        "strongly stretched)", k, (long long)m);
+            const int base = side == 0 ? NU_DM : NU_DP;
+            T(base, m) = d0;
+            T(base + 1, m) = d1;
+            T(base + 2, m) = d2;
+        }
+        T(NU_INV, m) = 1.0 / h;
+    }
+    CU_TRY(cudaMemcpy(c->nu[k], tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return MFC_OK;
+}
+
 // ------------------------------------------------------------ profiling
 
 enum { K_SWEEP_X = 0, K_SWEEP_Y = 1, K_SWEEP_Z = 2, K_BC = 3, K_HALO = 4, K_EOS = 5, K_NKIND = 6 };
@@ -468,25 +653,40 @@ int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
 //
 // Every rank performs the same sequence of fused-halo operations (collective calls).
 // Operation number e (1, 2, ...) of a rank: wait until every neighbour has completed
-// operation e-1 (its flag in my flags[] >= e-1), read my ghost layers, write the
-// neighbours' ghost layers, then signal e into each neighbour's flag.  Ghosts read in
-// operation e were written in the neighbours' operation e-1; ghosts I write in
-// operation e are read by the neighbour in its operation e+1, and the neighbour read
-// the previous contents of that buffer (written 3 operations earlier, buffers rotate
-// q -> S1 -> S2 -> q) in its operation e-2, which the wait on e-1 covers.  Waits and
-// signals are stream memory operations (no spinning kernel); loopback groups on one
-// stream need neither.
+// operation e-1, read my ghost layers, write the neighbours' ghost layers, then signal
+// e to each neighbour.  Ghosts read in operation e were written in the neighbours'
+// operation e-1; ghosts I write in operation e are read by the neighbour in its
+// operation e+1, and the neighbour read the previous contents of that buffer (written
+// 3 operations earlier, buffers rotate q -> S1 -> S2 -> q) in its operation e-2, which
+// the wait on e-1 covers.  Waits and signals are stream memory operations (no
+// spinning kernel); loopback groups on one stream need neither.
+//
+// Flags: 3 slots per face, slot e % 3 is "the neighbour completed operation e"
+// (values 0 / 1).  The neighbour sets it; I wait for 1 and reset it to 0 (every slot is
+// consumed once, in order).  Neighbours are at most one operation apart (operation e+1
+// waits for the other's e), so when a neighbour next sets slot e % 3 -- at its
+// operation e+3 -- I have long reset it.  The values are the same in every step, so a
+// step captured in a CUDA graph replays correctly (mfc_rk3_steps); an epoch counter
+// compared with >= would bake one step's values into the graph.
 
 using FnStreamValue64 = CUresult(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 extern FnStreamValue64* p_wait_value;
 extern FnStreamValue64* p_write_value;
 
+// wait until every neighbour has completed operation `value` (consuming the slots of
+// every operation not awaited yet, in order)
 int peer_wait(mfc_ctx* c, cudaStream_t s, uint64_t value) {
-    for (int f = 0; f < 2 * c->D; ++f) {
-        if (c->bc[f] != BC_NEIGHBOR) continue;
-        const CUresult r = p_wait_value((CUstream)s, (CUdeviceptr)(c->flags + f),
-                                        (cuuint64_t)value, CU_STREAM_WAIT_VALUE_GEQ);
-        if (r != CUDA_SUCCESS) return fail(MFC_ECUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
+    for (uint64_t v = c->waited + 1; v <= value; ++v) {
+        if (v == 0) continue;
+        for (int f = 0; f < 2 * c->D; ++f) {
+            if (c->bc[f] != BC_NEIGHBOR) continue;
+            const CUdeviceptr slot = (CUdeviceptr)(c->flags + 3 * f + v % 3);
+            CUresult r = p_wait_value((CUstream)s, slot, 1, CU_STREAM_WAIT_VALUE_EQ);
+            if (r == CUDA_SUCCESS)
+                r = p_write_value((CUstream)s, slot, 0, CU_STREAM_WRITE_VALUE_DEFAULT);
+            if (r != CUDA_SUCCESS) return fail(MFC_ECUDA, "stream memory operation failed (%d)", (int)r);
+        }
+        c->waited = v;
     }
     return MFC_OK;
 }
@@ -496,7 +696,7 @@ int peer_signal(mfc_ctx* c, cudaStream_t s) {
     for (int f = 0; f < 2 * c->D; ++f) {
         if (c->bc[f] != BC_NEIGHBOR) continue;
         // default flags: the write is ordered after (and flushes) all prior work
-        const CUresult r = p_write_value((CUstream)s, c->peer_flag[f], (cuuint64_t)c->epoch,
+        const CUresult r = p_write_value((CUstream)s, c->peer_flag[f] + 8 * (c->epoch % 3), 1,
                                          CU_STREAM_WRITE_VALUE_DEFAULT);
         if (r != CUDA_SUCCESS) return fail(MFC_ECUDA, "cuStreamWriteValue64 failed (%d)", (int)r);
     }
@@ -628,8 +828,12 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     const dim3 grid(1, 1, (a.s_hi - a.s_lo + a.T - 1) / a.T);
     cudaError_t e;
     ProfScope ps(c, s, K_SWEEP_X + dir);
-    // kernel template order: 3, 5, or 6 = WENO5 with mapped weights
-    const int ord = (c->weno_order == 5 && c->weno_mapped) ? 6 : c->weno_order;
+    // kernel template order: 3, 5, 6 = WENO5 with mapped weights, 7 = WENO5 on a
+    // stretched axis (per-cell coefficient tables, F4)
+    const bool nu = !c->xcb[dir].empty();
+    const int ord = nu ? 7 : ((c->weno_order == 5 && c->weno_mapped) ? 6 : c->weno_order);
+    a.nu = nu ? c->nu[dir] : nullptr;
+    a.nu_ld = c->nl[dir] + 2 * kGhost;
     switch (c->N) {
         case 1: e = launch_sweep<1>(c->D, dir, mode, ord, a, grid, block, s); break;
         case 2: e = launch_sweep<2>(c->D, dir, mode, ord, a, grid, block, s); break;
@@ -1240,10 +1444,12 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
         }
     }
     // neighbours (rank = cx + px*(cy + py*cz))
+    for (int k = 0; k < 3; ++k) c->n_global[k] = grid->n_global[k];
     for (int k = 0; k < D; ++k) {
         for (int sd = 0; sd < 2; ++sd) {
             const int f = 2 * k + sd;
             c->bc[f] = bc[f];
+            c->bc_phys[f] = bc[f];
             if (c->procs[k] == 1) continue;
             int cc[3] = {c->coords[0], c->coords[1], c->coords[2]};
             cc[k] += sd ? 1 : -1;
@@ -1278,6 +1484,8 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
             if (c->bc[2 * k + sd] == BC_NEIGHBOR)
                 need += 2 * (((size_t)c->face_elems[k] * sizeof(double) + 255) / 256 * 256);
     }
+    // non-uniform grid coefficient tables, one per active axis (F4)
+    for (int k = 0; k < D; ++k) need += nu_table_bytes(c, k);
     // streamed advance_host (single-rank 3D): dense staging rings for the PCIe copies
     if (D == 3 && nranks == 1 && c->nl[2] >= 3 * kStageCzMin) {
         c->stage_cz = std::max<int64_t>(kStageCzMin, (c->nl[2] + kStreamChunks - 1) / kStreamChunks);
@@ -1358,6 +1566,10 @@ int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
         c->stage_in = (double*)w; w += kStageSlots * stage_slot_bytes(c);
         c->stage_out = (double*)w; w += kStageSlots * stage_slot_bytes(c);
     }
+    for (int k = 0; k < c->D; ++k) {
+        c->nu[k] = (double*)w;
+        w += nu_table_bytes(c, k);
+    }
     for (int f = 0; f < 6; ++f) {
         c->sendb[f] = c->recvb[f] = nullptr;
         if (f / 2 < c->D && c->bc[f] == BC_NEIGHBOR) {
@@ -1365,6 +1577,44 @@ int mfc_bind_workspace(mfc_ctx* c, void* p, size_t bytes) {
             c->sendb[f] = (double*)w; w += fb;
             c->recvb[f] = (double*)w; w += fb;
         }
+    }
+    // a rebind keeps the stretched grids: their tables move into the new workspace
+    for (int k = 0; k < c->D; ++k) {
+        if (c->xcb[k].empty()) continue;
+        const int st = upload_nu_table(c, k);
+        if (st) return st;
+    }
+    return MFC_OK;
+}
+
+int mfc_set_grid(mfc_ctx* c, int32_t dim, const double* x_cb, int64_t n) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    if (dim < 0 || dim >= c->D) return fail(MFC_EINVAL, "dim %d is not active", dim);
+    int st;
+    if ((st = need_ws(c, true))) return st;
+    if ((st = set_device(c))) return st;
+    if (c->graph) {                  // captured kernels depend on the grid
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    if (!x_cb) {
+        c->xcb[dim].clear();
+        return MFC_OK;
+    }
+    if (n != c->n_global[dim]) return fail(MFC_EINVAL, "n = %lld != n_global[%d] = %lld",
+                                           (long long)n, dim, (long long)c->n_global[dim]);
+    if (c->weno_order != 5 || c->weno_mapped)
+        return fail(MFC_EUNSUPPORTED, "stretched grids run WENO5-JS only (DESIGN.md AMB-27)");
+    std::vector<double> x(x_cb, x_cb + n + 1);
+    for (int64_t i = 0; i < n; ++i)
+        if (!(x[i + 1] > x[i]) || !std::isfinite(x[i]) || !std::isfinite(x[i + 1]))
+            return fail(MFC_EINVAL, "x_cb must be finite and strictly increasing (index %lld)",
+                        (long long)i);
+    std::vector<double> keep = std::move(c->xcb[dim]);
+    c->xcb[dim] = std::move(x);
+    if ((st = upload_nu_table(c, dim))) {
+        c->xcb[dim] = std::move(keep);
+        return st;
     }
     return MFC_OK;
 }
@@ -1379,6 +1629,8 @@ int mfc_set_stream_chunks(mfc_ctx* c, int32_t chunks) {
 int mfc_set_weno_mapped(mfc_ctx* c, int32_t on) {
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     if (on != 0 && on != 1) return fail(MFC_EINVAL, "mapped must be 0 or 1");
+    if (on && any_stretched(c))
+        return fail(MFC_EUNSUPPORTED, "stretched grids run WENO5-JS only (DESIGN.md AMB-27)");
     c->weno_mapped = on;
     if (c->graph) {                  // captured kernels depend on the weights
         cudaGraphExecDestroy(c->graph);
@@ -1390,6 +1642,8 @@ int mfc_set_weno_mapped(mfc_ctx* c, int32_t on) {
 int mfc_set_weno_order(mfc_ctx* c, int32_t order) {
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     if (order != 3 && order != 5) return fail(MFC_EINVAL, "WENO order must be 3 or 5");
+    if (order != 5 && any_stretched(c))
+        return fail(MFC_EUNSUPPORTED, "stretched grids run WENO5-JS only (DESIGN.md AMB-27)");
     c->weno_order = order;
     if (c->graph) {                  // captured kernels depend on the order
         cudaGraphExecDestroy(c->graph);
@@ -1461,12 +1715,16 @@ int mfc_max_wave_rate(mfc_ctx* c, const double* q, double* d_out, void* stream) 
     a.nz = (int32_t)c->nl[2];
     a.mat = c->mat;
     const double3 inv = make_double3(1.0 / c->dx[0], 1.0 / c->dx[1], 1.0 / c->dx[2]);
+    WaveGrid wg;
+    for (int k = 0; k < 3; ++k)   // stretched axes: the 1/dx row of the table, from cell 0
+        wg.inv[k] = (k < c->D && !c->xcb[k].empty())
+                        ? c->nu[k] + NU_INV * (c->nl[k] + 2 * kGhost) + kGhost : nullptr;
     CU_TRY(cudaMemsetAsync(d_out, 0, sizeof(double), s));
     cudaError_t e;
     switch (c->N) {
-        case 1: e = launch_wave_rate<1>(c->D, a, inv, d_out, s); break;
-        case 2: e = launch_wave_rate<2>(c->D, a, inv, d_out, s); break;
-        default: e = launch_wave_rate<3>(c->D, a, inv, d_out, s); break;
+        case 1: e = launch_wave_rate<1>(c->D, a, inv, wg, d_out, s); break;
+        case 2: e = launch_wave_rate<2>(c->D, a, inv, wg, d_out, s); break;
+        default: e = launch_wave_rate<3>(c->D, a, inv, wg, d_out, s); break;
     }
     if (e != cudaSuccess) return fail(MFC_ECUDA, "wave rate launch: %s", cudaGetErrorString(e));
     if (c->comm) NCCL_TRY(ncclAllReduce(d_out, d_out, 1, ncclFloat64, ncclMax, c->comm, s));
@@ -1527,15 +1785,23 @@ int mfc_rk3_steps(mfc_ctx* c, double* q, double dt, int64_t nsteps, void* stream
     int st = set_device(c);
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    if (c->prof || c->peer_sync) {
-        // per-launch event timing needs the plain launches; IPC-peer waits compare
-        // against per-operation values that a replayed graph could not advance
+    if (c->prof) {
+        // per-launch event timing needs the plain launches
         for (int64_t i = 0; i < nsteps; ++i)
             if ((st = rk3_group(&c, &q, 1, dt, s))) return st;
         return MFC_OK;
     }
     if (nsteps == 0) return MFC_OK;
-    if (!c->graph || c->graph_q != q || c->graph_dt != dt) {
+    // IPC peers: the captured flag slots depend on the operation phase (peer_wait).  A
+    // step that starts one awaited operation behind (epoch - waited == 1, the state
+    // every step leaves) advances both counters by 3, so one graph serves all of them;
+    // from any other state (after an exchange or an RHS call) one plain step first
+    if (c->peer_sync && c->epoch - c->waited != 1) {
+        if ((st = rk3_group(&c, &q, 1, dt, s))) return st;
+        if (--nsteps == 0) return MFC_OK;
+    }
+    const uint64_t phase = c->peer_sync ? ((c->epoch % 3) | ((c->epoch - c->waited) << 2)) : 0;
+    if (!c->graph || c->graph_q != q || c->graph_dt != dt || c->graph_phase != phase) {
         if (c->graph) {
             cudaGraphExecDestroy(c->graph);
             c->graph = nullptr;
@@ -1555,9 +1821,22 @@ int mfc_rk3_steps(mfc_ctx* c, double* q, double dt, int64_t nsteps, void* stream
         if (ei != cudaSuccess) return fail(MFC_ECUDA, "graph instantiate: %s", cudaGetErrorString(ei));
         c->graph_q = q;
         c->graph_dt = dt;
+        c->graph_phase = phase;
         c->graph_launches = c->launches;
+        // the capture advanced the host-side operation counters by one step; undo it,
+        // every launch below accounts for its own step
+        if (c->peer_sync) {
+            c->epoch -= 3;
+            c->waited -= 3;
+        }
     }
-    for (int64_t i = 0; i < nsteps; ++i) CU_TRY(cudaGraphLaunch(c->graph, s));
+    for (int64_t i = 0; i < nsteps; ++i) {
+        CU_TRY(cudaGraphLaunch(c->graph, s));
+        if (c->peer_sync) {          // the replayed step's three operations
+            c->epoch += 3;
+            c->waited += 3;
+        }
+    }
     c->launches = c->graph_launches * nsteps;
     return MFC_OK;
 }
@@ -1676,9 +1955,9 @@ int mfc_peer_export(mfc_ctx* c, double* q, void* blob) {
         p_dev_attr(&memops, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, dev) != CUDA_SUCCESS)
         return fail(MFC_ECUDA, "cuDeviceGetAttribute failed");
     if (!memops) return fail(MFC_EUNSUPPORTED, "device lacks 64-bit stream memory operations");
-    if (!c->flags) {
-        CU_TRY(cudaMalloc(&c->flags, 8 * sizeof(uint64_t)));
-        CU_TRY(cudaMemset(c->flags, 0, 8 * sizeof(uint64_t)));
+    if (!c->flags) {                 // 6 faces x 3 slots (see peer_wait)
+        CU_TRY(cudaMalloc(&c->flags, 18 * sizeof(uint64_t)));
+        CU_TRY(cudaMemset(c->flags, 0, 18 * sizeof(uint64_t)));
     }
     PeerBlob b{};
     b.magic = kPeerMagic;
@@ -1726,7 +2005,7 @@ int mfc_peer_import(mfc_ctx* c, int32_t face, const void* blob) {
     }
     const Lay L = layout_for(b.D, b.E, b.nl);
     for (int i = 0; i < 3; ++i) c->pf[face][i] = make_peer_face(c, face, (double*)base[i], L, b.nl);
-    c->peer_flag[face] = (CUdeviceptr)((uint64_t*)base[3] + (face ^ 1));
+    c->peer_flag[face] = (CUdeviceptr)((uint64_t*)base[3] + 3 * (face ^ 1));
     c->pf_set[face] = true;
     bool all = true;
     for (int f = 0; f < 2 * c->D; ++f)
@@ -1735,6 +2014,7 @@ int mfc_peer_import(mfc_ctx* c, int32_t face, const void* blob) {
         c->fused = true;
         c->peer_sync = true;
         c->epoch = 0;
+        c->waited = 0;
     }
     return MFC_OK;
 }

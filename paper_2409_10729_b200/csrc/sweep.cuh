@@ -30,6 +30,7 @@
 // assembled across the sweeps.
 #pragma once
 #include "physics.cuh"
+#include "tma.cuh"
 
 #ifndef MFC_MARCH_FEWOP
 #define MFC_MARCH_FEWOP false   // weno5_fewop in the ring marches (spills at 168 registers)
@@ -124,6 +125,17 @@ __device__ __forceinline__ void peer_copy(const PeerOut& po, int x, int y, int z
     }
 }
 
+// Non-uniform grid (F4, DESIGN.md AMB-27): per-cell coefficients of the sweep axis,
+// structure of arrays over cells -3 .. n+2 (element (c, m) at nu[c * nu_ld + m + 3]):
+//   NU_B + 2k, +1 : b_k = Δ q_k'(x_m) on the two first differences of candidate k's stencil
+//   NU_C + 2k, +1 : sqrt(13/3) c_k, c_k = Δ² q_k''/2  (beta_k = b_k² + (13/3) c_k²)
+//   NU_PM + 2k, +1: q_k(x_{m+1/2}) - v_m,   NU_PP + 2k, +1: q_k(x_{m-1/2}) - v_m
+//   NU_DM + k, NU_DP + k: ideal weights of v- and v+;   NU_INV: 1/Δ_m
+// (candidate k's differences: k = 0: (D0, D1), 1: (D1, D2), 2: (D2, D3), D_i = v_{m-1+i} -
+//  v_{m-2+i})
+enum { NU_B = 0, NU_C = 6, NU_PM = 12, NU_PP = 18, NU_DM = 24, NU_DP = 27, NU_INV = 30,
+       NU_NCOEF = 31 };
+
 struct SweepArgs {
     const double* __restrict__ q;   // stencil state (padded layout, ghosts filled)
     const double* acc;              // accumulator input (M_ACC, M_ACCN)
@@ -143,6 +155,8 @@ struct SweepArgs {
     double w, ca, cb;               // epilogue weights
     Materials mat;
     PeerOut po;                     // fused halo stores (last sweep of a stage only)
+    const double* nu;               // non-uniform coefficients of the sweep axis (ORD 7)
+    int64_t nu_ld;                  // their cell stride (n + 6)
 };
 
 // The 3D y and z marches (M_ACC, M_ACCN; E <= 8) run the fewer-op WENO (weno5_fewop) at
@@ -210,14 +224,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-template <class M, int DIR, int MODE>
+template <class M, int DIR, int MODE, int ORD = 5>
 __host__ __device__ constexpr int sweep_min_blocks() {
-    if (march_fewop<M, DIR, MODE>()) return 2;
+    if (march_fewop<M, DIR, MODE>() || ORD == 7) return 2;   // (ORD 7: 30 coefficients)
     return ((MODE == M_ACC || MODE == M_SET || MODE == M_ACCN) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
-__global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, DIR, MODE>())
+__global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, DIR, MODE, ORD>())
 sweep_kernel(const SweepArgs a) {
     constexpr int E = M::E;
     using R = RingsOf<M, DIR, MODE>;
@@ -380,6 +394,9 @@ sweep_kernel(const SweepArgs a) {
                 w[1][e] = D2;
                 w[2][e] = w[3][e];
                 w[3][e] = w[4][e];
+            } else if constexpr (ORD == 7) {      // non-uniform grid: cell j's coefficients
+                weno5_nu(w[1][e] - w[0][e], w[2][e] - w[1][e], w[3][e] - w[2][e],
+                         w[4][e] - w[3][e], w[2][e], a.nu + (j + 3), a.nu_ld, a.eps, vm[e], vp[e]);
             } else {
                 reconstruct<ORD, march_fewop<M, DIR, MODE>()>(w[0][e], w[1][e], w[2][e], w[3][e],
                                                                 w[4][e], a.eps4, a.eps, vm[e], vp[e]);
@@ -394,21 +411,23 @@ sweep_kernel(const SweepArgs a) {
                 const int cc = j - 1;
                 const int64_t c = line + (int64_t)cc * a.sS;
                 const double du = uf - uf_prev;
+                // 1/dx of cell j-1: uniform, or its own width on a stretched axis
+                const double invd = ORD == 7 ? __ldg(a.nu + NU_INV * a.nu_ld + cc + 3) : a.invd;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     double r = F_prev[e] - F[e];                 // dx * c_e
                     if (e >= M::IA) r = fma(DW ? bA[e - M::IA] : w[1][e], du, r);
                     double out;
-                    if (MODE == M_SET) out = r * a.invd;
-                    else if (MODE == M_ACC) out = fma(a.w * a.invd, r, at(ringA, ka, e));
+                    if (MODE == M_SET) out = r * invd;
+                    else if (MODE == M_ACC) out = fma(a.w * invd, r, at(ringA, ka, e));
                     else if (MODE == M_ACCN)
-                        out = fma(a.ca, at(ringN, ka, e), fma(a.w * a.invd, r, at(ringA, ka, e)));
+                        out = fma(a.ca, at(ringN, ka, e), fma(a.w * invd, r, at(ringA, ka, e)));
                     else {
                         const double qs = at(ringQ, kqs, e);
                         const double base = a.ca != 0.0
                                                 ? fma(a.ca, at(ringN, ka, e), a.cb * qs)
                                                 : a.cb * qs;
-                        out = fma(a.w * a.invd, r, base);
+                        out = fma(a.w * invd, r, base);
                     }
                     a.dst[c + e * a.sE] = out;
                 }
@@ -474,8 +493,11 @@ namespace mfc {
 #ifndef MFC_XT_MINB_BIG
 #define MFC_XT_MINB_BIG 3    // E > 8: 3 blocks too (24-48 bytes of spills, still faster: C5 x 29.1 -> 24.1 ms/step, r51)
 #endif
-template <class M>
-__host__ __device__ constexpr int x_tile_minb() { return M::E <= 8 ? MFC_XT_MINB : MFC_XT_MINB_BIG; }
+template <class M, int ORD = 5>
+__host__ __device__ constexpr int x_tile_minb() {
+    // the stretched-grid WENO (ORD 7) holds its cell's coefficients: 2 blocks, 128 registers
+    return ORD == 7 ? 2 : (M::E <= 8 ? MFC_XT_MINB : MFC_XT_MINB_BIG);
+}
 
 // RK stage base of the x sweeps (RKB): cb*q^s, plus ca*q^n when the host hands q^n over
 // (MFC_XBASE_N; otherwise the last sweep adds it, M_ACCN)
@@ -492,7 +514,7 @@ __host__ __device__ constexpr size_t x_tile_smem_doubles(int seg) {
 }
 
 template <class M, int ORD, bool RKB>
-__global__ void __launch_bounds__(256, x_tile_minb<M>())
+__global__ void __launch_bounds__(256, x_tile_minb<M, ORD>())
 sweep_x_tile(const SweepArgs a, int W) {
     constexpr int E = M::E;
     const int t = threadIdx.x;
@@ -540,7 +562,11 @@ sweep_x_tile(const SweepArgs a, int W) {
     for (int e = 0; e < E; ++e) {
         const double* r = V + e * LV + t + 1;
         double vm;
-        reconstruct<ORD, true>(r[0], r[1], v[e], r[3], r[4], a.eps4, a.eps, vm, vp[e]);
+        if constexpr (ORD == 7)            // non-uniform grid: cell x's coefficients
+            weno5_nu(r[1] - r[0], v[e] - r[1], r[3] - v[e], r[4] - r[3], v[e],
+                     a.nu + (min(x, x1) + 3), a.nu_ld, a.eps, vm, vp[e]);
+        else
+            reconstruct<ORD, true>(r[0], r[1], v[e], r[3], r[4], a.eps4, a.eps, vm, vp[e]);
         VM[e * LM + t + 1] = vm;
     }
     if (!wrap) {
@@ -550,7 +576,12 @@ sweep_x_tile(const SweepArgs a, int W) {
             const int e = right ? k - E : k;
             const double* r = V + e * LV + (right ? seg + 1 : 0);
             double bm, bp;
-            reconstruct<ORD, true>(r[0], r[1], r[2], r[3], r[4], a.eps4, a.eps, bm, bp);
+            if constexpr (ORD == 7)
+                weno5_nu(r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[2],
+                         a.nu + ((right ? min(x0 + seg, x1) : x0 - 1) + 3), a.nu_ld, a.eps,
+                         bm, bp);   // (right and x1 < x0 + seg: unused, index kept in range)
+            else
+                reconstruct<ORD, true>(r[0], r[1], r[2], r[3], r[4], a.eps4, a.eps, bm, bp);
             if (right) VPX[e] = bp;
             else VM[e * LM] = bm;
         }
@@ -585,7 +616,8 @@ sweep_x_tile(const SweepArgs a, int W) {
     if (x < x1) {
         const int ri = (wrap && t + 1 == n) ? 0 : t + 1;
         const double du = FS[E * LF + ri] - uf;
-        const double wi = a.w * a.invd;
+        const double invd = ORD == 7 ? __ldg(a.nu + NU_INV * a.nu_ld + x + 3) : a.invd;
+        const double wi = a.w * invd;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             double r = F[e] - FS[e * LF + ri];
@@ -593,7 +625,7 @@ sweep_x_tile(const SweepArgs a, int W) {
             if constexpr (RKB)
                 a.dst[row + x + e * a.sE] = fma(wi, r, xbase(a, row + x + e * a.sE));
             else
-                a.dst[row + x + e * a.sE] = r * a.invd;
+                a.dst[row + x + e * a.sE] = r * invd;
         }
     }
 }
@@ -774,6 +806,208 @@ sweep_x_pair(const SweepArgs a, int W) {
             else
                 a.dst[row + xa + 1 + e * a.sE] = r * a.invd;
         }
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// x sweep, two cells per thread, PERSISTENT with TMA tile loads (sweep_x_pair_tma).
+//
+// The same arithmetic as sweep_x_pair, segment by segment, but a block loops over row
+// segments (sid = blockIdx.x, += gridDim.x) and the raw conserved state of a segment
+// (E rows of seg cells, one 4D tensor-map box) is loaded by TMA into shared memory while
+// the block computes the previous segment: issued by one thread right after the
+// block's first barrier of segment k (the raw tile of k is converted by then), it has
+// phases 2-4 of segment k to land, and phase 1 of segment k+1 waits on the mbarrier
+// instead of on DRAM (sweep_x_pair: long-scoreboard stalls at the first use of the
+// loaded state, 16 % of stall samples, r102).  The 6 halo cells come from the tile when
+// they lie in the segment (a whole periodic row), else from global memory.  The RK
+// base operands q^s, q^n of the epilogue are read from global memory (q^s: L2 hit).
+//   raw [E][seg] : the segment's conserved state (TMA destination, 128-byte aligned)
+// followed by the shared layout of sweep_x_pair.
+// ---------------------------------------------------------------------------
+template <class M>
+__host__ __device__ constexpr size_t x_pair_tma_smem_bytes(int seg) {
+    return (size_t)M::E * seg * sizeof(double) + x_pair_smem_doubles<M>(seg) * sizeof(double) + 16;
+}
+
+template <class M, bool RKB>
+__global__ void __launch_bounds__(128, x_pair_minb<M>())
+sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int W, int nsegr,
+                 int nseg_total, int ox, int oy, int oz) {
+    constexpr int E = M::E;
+    const int t = threadIdx.x;
+    const int NT = 32 * W;
+    const int seg = 2 * NT;
+    const int n = a.nS;
+    const int LH = NT + 3, LP = NT + 1;
+    extern __shared__ __align__(128) double smx[];
+    double* const raw = smx;                                   // [E][seg]
+    double* const sm = smx + (size_t)E * seg;
+    double* const Ve = sm;                                     // [E][LH]
+    double* const Vo = sm + (size_t)E * LH;                    // [E][LH]
+    double* const FS = sm;                                     // [E+1][LP] after phase 2
+    double* const VM2 = sm + x_pair_smem_doubles<M>(seg) - (size_t)E * LP - E;   // [E][LP]
+    double* const VPX = VM2 + (size_t)E * LP;                  // [E]
+    uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + x_pair_smem_doubles<M>(seg));
+    auto V = [&](int e, int i) -> double& {
+        return (i & 1) ? Vo[e * LH + (i >> 1)] : Ve[e * LH + (i >> 1)];
+    };
+    const uint32_t tx_bytes = (uint32_t)(E * seg * sizeof(double));
+    // segment sid -> x0 and its row (y, z) = (r % nA, r / nA)
+    auto issue = [&](int sid) {
+        const int r = sid / nsegr, x0s = (sid % nsegr) * seg;
+        mbar_arrive_expect_tx(bar, tx_bytes);
+        tma_load_4d(raw, &tq, bar, ox + x0s, oy + r % a.nA, oz + r / a.nA, 0);
+    };
+    if (t == 0) {
+        tma_prefetch_desc(&tq);
+        mbar_init(bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (t == 0 && (int)blockIdx.x < nseg_total) issue(blockIdx.x);
+    uint32_t parity = 0;
+    const double wi = a.w * a.invd;
+
+    for (int sid = blockIdx.x; sid < nseg_total; sid += gridDim.x) {
+        const int rr = sid / nsegr;
+        const int x0 = (sid % nsegr) * seg;
+        const int x1 = min(x0 + seg, n);
+        const bool wrap = (a.gm.blo == 1 && a.gm.alo == n) && x0 == 0 && x1 == n && (n & 1) == 0;
+        const int tl = n / 2 - 1;
+        const int xa = x0 + 2 * t;
+        const int64_t row = a.base + (int64_t)(rr % a.nA) * a.sA + (int64_t)(rr / a.nA) * a.sB;
+
+        // cell of the tile (mapped like every stencil cell) -> primitives
+        auto tile_prim = [&](int cell, double (&v)[E]) {
+            const int cl = min(cell, x1 + 2);
+            const int sc = map_cell(cl, n, a.gm);
+            double qc[E];
+            if (sc >= x0 && sc < x0 + seg) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) qc[e] = raw[e * seg + (sc - x0)];
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) qc[e] = __ldg(a.q + row + sc + e * a.sE);
+            }
+            if (map_flip(cl, n, a.gm)) qc[M::IM] = -qc[M::IM];
+            cons_to_prim_fast<M>(qc, v, a.mat);
+        };
+
+        // 1. primitives of my two cells and of the six halo cells (tile landed)
+        mbar_wait(bar, parity);
+        parity ^= 1;
+        double v0[E], v1[E];
+        tile_prim(xa, v0);
+        tile_prim(xa + 1, v1);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            Vo[e * LH + t + 1] = v0[e];
+            Ve[e * LH + t + 2] = v1[e];
+        }
+        if (t < 6) {
+            double h[E];
+            tile_prim(t < 3 ? x0 - 3 + t : x0 + seg + t - 3, h);
+            const int i = t < 3 ? t : seg + t;
+#pragma unroll
+            for (int e = 0; e < E; ++e) V(e, i) = h[e];
+        }
+        __syncthreads();
+        // the tile is converted: load the block's next segment into it
+        if (t == 0 && sid + (int)gridDim.x < nseg_total) {
+            fence_proxy_async_smem();
+            issue(sid + gridDim.x);
+        }
+
+        // 2. WENO of both cells
+        double vm0[E], vp0[E], vp1[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double a1 = Vo[e * LH + t], a2 = Ve[e * LH + t + 1];
+            const double b5 = Vo[e * LH + t + 2], b6 = Ve[e * LH + t + 3];
+            const double D2 = a2 - a1, D3 = v0[e] - a2, D4 = v1[e] - v0[e], D5 = b5 - v1[e],
+                         D6 = b6 - b5;
+            const double s3 = D3 - D2, s4 = D4 - D3, s5 = D5 - D4, s6 = D6 - D5;
+            const double S3 = weno_S(s3, a.eps4), S4 = weno_S(s4, a.eps4), S5 = weno_S(s5, a.eps4),
+                         S6 = weno_S(s6, a.eps4);
+            double vm1;
+            weno5_fewop_s(fma(3.0, D3, -D2), D3, D4, D5, v0[e], s3, s4, s5, S3, S4, S5, vm0[e],
+                          vp0[e]);
+            weno5_fewop_s(fma(3.0, D4, -D3), D4, D5, D6, v1[e], s4, s5, s6, S4, S5, S6, vm1, vp1[e]);
+            VM2[e * LP + t + 1] = vm1;
+        }
+        if (!wrap) {
+            const int k = t - (NT - 32);
+            if (k >= 0 && k < 2 * E) {
+                const bool right = k >= E;
+                const int e = right ? k - E : k;
+                const int i0 = right ? seg + 1 : 0;
+                double r[5];
+#pragma unroll
+                for (int j = 0; j < 5; ++j) r[j] = V(e, i0 + j);
+                const double D0 = r[1] - r[0], D1 = r[2] - r[1], D2 = r[3] - r[2], D3 = r[4] - r[3];
+                const double s0 = D1 - D0, s1 = D2 - D1, s2 = D3 - D2;
+                double bm, bp;
+                weno5_fewop_s(fma(3.0, D1, -D0), D1, D2, D3, r[2], s0, s1, s2, weno_S(s0, a.eps4),
+                              weno_S(s1, a.eps4), weno_S(s2, a.eps4), bm, bp);
+                if (right) VPX[e] = bp;
+                else VM2[e * LP] = bm;
+            }
+        }
+        __syncthreads();
+
+        // 3. my faces xa-1/2 and xa+1/2
+        double FA[E], ufA, FB[E], ufB;
+        {
+            const int li = (wrap && t == 0) ? tl + 1 : t;
+            double vL[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) vL[e] = VM2[e * LP + li];
+            hllc<M, 0>(vL, vp0, a.mat, FA, ufA);
+        }
+        hllc<M, 0>(vm0, vp1, a.mat, FB, ufB);
+#pragma unroll
+        for (int e = 0; e < E; ++e) FS[e * LP + t] = FA[e];
+        FS[E * LP + t] = ufA;
+        if (!wrap && x1 == x0 + seg && t == 0) {
+            double vl[E], vr[E], FE[E], ufE;
+#pragma unroll
+            for (int e = 0; e < E; ++e) { vl[e] = VM2[e * LP + NT]; vr[e] = VPX[e]; }
+            hllc<M, 0>(vl, vr, a.mat, FE, ufE);
+#pragma unroll
+            for (int e = 0; e < E; ++e) FS[e * LP + NT] = FE[e];
+            FS[E * LP + NT] = ufE;
+        }
+        __syncthreads();
+
+        // 4. updates
+        if (xa < x1) {
+            const double du = ufB - ufA;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                double r = FA[e] - FB[e];
+                if (e >= M::IA) r = fma(v0[e], du, r);
+                if constexpr (RKB)
+                    a.dst[row + xa + e * a.sE] = fma(wi, r, xbase(a, row + xa + e * a.sE));
+                else
+                    a.dst[row + xa + e * a.sE] = r * a.invd;
+            }
+        }
+        if (xa + 1 < x1) {
+            const int ri = (wrap && t == tl) ? 0 : t + 1;
+            const double du = FS[E * LP + ri] - ufB;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                double r = FB[e] - FS[e * LP + ri];
+                if (e >= M::IA) r = fma(v1[e], du, r);
+                if constexpr (RKB)
+                    a.dst[row + xa + 1 + e * a.sE] = fma(wi, r, xbase(a, row + xa + 1 + e * a.sE));
+                else
+                    a.dst[row + xa + 1 + e * a.sE] = r * a.invd;
+            }
+        }
+        __syncthreads();      // FS (aliasing Ve/Vo) is read above; the next segment writes Ve/Vo
     }
 }
 

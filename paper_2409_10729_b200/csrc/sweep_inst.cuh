@@ -8,6 +8,10 @@
 
 #include "dispatch.h"
 
+#ifndef MFC_XPAIR_TMA
+#define MFC_XPAIR_TMA 0     // persistent TMA x pair (sweep_x_pair_tma); A/B build flag
+#endif
+
 namespace mfc {
 
 template <class M>
@@ -34,7 +38,7 @@ __global__ void __launch_bounds__(256) eos_kernel(const EosArgs a, bool to_cons)
 // (non-negative) double, which orders like an unsigned integer.
 template <class M>
 __global__ void __launch_bounds__(256) wave_rate_kernel(const EosArgs a, double3 inv_dx,
-                                                        unsigned long long* out) {
+                                                        WaveGrid wg, unsigned long long* out) {
     __shared__ double red[256];
     const int64_t n = (int64_t)a.nx * a.ny * a.nz;
     double m = 0.0;
@@ -56,9 +60,14 @@ __global__ void __launch_bounds__(256) wave_rate_kernel(const EosArgs a, double3
             P = fma(v[M::IA + f], a.mat.Pi[f], P);
         }
         const double cs = sqrt(fma(G + 1.0, v[M::IE], P) / (rho * G));
+        // 1/dx per axis: uniform, or the cell's own width on a stretched axis (F4)
+        const int ijk[3] = {i, j, k};
         const double idx[3] = {inv_dx.x, inv_dx.y, inv_dx.z};
 #pragma unroll
-        for (int d = 0; d < M::D; ++d) m = fmax(m, (fabs(v[M::IM + d]) + cs) * idx[d]);
+        for (int d = 0; d < M::D; ++d) {
+            const double id = wg.inv[d] ? __ldg(wg.inv[d] + ijk[d]) : idx[d];
+            m = fmax(m, (fabs(v[M::IM + d]) + cs) * id);
+        }
     }
     red[threadIdx.x] = m;
     __syncthreads();
@@ -113,6 +122,34 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
             // (128-cell segments: C3 x 2.15 -> 2.28 ms per step, r93)
             const int W = (int)std::min<int64_t>(4, (a.nS + 63) / 64);
             const int nseg = (a.nS + 64 * W - 1) / (64 * W);
+            if (MFC_XPAIR_TMA) {
+                // persistent blocks, the next segment's tile loaded by TMA (sweep_x_pair_tma)
+                const int64_t X = a.sA, Y = a.sB / a.sA, Z = a.sE / a.sB;
+                const int ox = (int)(a.base % X), oy = (int)((a.base / X) % Y),
+                          oz = (int)(a.base / (X * Y));
+                const int total = nseg * a.nA * a.nB;
+                const size_t smem = x_pair_tma_smem_bytes<M>(64 * W);
+                int st;
+                if ((st = set_smem_attr(sweep_x_pair_tma<M, false>, smem)) ||
+                    (st = set_smem_attr(sweep_x_pair_tma<M, true>, smem)))
+                    return (cudaError_t)st;
+                CUtensorMap tm;
+                cudaError_t e = encode_state_map(&tm, a.q, X, Y, Z, M::E, 64 * W);
+                if (e != cudaSuccess) return e;
+                int dev = 0, nsm = 0, occ = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                if (mode == M_SET)
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_x_pair_tma<M, false>, 32 * W, smem);
+                else
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_x_pair_tma<M, true>, 32 * W, smem);
+                const int grid = (int)std::min<int64_t>(total, (int64_t)nsm * std::max(occ, 1));
+                if (mode == M_SET)
+                    sweep_x_pair_tma<M, false><<<grid, 32 * W, smem, s>>>(tm, a, W, nseg, total, ox, oy, oz);
+                else
+                    sweep_x_pair_tma<M, true><<<grid, 32 * W, smem, s>>>(tm, a, W, nseg, total, ox, oy, oz);
+                return cudaGetLastError();
+            }
             const size_t smem = sizeof(double) * x_pair_smem_doubles<M>(64 * W);
             int st;
             if ((st = set_smem_attr(sweep_x_pair<M, false>, smem)) ||
@@ -193,20 +230,21 @@ template <>
 cudaError_t launch_sweep<MFC_NF>(int D, int DIR, int mode, int order, const SweepArgs& a, dim3 g,
                                  dim3 b, cudaStream_t s) {
     if (order == 3) return launch_order<3>(D, DIR, mode, a, g, b, s);
+    if (order == 7) return launch_order<7>(D, DIR, mode, a, g, b, s);   // WENO5, stretched
     if (order == 6) return launch_order<6>(D, DIR, mode, a, g, b, s);   // WENO5-M
     return launch_order<5>(D, DIR, mode, a, g, b, s);
 }
 
 template <>
-cudaError_t launch_wave_rate<MFC_NF>(int D, const EosArgs& a, double3 inv_dx, double* out,
-                                     cudaStream_t s) {
+cudaError_t launch_wave_rate<MFC_NF>(int D, const EosArgs& a, double3 inv_dx, const WaveGrid& wg,
+                                     double* out, cudaStream_t s) {
     const int64_t n = (int64_t)a.nx * a.ny * a.nz;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
     auto* o = reinterpret_cast<unsigned long long*>(out);
     switch (D) {
-        case 1: wave_rate_kernel<Model<MFC_NF, 1>><<<blocks, 256, 0, s>>>(a, inv_dx, o); break;
-        case 2: wave_rate_kernel<Model<MFC_NF, 2>><<<blocks, 256, 0, s>>>(a, inv_dx, o); break;
-        case 3: wave_rate_kernel<Model<MFC_NF, 3>><<<blocks, 256, 0, s>>>(a, inv_dx, o); break;
+        case 1: wave_rate_kernel<Model<MFC_NF, 1>><<<blocks, 256, 0, s>>>(a, inv_dx, wg, o); break;
+        case 2: wave_rate_kernel<Model<MFC_NF, 2>><<<blocks, 256, 0, s>>>(a, inv_dx, wg, o); break;
+        case 3: wave_rate_kernel<Model<MFC_NF, 3>><<<blocks, 256, 0, s>>>(a, inv_dx, wg, o); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -30,7 +30,7 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ES
 
 EXPORTED = [
     "mfc_init", "mfc_get_layout", "mfc_get_neighbors", "mfc_bind_workspace", "mfc_set_weno_eps",
-    "mfc_set_weno_order", "mfc_set_weno_mapped",
+    "mfc_set_weno_order", "mfc_set_weno_mapped", "mfc_set_grid",
     "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
     "mfc_rk3_steps", "mfc_max_wave_rate", "mfc_cfl_dt",
     "mfc_advance_host", "mfc_set_stream_chunks", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
@@ -79,6 +79,7 @@ def _load():
         "mfc_set_weno_eps": [vp, dbl],
         "mfc_set_weno_order": [vp, i32],
         "mfc_set_weno_mapped": [vp, i32],
+        "mfc_set_grid": [vp, i32, ctypes.POINTER(dbl), i64],
         "mfc_prim_to_cons": [vp, vp, vp, vp],
         "mfc_cons_to_prim": [vp, vp, vp, vp],
         "mfc_halo_exchange": [vp, vp, vp],
@@ -220,6 +221,20 @@ class Solver:
         nbytes = self.layout.workspace_bytes
         self.workspace = torch.empty((nbytes + 7) // 8, dtype=torch.float64, device=self.device)
         _check(lib.mfc_bind_workspace(h, _ptr(self.workspace), nbytes), "mfc_bind_workspace")
+        # stretched axes (F4): the global cell boundaries of each
+        for k, xb in enumerate(getattr(problem, "x_cb", None) or ()):
+            if xb is not None and k < problem.ndim:
+                self.set_grid(k, xb)
+
+    def set_grid(self, dim: int, x_cb=None):
+        """Non-uniform cell boundaries of the GLOBAL axis dim (n_global+1 increasing
+        values), or None for the uniform spacing (mfc_set_grid)."""
+        if x_cb is None:
+            _check(lib.mfc_set_grid(self._h, int(dim), None, 0), "mfc_set_grid")
+            return
+        x = np.ascontiguousarray(x_cb, dtype=np.float64)
+        _check(lib.mfc_set_grid(self._h, int(dim), x.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                x.size - 1), "mfc_set_grid")
 
     # ------------------------------------------------------------- buffers
     def empty_state(self) -> torch.Tensor:

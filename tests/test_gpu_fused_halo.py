@@ -174,6 +174,7 @@ def _ipc_worker(rank, world, port, procs, nsteps, out_dir):
     lo, n = L.lo_global, L.n_local
     qd = s.state_from_cons(q[:, lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]])
     s.attach_fused_halo(qd)
+    q0 = s.interior(qd).clone()
     rhs = s.rhs(qd)
     s.halo_exchange(qd)
     for _ in range(nsteps):
@@ -181,6 +182,15 @@ def _ipc_worker(rank, world, port, procs, nsteps, out_dir):
     T.cuda.synchronize()
     np.save(os.path.join(out_dir, f"rhs{rank}.npy"), s.interior(rhs).cpu().numpy())
     np.save(os.path.join(out_dir, f"q{rank}.npy"), s.interior(qd).cpu().numpy())
+    # the same steps replayed from a CUDA graph (F1: stream memory operations captured;
+    # the flag slots repeat every step), from the same initial state of the registered
+    # buffer, in two calls (graph re-used across calls)
+    s.interior(qd).copy_(q0)
+    s.halo_exchange(qd)
+    s.rk3_steps(qd, dt, 1)
+    s.rk3_steps(qd, dt, nsteps - 1)
+    T.cuda.synchronize()
+    np.save(os.path.join(out_dir, f"qg{rank}.npy"), s.interior(qd).cpu().numpy())
     np.save(os.path.join(out_dir, f"lo{rank}.npy"), np.array(lo + n))
     dist.barrier()
     s.close()
@@ -190,7 +200,7 @@ def _ipc_worker(rank, world, port, procs, nsteps, out_dir):
 @pytest.mark.parametrize("procs", [(1, 1, 2), (1, 2, 1)])
 def test_ipc_peer_two_processes_bitwise(procs, tmp_path):
     import torch.multiprocessing as mp
-    world, nsteps = 2, 3
+    world, nsteps = 2, 5
     ctx = mp.get_context("spawn")
     port = _free_port()
     ps = [ctx.Process(target=_ipc_worker, args=(r, world, port, procs, nsteps, str(tmp_path)))
@@ -215,6 +225,7 @@ def test_ipc_peer_two_processes_bitwise(procs, tmp_path):
         sl = (slice(None), slice(lo2, lo2 + n2), slice(lo1, lo1 + n1), slice(lo0, lo0 + n0))
         r_f[sl] = np.load(tmp_path / f"rhs{r}.npy")
         q_f[sl] = np.load(tmp_path / f"q{r}.npy")
+        assert np.array_equal(np.load(tmp_path / f"qg{r}.npy"), q_f[sl])   # graph == steps
     assert np.array_equal(r_f, r_ref)
     assert np.array_equal(q_f, q_ref)
     check_against_oracle(f"IPC 2 processes procs={procs} " + pb.name, pb, v, q, r_f, q_f, dt,

@@ -230,18 +230,42 @@ __host__ __device__ constexpr int sweep_min_blocks() {
     return ((MODE == M_ACC || MODE == M_SET || MODE == M_ACCN) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
 
+// TMA rings (MFC_MARCH_TMA): the 3D y/z accumulate marches fill their per-warp rings
+// with cp.async.bulk.tensor boxes of 32 lanes x E equations (one box per operand and
+// step, issued by lane 0 of the warp, completion on one mbarrier per ring slot) instead
+// of E per-thread cp.async of 8 bytes per operand and step.
+#ifndef MFC_MARCH_TMA
+#define MFC_MARCH_TMA 0
+#endif
+template <class M, int DIR, int MODE, int ORD>
+__host__ __device__ constexpr bool march_tma() {
+    return MFC_MARCH_TMA && M::D == 3 && DIR >= 1 && (MODE == M_ACC || MODE == M_ACCN) && ORD != 7;
+}
+// tensor maps of the marches' streamed operands (state, accumulator, q^n) and the
+// padded coordinates of interior cell (0, 0, 0)
+struct MarchMaps {
+    CUtensorMap q, acc, qn;
+    int32_t ox, oy, oz;
+};
+
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
 __global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, DIR, MODE, ORD>())
-sweep_kernel(const SweepArgs a) {
+sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
     constexpr int E = M::E;
     using R = RingsOf<M, DIR, MODE>;
-    extern __shared__ double smem[];
+    constexpr bool TMA = march_tma<M, DIR, MODE, ORD>();
+    extern __shared__ __align__(128) double smem[];
     constexpr int nth = sweep_nth<M, MODE>();            // == blockDim.x * blockDim.y
     const int tid = threadIdx.y * 32 + threadIdx.x;      // blockDim.x == 32
-    double* const ringQ = smem + tid;                       // QS slots
-    double* const ringA = ringQ + R::QS * E * nth;          // AS slots
-    double* const ringN = ringA + R::AS * E * nth;          // NS slots
-    auto at = [&](double* ring, int slot, int e) -> double& { return ring[(slot * E + e) * nth]; };
+    // cp.async rings: element (slot, e) of thread t at [(slot*E + e)*nth + t];
+    // TMA rings: per warp w, [slot][E][32] (a box lands contiguously), element at
+    // [w*SLOTS*E*32 + (slot*E + e)*32 + lane] for the slot of the respective ring
+    constexpr int RS = TMA ? 32 : nth;                      // row stride of a ring
+    double* const wbase = TMA ? smem + (size_t)threadIdx.y * R::SLOTS * E * 32 : smem;
+    double* const ringQ = wbase + (TMA ? threadIdx.x : tid);   // QS slots
+    double* const ringA = ringQ + R::QS * E * RS;           // AS slots
+    double* const ringN = ringA + R::AS * E * RS;           // NS slots
+    auto at = [&](double* ring, int slot, int e) -> double& { return ring[(slot * E + e) * RS]; };
 
     // warp-lines (32 consecutive lines along the lane axis A) are numbered A-chunk
     // fastest, and a block's warps take consecutive warp-lines: 2D / 1D grids (nB == 1)
@@ -251,6 +275,18 @@ sweep_kernel(const SweepArgs a) {
     const int ia = (wl % nAw) * 32 + threadIdx.x;
     const int ib = wl / nAw;
     if (ia >= a.nA || ib >= a.nB) return;                   // no block-level sync below
+    // TMA: ring slot barriers of this warp (after the ring rows in the dynamic smem)
+    uint64_t* const wbar = reinterpret_cast<uint64_t*>(smem + (size_t)(nth / 32) * R::SLOTS * E * 32) +
+                           threadIdx.y * 4;
+    if constexpr (TMA) {
+        if (threadIdx.x == 0) {
+            for (int k = 0; k <= R::PD; ++k) mbar_init(wbar + k, 1);
+            mbar_fence_init();
+        }
+        __syncwarp(__activemask());
+    }
+    const int ia0 = ia - threadIdx.x;                       // the warp's first lane
+    uint32_t tma_par = 0;                                   // phase parity per slot (bit k)
     const int s0 = a.s_lo + blockIdx.z * a.T;
     const int s1 = min(s0 + a.T, a.s_hi);   // cells s0 .. s1-1 are updated
     const int64_t line = a.base + (int64_t)ia * a.sA + (int64_t)ib * a.sB;
@@ -277,14 +313,41 @@ sweep_kernel(const SweepArgs a) {
     // group for step j (issued PD steps earlier): state of cell j+2 -> state slot sq,
     // epilogue operands of cell j-1 -> operand slot sa.  Slots: state cell c at
     // (c+3) % QS, operands at (c+3) % OS.
+    // TMA box of cell `cell` along the sweep for this warp's 32 lanes (all E equations)
+    auto tma_fetch = [&](const CUtensorMap* map, double* slot_base, uint64_t* bar, int cell) {
+        const int sc = map_cell(cell, a.nS, a.gm);
+        const int cy = DIR == 1 ? mm.oy + sc : mm.oy + ib;
+        const int cz = DIR == 2 ? mm.oz + sc : mm.oz + ib;
+        tma_load_4d(slot_base, map, bar, mm.ox + ia0, cy, cz, 0);
+    };
     auto issue = [&](int j, int sq, int sa) {
-        if (j + 2 <= s1 + 2) fetch(ringQ, sq, q, j + 2);
-        const int c = j - 1;
-        if (c >= s0 && c < s1) {
-            if (R::AS) fetch(ringA, sa, a.acc, c);
-            if (R::NS && a.ca != 0.0) fetch(ringN, sa, a.qn, c);
+        if constexpr (TMA) {
+            // slot sq == sa for these marches (QS == AS == NS == PD + 1); lane 0 of the
+            // warp issues after every lane has read the slot's previous contents
+            __syncwarp(__activemask());
+            if (threadIdx.x == 0) {
+                const int c = j - 1;
+                const bool st = j <= s1;              // (cells past s1+2 are never read)
+                const bool ops = c >= s0 && c < s1;
+                const bool qn = R::NS && a.ca != 0.0 && ops;
+                const uint32_t bytes = (uint32_t)(E * 32 * sizeof(double)) *
+                                       ((st ? 1u : 0u) + (R::AS && ops ? 1u : 0u) + (qn ? 1u : 0u));
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(wbar + sq, bytes);
+                double* const wb = wbase;
+                if (st) tma_fetch(&mm.q, wb + (size_t)sq * E * 32, wbar + sq, j + 2);
+                if (R::AS && ops) tma_fetch(&mm.acc, wb + (size_t)(R::QS + sa) * E * 32, wbar + sq, c);
+                if (qn) tma_fetch(&mm.qn, wb + (size_t)(R::QS + R::AS + sa) * E * 32, wbar + sq, c);
+            }
+        } else {
+            if (j + 2 <= s1 + 2) fetch(ringQ, sq, q, j + 2);
+            const int c = j - 1;
+            if (c >= s0 && c < s1) {
+                if (R::AS) fetch(ringA, sa, a.acc, c);
+                if (R::NS && a.ca != 0.0) fetch(ringN, sa, a.qn, c);
+            }
+            cp_async_commit();
         }
-        cp_async_commit();
     };
     auto inc = [](int k, int n) { return k + 1 == n ? 0 : k + 1; };
 
@@ -353,8 +416,14 @@ sweep_kernel(const SweepArgs a) {
     double uf_prev = 0.0;
 
     for (int j = s0 - 1; j <= s1; ++j) {
-        if constexpr (R::PD == 2) cp_async_wait_1();   // group of step j has landed
-        else cp_async_wait_all();
+        if constexpr (TMA) {                          // the boxes of step j have landed
+            mbar_wait(wbar + kq % (R::PD + 1), (tma_par >> (kq % (R::PD + 1))) & 1u);
+            tma_par ^= 1u << (kq % (R::PD + 1));
+        } else if constexpr (R::PD == 2) {
+            cp_async_wait_1();                        // group of step j has landed
+        } else {
+            cp_async_wait_all();
+        }
         issue(j + R::PD, kqf, kaf);
         if constexpr (!DW) {
 #pragma unroll
@@ -459,7 +528,17 @@ sweep_kernel(const SweepArgs a) {
         ka = inc(ka, R::OS);
         kaf = inc(kaf, R::OS);
     }
-    cp_async_wait_all();
+    if constexpr (TMA) {
+        // the PD boxes issued for steps past the segment end: wait so that no TMA write
+        // is in flight into this block's shared memory when the warp exits
+        for (int i = 0; i < R::PD; ++i) {
+            mbar_wait(wbar + kq % (R::PD + 1), (tma_par >> (kq % (R::PD + 1))) & 1u);
+            tma_par ^= 1u << (kq % (R::PD + 1));
+            kq = inc(kq, R::QS);
+        }
+    } else {
+        cp_async_wait_all();
+    }
 }
 
 }  // namespace mfc
@@ -826,13 +905,19 @@ sweep_x_pair(const SweepArgs a, int W) {
 //   raw [E][seg] : the segment's conserved state (TMA destination, 128-byte aligned)
 // followed by the shared layout of sweep_x_pair.
 // ---------------------------------------------------------------------------
+#ifndef MFC_XPAIR_TMA_NBUF
+#define MFC_XPAIR_TMA_NBUF 2      // raw tiles per block: 2 = double buffer (the epilogue
+#endif                            // reads q^s from its tile; 3 blocks/SM at 57 KB)
 template <class M>
 __host__ __device__ constexpr size_t x_pair_tma_smem_bytes(int seg) {
-    return (size_t)M::E * seg * sizeof(double) + x_pair_smem_doubles<M>(seg) * sizeof(double) + 16;
+    return (size_t)MFC_XPAIR_TMA_NBUF * M::E * seg * sizeof(double) +
+           x_pair_smem_doubles<M>(seg) * sizeof(double) + 16 * MFC_XPAIR_TMA_NBUF;
 }
+template <class M>
+__host__ __device__ constexpr int x_pair_tma_minb() { return MFC_XPAIR_TMA_NBUF == 2 ? 3 : x_pair_minb<M>(); }
 
 template <class M, bool RKB>
-__global__ void __launch_bounds__(128, x_pair_minb<M>())
+__global__ void __launch_bounds__(128, x_pair_tma_minb<M>())
 sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int W, int nsegr,
                  int nseg_total, int ox, int oy, int oz) {
     constexpr int E = M::E;
@@ -841,36 +926,44 @@ sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int 
     const int seg = 2 * NT;
     const int n = a.nS;
     const int LH = NT + 3, LP = NT + 1;
+    constexpr int NB = MFC_XPAIR_TMA_NBUF;
     extern __shared__ __align__(128) double smx[];
-    double* const raw = smx;                                   // [E][seg]
-    double* const sm = smx + (size_t)E * seg;
+    double* const raw0 = smx;                                  // [NB][E][seg]
+    double* const sm = smx + (size_t)NB * E * seg;
     double* const Ve = sm;                                     // [E][LH]
     double* const Vo = sm + (size_t)E * LH;                    // [E][LH]
     double* const FS = sm;                                     // [E+1][LP] after phase 2
     double* const VM2 = sm + x_pair_smem_doubles<M>(seg) - (size_t)E * LP - E;   // [E][LP]
     double* const VPX = VM2 + (size_t)E * LP;                  // [E]
-    uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + x_pair_smem_doubles<M>(seg));
+    uint64_t* const bar0 = reinterpret_cast<uint64_t*>(sm + x_pair_smem_doubles<M>(seg));
     auto V = [&](int e, int i) -> double& {
         return (i & 1) ? Vo[e * LH + (i >> 1)] : Ve[e * LH + (i >> 1)];
     };
     const uint32_t tx_bytes = (uint32_t)(E * seg * sizeof(double));
     // segment sid -> x0 and its row (y, z) = (r % nA, r / nA)
-    auto issue = [&](int sid) {
+    auto issue = [&](int sid, int b) {
         const int r = sid / nsegr, x0s = (sid % nsegr) * seg;
-        mbar_arrive_expect_tx(bar, tx_bytes);
-        tma_load_4d(raw, &tq, bar, ox + x0s, oy + r % a.nA, oz + r / a.nA, 0);
+        mbar_arrive_expect_tx(bar0 + b, tx_bytes);
+        tma_load_4d(raw0 + (size_t)b * E * seg, &tq, bar0 + b, ox + x0s, oy + r % a.nA,
+                    oz + r / a.nA, 0);
     };
     if (t == 0) {
         tma_prefetch_desc(&tq);
-        mbar_init(bar, 1);
+        for (int b = 0; b < NB; ++b) mbar_init(bar0 + b, 1);
         mbar_fence_init();
     }
     __syncthreads();
-    if (t == 0 && (int)blockIdx.x < nseg_total) issue(blockIdx.x);
-    uint32_t parity = 0;
+    if (t == 0)
+        for (int b = 0; b < NB; ++b)
+            if ((int)(blockIdx.x + b * gridDim.x) < nseg_total) issue(blockIdx.x + b * gridDim.x, b);
+    uint32_t parity = 0;                  // phase parity of the current buffer's barrier
     const double wi = a.w * a.invd;
 
-    for (int sid = blockIdx.x; sid < nseg_total; sid += gridDim.x) {
+    int it = 0;
+    for (int sid = blockIdx.x; sid < nseg_total; sid += gridDim.x, ++it) {
+        const int buf = NB == 2 ? (it & 1) : 0;
+        double* const raw = raw0 + (size_t)buf * E * seg;
+        uint64_t* const bar = bar0 + buf;
         const int rr = sid / nsegr;
         const int x0 = (sid % nsegr) * seg;
         const int x1 = min(x0 + seg, n);
@@ -879,6 +972,15 @@ sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int 
         const int xa = x0 + 2 * t;
         const int64_t row = a.base + (int64_t)(rr % a.nA) * a.sA + (int64_t)(rr / a.nA) * a.sB;
 
+        // RK stage base of my cell x: cb*q^s (+ ca*q^n); q^s from the tile when it is kept
+        // to the epilogue (double buffer), else re-read (L2)
+        // (single buffer: the tile is kept when the block has no next segment to load)
+        const bool kept = NB == 2 || sid + (int)gridDim.x >= nseg_total;
+        auto tbase = [&](int x, int e) -> double {
+            const double qs = kept ? raw[e * seg + (x - x0)] : __ldg(a.q + row + x + e * a.sE);
+            const double b = a.cb * qs;
+            return (a.qn != nullptr && a.ca != 0.0) ? fma(a.ca, __ldg(a.qn + row + x + e * a.sE), b) : b;
+        };
         // cell of the tile (mapped like every stencil cell) -> primitives
         auto tile_prim = [&](int cell, double (&v)[E]) {
             const int cl = min(cell, x1 + 2);
@@ -897,7 +999,15 @@ sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int 
 
         // 1. primitives of my two cells and of the six halo cells (tile landed)
         mbar_wait(bar, parity);
-        parity ^= 1;
+        if (NB == 1 || buf == 1) parity ^= 1;     // each buffer's barrier completes once
+                                                  // per NB segments
+        if constexpr (RKB) {
+            // q^n of my cells, read in the epilogue: start it towards L1 now
+            if (a.qn != nullptr && a.ca != 0.0 && xa < x1)
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.qn + row + xa + e * a.sE));
+        }
         double v0[E], v1[E];
         tile_prim(xa, v0);
         tile_prim(xa + 1, v1);
@@ -914,10 +1024,10 @@ sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int 
             for (int e = 0; e < E; ++e) V(e, i) = h[e];
         }
         __syncthreads();
-        // the tile is converted: load the block's next segment into it
-        if (t == 0 && sid + (int)gridDim.x < nseg_total) {
+        // single buffer: the tile is converted, load the block's next segment into it
+        if (NB == 1 && t == 0 && sid + (int)gridDim.x < nseg_total) {
             fence_proxy_async_smem();
-            issue(sid + gridDim.x);
+            issue(sid + gridDim.x, 0);
         }
 
         // 2. WENO of both cells
@@ -989,7 +1099,7 @@ sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int 
                 double r = FA[e] - FB[e];
                 if (e >= M::IA) r = fma(v0[e], du, r);
                 if constexpr (RKB)
-                    a.dst[row + xa + e * a.sE] = fma(wi, r, xbase(a, row + xa + e * a.sE));
+                    a.dst[row + xa + e * a.sE] = fma(wi, r, tbase(xa, e));
                 else
                     a.dst[row + xa + e * a.sE] = r * a.invd;
             }
@@ -1002,12 +1112,17 @@ sweep_x_pair_tma(const __grid_constant__ CUtensorMap tq, const SweepArgs a, int 
                 double r = FB[e] - FS[e * LP + ri];
                 if (e >= M::IA) r = fma(v1[e], du, r);
                 if constexpr (RKB)
-                    a.dst[row + xa + 1 + e * a.sE] = fma(wi, r, xbase(a, row + xa + 1 + e * a.sE));
+                    a.dst[row + xa + 1 + e * a.sE] = fma(wi, r, tbase(xa + 1, e));
                 else
                     a.dst[row + xa + 1 + e * a.sE] = r * a.invd;
             }
         }
         __syncthreads();      // FS (aliasing Ve/Vo) is read above; the next segment writes Ve/Vo
+        // double buffer: this tile is free now (its last reads were the RK bases above)
+        if (NB == 2 && t == 0 && sid + 2 * (int)gridDim.x < nseg_total) {
+            fence_proxy_async_smem();
+            issue(sid + 2 * gridDim.x, buf);
+        }
     }
 }
 

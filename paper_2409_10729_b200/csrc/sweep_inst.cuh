@@ -104,10 +104,26 @@ static cudaError_t launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t 
     b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
     const int64_t warp_lines = (int64_t)((a.nA + 31) / 32) * a.nB;
     g = dim3((unsigned)((warp_lines + b.y - 1) / b.y), 1, g.z);
-    const size_t smem = sweep_smem_per_thread<M, DIR, MODE>() * NTH;
+    constexpr bool TMA = march_tma<M, DIR, MODE, ORD>();
+    // + the TMA rings' slot barriers (<= 4 per warp)
+    const size_t smem = sweep_smem_per_thread<M, DIR, MODE>() * NTH + (TMA ? 32 * (NTH / 32) : 0);
     const int st = set_smem_attr(sweep_kernel<M, DIR, MODE, ORD, PEER>, smem);
     if (st) return (cudaError_t)st;
-    sweep_kernel<M, DIR, MODE, ORD, PEER><<<g, b, smem, s>>>(a);
+    MarchMaps mm{};
+    if constexpr (TMA) {
+        // padded extents and the interior origin from the strides (x unit stride)
+        const int64_t X = DIR == 1 ? a.sS : a.sB, XY = DIR == 1 ? a.sB : a.sS;
+        const int64_t Y = XY / X, Z = a.sE / XY;
+        mm.ox = (int32_t)(a.base % X);
+        mm.oy = (int32_t)((a.base / X) % Y);
+        mm.oz = (int32_t)(a.base / XY);
+        cudaError_t e;
+        if ((e = encode_state_map(&mm.q, a.q, X, Y, Z, M::E, 32)) != cudaSuccess ||
+            (e = encode_state_map(&mm.acc, a.acc ? a.acc : a.q, X, Y, Z, M::E, 32)) != cudaSuccess ||
+            (e = encode_state_map(&mm.qn, a.qn ? a.qn : a.q, X, Y, Z, M::E, 32)) != cudaSuccess)
+            return e;
+    }
+    sweep_kernel<M, DIR, MODE, ORD, PEER><<<g, b, smem, s>>>(a, mm);
     return cudaGetLastError();
 }
 
@@ -133,6 +149,10 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                 if ((st = set_smem_attr(sweep_x_pair_tma<M, false>, smem)) ||
                     (st = set_smem_attr(sweep_x_pair_tma<M, true>, smem)))
                     return (cudaError_t)st;
+                cudaFuncSetAttribute(sweep_x_pair_tma<M, false>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+                cudaFuncSetAttribute(sweep_x_pair_tma<M, true>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100);
                 CUtensorMap tm;
                 cudaError_t e = encode_state_map(&tm, a.q, X, Y, Z, M::E, 64 * W);
                 if (e != cudaSuccess) return e;
@@ -143,7 +163,10 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_x_pair_tma<M, false>, 32 * W, smem);
                 else
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_x_pair_tma<M, true>, 32 * W, smem);
-                const int grid = (int)std::min<int64_t>(total, (int64_t)nsm * std::max(occ, 1));
+                // MFC_XPAIR_TMA == 2: one segment per block (not persistent), the tile kept
+                // in shared memory for the epilogue's RK base
+                const int grid = MFC_XPAIR_TMA == 2 ? total
+                                                    : (int)std::min<int64_t>(total, (int64_t)nsm * std::max(occ, 1));
                 if (mode == M_SET)
                     sweep_x_pair_tma<M, false><<<grid, 32 * W, smem, s>>>(tm, a, W, nseg, total, ox, oy, oz);
                 else

@@ -213,8 +213,17 @@ constexpr size_t sweep_smem_per_thread() { return (size_t)RingsOf<M, DIR, MODE>:
 // Threads per block of the ring sweeps (a compile-time constant so that ring offsets
 // fold into instruction immediates): 128, or 64 where 12 ring slots of E > 9 doubles
 // would not leave room for two blocks per SM.
-template <class M, int MODE>
-__host__ __device__ constexpr int sweep_nth() { return (MODE == M_RKINIT && M::E > 9) ? 64 : 128; }
+#ifndef MFC_FEWOP_NTH
+#define MFC_FEWOP_NTH 128   // threads per block of the fewer-op y/z marches
+#endif
+#ifndef MFC_FEWOP_MINB
+#define MFC_FEWOP_MINB 2    // and their resident blocks per SM (2 x 128 at <= 255 registers)
+#endif
+template <class M, int DIR, int MODE>
+__host__ __device__ constexpr int sweep_nth() {
+    return march_fewop<M, DIR, MODE>() ? MFC_FEWOP_NTH
+                                       : ((MODE == M_RKINIT && M::E > 9) ? 64 : 128);
+}
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -226,6 +235,7 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 
 template <class M, int DIR, int MODE, int ORD = 5>
 __host__ __device__ constexpr int sweep_min_blocks() {
+    if (march_fewop<M, DIR, MODE>() && ORD != 7) return MFC_FEWOP_MINB;
     if (march_fewop<M, DIR, MODE>() || ORD == 7) return 2;   // (ORD 7: 30 coefficients)
     return ((MODE == M_ACC || MODE == M_SET || MODE == M_ACCN) && M::E <= 8) ? MFC_ACC_MINB : 2;
 }
@@ -249,13 +259,13 @@ struct MarchMaps {
 };
 
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
-__global__ void __launch_bounds__(sweep_nth<M, MODE>(), sweep_min_blocks<M, DIR, MODE, ORD>())
+__global__ void __launch_bounds__(sweep_nth<M, DIR, MODE>(), sweep_min_blocks<M, DIR, MODE, ORD>())
 sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
     constexpr int E = M::E;
     using R = RingsOf<M, DIR, MODE>;
     constexpr bool TMA = march_tma<M, DIR, MODE, ORD>();
     extern __shared__ __align__(128) double smem[];
-    constexpr int nth = sweep_nth<M, MODE>();            // == blockDim.x * blockDim.y
+    constexpr int nth = sweep_nth<M, DIR, MODE>();            // == blockDim.x * blockDim.y
     const int tid = threadIdx.y * 32 + threadIdx.x;      // blockDim.x == 32
     // cp.async rings: element (slot, e) of thread t at [(slot*E + e)*nth + t];
     // TMA rings: per warp w, [slot][E][32] (a box lands contiguously), element at
@@ -415,6 +425,11 @@ sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
     double F_prev[E];      // flux at face j-3/2
     double uf_prev = 0.0;
 
+#ifdef MFC_MARCH_UNROLL
+#define MFC_STR_(x) #x
+#define MFC_UNROLL_(n) _Pragma(MFC_STR_(unroll n))
+    MFC_UNROLL_(MFC_MARCH_UNROLL)
+#endif
     for (int j = s0 - 1; j <= s1; ++j) {
         if constexpr (TMA) {                          // the boxes of step j have landed
             mbar_wait(wbar + kq % (R::PD + 1), (tma_par >> (kq % (R::PD + 1))) & 1u);

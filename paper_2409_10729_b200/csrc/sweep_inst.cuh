@@ -100,7 +100,7 @@ static int set_smem_attr(K* kernel, size_t smem) {
 
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
 static cudaError_t launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
-    constexpr int NTH = sweep_nth<M, MODE>();
+    constexpr int NTH = sweep_nth<M, DIR, MODE>();
     b = dim3(32, NTH / 32);                          // ring kernels: fixed block shape
     const int64_t warp_lines = (int64_t)((a.nA + 31) / 32) * a.nB;
     g = dim3((unsigned)((warp_lines + b.y - 1) / b.y), 1, g.z);
@@ -138,7 +138,7 @@ static cudaError_t launch_dir(int mode, const SweepArgs& a, dim3 g, dim3 b, cuda
             // (128-cell segments: C3 x 2.15 -> 2.28 ms per step, r93)
             const int W = (int)std::min<int64_t>(4, (a.nS + 63) / 64);
             const int nseg = (a.nS + 64 * W - 1) / (64 * W);
-            if (MFC_XPAIR_TMA) {
+            if constexpr (MFC_XPAIR_TMA != 0) {
                 // persistent blocks, the next segment's tile loaded by TMA (sweep_x_pair_tma)
                 const int64_t X = a.sA, Y = a.sB / a.sA, Z = a.sE / a.sB;
                 const int ox = (int)(a.base % X), oy = (int)((a.base / X) % Y),

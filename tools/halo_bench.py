@@ -63,6 +63,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     args = ap.parse_args()
+    for n in (256, 128, 64):              # the single domain of each size, for reference
+        print(json.dumps(run(n, (1, 1, 1), "single", args.steps, args.warmup)), flush=True)
     for n, procs in ((256, (1, 1, 2)), (256, (1, 2, 2)), (128, (2, 2, 2)), (64, (2, 2, 2))):
         for mode in ("exchanged", "fused"):
             print(json.dumps(run(n, procs, mode, args.steps, args.warmup)), flush=True)

@@ -238,10 +238,11 @@ __device__ __forceinline__ void weno5_fewop_d(double D0, double D1, double D2, d
     double t2 = fma(k133 * s2, s2, fma(r2, r2, eps4)); t2 *= t2;
     const double P0 = t1 * t2, P1 = t0 * t2, P2 = t0 * t1;
     const double xm0 = fma(k23, s0, D1), xm1 = fma(3.0, r1, s1), xm2 = D2 - r2;
-    const double Dm = fma(12.0, P1, fma(6.0, P2, 2.0 * P0));
+    const double A12 = 12.0 * P1;        // shared by both weight sums (5 operations, not 6)
+    const double Dm = fma(2.0, P0, fma(6.0, P2, A12));
     const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
     const double yp0 = r0 + D1, yp1 = fma(3.0, r1, -s1), yp2 = fma(-k23, s2, D2);   // = -X
-    const double Dp = fma(12.0, P1, fma(2.0, P2, 6.0 * P0));
+    const double Dp = fma(6.0, P0, fma(2.0, P2, A12));
     const double Np = fma(P2, yp2, fma(P1, yp1, P0 * yp0));
 #if MFC_WENO_ONE_RCP
     const double R = rcp(Dm * Dp);           // see weno5_fewop_s
@@ -270,10 +271,11 @@ __device__ __forceinline__ void weno5_fewop_s(double r0, double D1, double D2, d
     double t2 = fma(r2, r2, S2); t2 *= t2;
     const double P0 = t1 * t2, P1 = t0 * t2, P2 = t0 * t1;
     const double xm0 = fma(k23, s0, D1), xm1 = fma(3.0, r1, s1), xm2 = D2 - r2;
-    const double Dm = fma(12.0, P1, fma(6.0, P2, 2.0 * P0));
+    const double A12 = 12.0 * P1;        // shared by both weight sums (5 operations, not 6)
+    const double Dm = fma(2.0, P0, fma(6.0, P2, A12));
     const double Nm = fma(P2, xm2, fma(P1, xm1, P0 * xm0));
     const double yp0 = r0 + D1, yp1 = fma(3.0, r1, -s1), yp2 = fma(-k23, s2, D2);   // = -X
-    const double Dp = fma(12.0, P1, fma(2.0, P2, 6.0 * P0));
+    const double Dp = fma(6.0, P0, fma(2.0, P2, A12));
     const double Np = fma(P2, yp2, fma(P1, yp1, P0 * yp0));
 #if MFC_WENO_ONE_RCP
     // one reciprocal for both sides: 1/Dm = Dp R, 1/Dp = Dm R, R = 1/(Dm Dp)
@@ -521,11 +523,13 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     const double EK = fma(0.5, rK * uu, fma(GK, pK, PK));
     const double dK = sK - uK;
 #if MFC_HLLC_ONE_RCP
-    const double D2 = fma(sK, den, -num);
-    const double R = rcp((den * dK) * D2);
-    const double sS = num * ((dK * D2) * R);
-    const double rr = (den * den) * R;       // 1/(dK dS)
-    const double pdK = pK * ((D2 * den) * R);   // p_K/(s_K-u_K)
+    const double D2 = fma(sK, den, -num);    // den dS
+    const double X = dK * D2;
+    const double R = rcp(den * X);           // 1/(den dK D2)
+    const double sS = num * (X * R);         // num/den
+    const double Y = den * R;                // 1/(dK D2)
+    const double rr = den * Y;               // 1/(dK dS)
+    const double pdK = pK * (D2 * Y);        // p_K/(s_K-u_K)
 #else
     const double dS = sK - sS;
     const double rr = rcp(dK * dS);          // one reciprocal for xi and p_K/(s_K-u_K)

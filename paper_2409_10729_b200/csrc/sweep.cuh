@@ -804,7 +804,27 @@ sweep_x_pair(const SweepArgs a, int W) {
         Vo[e * LH + t + 1] = v0[e];
         Ve[e * LH + t + 2] = v1[e];
     }
-    if (t < 6) {
+    if (wrap && n == seg) {
+        // a whole periodic row: the halo cells are the row's own last / first three
+        // cells; their owners store them into the halo slots as well (bitwise the values
+        // a halo load would convert), so warp 0 neither loads nor converts extra cells
+        if (xa >= n - 3) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) V(e, xa - (n - 3)) = v0[e];
+        }
+        if (xa + 1 >= n - 3) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) V(e, xa + 1 - (n - 3)) = v1[e];
+        }
+        if (xa < 3) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) V(e, seg + 3 + xa) = v0[e];
+        }
+        if (xa + 1 < 3) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) V(e, seg + 4 + xa) = v1[e];
+        }
+    } else if (t < 6) {
         double h[E];
         load_prim(t < 3 ? x0 - 3 + t : x0 + seg + t - 3, h);
         const int i = t < 3 ? t : seg + t;

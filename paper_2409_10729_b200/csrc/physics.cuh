@@ -523,13 +523,11 @@ __device__ __forceinline__ void hllc(const double (&vL)[M::E], const double (&vR
     const double EK = fma(0.5, rK * uu, fma(GK, pK, PK));
     const double dK = sK - uK;
 #if MFC_HLLC_ONE_RCP
-    const double D2 = fma(sK, den, -num);    // den dS
-    const double X = dK * D2;
-    const double R = rcp(den * X);           // 1/(den dK D2)
-    const double sS = num * (X * R);         // num/den
-    const double Y = den * R;                // 1/(dK D2)
-    const double rr = den * Y;               // 1/(dK dS)
-    const double pdK = pK * (D2 * Y);        // p_K/(s_K-u_K)
+    const double D2 = fma(sK, den, -num);
+    const double R = rcp((den * dK) * D2);
+    const double sS = num * ((dK * D2) * R);
+    const double rr = (den * den) * R;       // 1/(dK dS)
+    const double pdK = pK * ((D2 * den) * R);   // p_K/(s_K-u_K)
 #else
     const double dS = sK - sS;
     const double rr = rcp(dK * dS);          // one reciprocal for xi and p_K/(s_K-u_K)

@@ -247,6 +247,7 @@ __host__ __device__ constexpr int sweep_min_blocks() {
 #ifndef MFC_MARCH_TMA
 #define MFC_MARCH_TMA 0
 #endif
+
 template <class M, int DIR, int MODE, int ORD>
 __host__ __device__ constexpr bool march_tma() {
     return MFC_MARCH_TMA && M::D == 3 && DIR >= 1 && (MODE == M_ACC || MODE == M_ACCN) && ORD != 7;
@@ -425,11 +426,6 @@ sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
     double F_prev[E];      // flux at face j-3/2
     double uf_prev = 0.0;
 
-#ifdef MFC_MARCH_UNROLL
-#define MFC_STR_(x) #x
-#define MFC_UNROLL_(n) _Pragma(MFC_STR_(unroll n))
-    MFC_UNROLL_(MFC_MARCH_UNROLL)
-#endif
     for (int j = s0 - 1; j <= s1; ++j) {
         if constexpr (TMA) {                          // the boxes of step j have landed
             mbar_wait(wbar + kq % (R::PD + 1), (tma_par >> (kq % (R::PD + 1))) & 1u);
@@ -804,27 +800,7 @@ sweep_x_pair(const SweepArgs a, int W) {
         Vo[e * LH + t + 1] = v0[e];
         Ve[e * LH + t + 2] = v1[e];
     }
-    if (wrap && n == seg) {
-        // a whole periodic row: the halo cells are the row's own last / first three
-        // cells; their owners store them into the halo slots as well (bitwise the values
-        // a halo load would convert), so warp 0 neither loads nor converts extra cells
-        if (xa >= n - 3) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) V(e, xa - (n - 3)) = v0[e];
-        }
-        if (xa + 1 >= n - 3) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) V(e, xa + 1 - (n - 3)) = v1[e];
-        }
-        if (xa < 3) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) V(e, seg + 3 + xa) = v0[e];
-        }
-        if (xa + 1 < 3) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) V(e, seg + 4 + xa) = v1[e];
-        }
-    } else if (t < 6) {
+    if (t < 6) {
         double h[E];
         load_prim(t < 3 ? x0 - 3 + t : x0 + seg + t - 3, h);
         const int i = t < 3 ? t : seg + t;

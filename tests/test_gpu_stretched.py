@@ -168,3 +168,38 @@ def test_c3_full_size_stretched_rhs():
     got = gpu_rhs(pb, q)
     ref = O.rhs(P, q)
     check_rhs("rhs C3 full 256^3 stretched (bench --stretch launch config)", pb, v, q, got, ref)
+
+
+def test_stretched_fused_halo_and_streamed_advance_host():
+    """The stretched tables through the other step paths: the fused-halo loopback group
+    (peer stores from the ORD-7 marches) and the streamed host-to-host step, both
+    bitwise equal to the plain single-domain step."""
+    pb = _st(W.random_problem(3, (20, 18, 36), 2, "water"))
+    P_, v, q = oracle_inputs(pb)
+    dt = _dt(pb, v)
+    ref = gpu_steps(pb, q, dt, 2)
+    procs = (1, 2, 2)
+    solvers = [mfc.Solver(pb, procs=procs, rank=r, nranks=4, loopback=True) for r in range(4)]
+    qs = []
+    for s in solvers:
+        lo, n = s.layout.lo_global, s.layout.n_local
+        qs.append(s.state_from_cons(q[:, lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]]))
+    mfc.fused_halo_group(solvers, qs)
+    mfc.halo_exchange_group(solvers, qs)
+    for _ in range(2):
+        mfc.rk3_step_group(solvers, qs, dt)
+    torch.cuda.synchronize()
+    got = np.empty_like(q)
+    for s, t in zip(solvers, qs):
+        lo, n = s.layout.lo_global, s.layout.n_local
+        got[:, lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]] = s.interior(t).cpu().numpy()
+    assert np.array_equal(got, ref)
+    # streamed advance_host (one step, z-chunks) == one device step
+    one = gpu_steps(pb, q, dt, 1)
+    s = mfc.Solver(pb)
+    s.set_stream_chunks(5)
+    qi = torch.as_tensor(q).pin_memory()
+    qo = torch.empty_like(qi).pin_memory()
+    s.advance_host(qi, qo, s.empty_state(), 1, dt)
+    assert s.last_launch_count() > 9
+    assert np.array_equal(qo.numpy(), one)

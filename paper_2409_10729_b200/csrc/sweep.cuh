@@ -743,9 +743,6 @@ sweep_x_tile(const SweepArgs a, int W) {
 #ifndef MFC_XP_MINB
 #define MFC_XP_MINB 5
 #endif
-#ifndef MFC_XPAIR_VEC_OUT
-#define MFC_XPAIR_VEC_OUT 1   // the pair's RK base loads and stores as 16-byte accesses
-#endif
 #ifndef MFC_XP_MINB_BIG
 #define MFC_XP_MINB_BIG 4
 #endif
@@ -796,21 +793,8 @@ sweep_x_pair(const SweepArgs a, int W) {
 
     // 1. primitives of my two cells (tile indices 2t+3, 2t+4) and of the six halo cells
     double v0[E], v1[E];
-    if (xa + 1 < n) {
-        // both cells interior (unmapped): one 16-byte load per equation for the pair
-        double q0[E], q1[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const double2 d = __ldg(reinterpret_cast<const double2*>(a.q + row + xa + e * a.sE));
-            q0[e] = d.x;
-            q1[e] = d.y;
-        }
-        cons_to_prim_fast<M>(q0, v0, a.mat);
-        cons_to_prim_fast<M>(q1, v1, a.mat);
-    } else {
-        load_prim(xa, v0);
-        load_prim(xa + 1, v1);
-    }
+    load_prim(xa, v0);
+    load_prim(xa + 1, v1);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         Vo[e * LH + t + 1] = v0[e];
@@ -888,38 +872,6 @@ sweep_x_pair(const SweepArgs a, int W) {
 
     // 4. updates: cell xa with (FA, FB), cell xa+1 with (FB, the next thread's FA)
     const double wi = a.w * a.invd;
-    if (MFC_XPAIR_VEC_OUT && xa + 1 < x1) {
-        // both cells: the same arithmetic, 16-byte loads of the RK base and stores
-        const int ri = (wrap && t == tl) ? 0 : t + 1;
-        const double du0 = ufB - ufA, du1 = FS[E * LP + ri] - ufB;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            double r0 = FA[e] - FB[e];
-            double r1 = FB[e] - FS[e * LP + ri];
-            if (e >= M::IA) {
-                r0 = fma(v0[e], du0, r0);
-                r1 = fma(v1[e], du1, r1);
-            }
-            const int64_t i = row + xa + e * a.sE;
-            double2 o;
-            if constexpr (RKB) {
-                const double2 qs = __ldg(reinterpret_cast<const double2*>(a.q + i));
-                double b0 = a.cb * qs.x, b1 = a.cb * qs.y;
-                if (a.qn != nullptr && a.ca != 0.0) {
-                    const double2 qn = __ldg(reinterpret_cast<const double2*>(a.qn + i));
-                    b0 = fma(a.ca, qn.x, b0);
-                    b1 = fma(a.ca, qn.y, b1);
-                }
-                o.x = fma(wi, r0, b0);
-                o.y = fma(wi, r1, b1);
-            } else {
-                o.x = r0 * a.invd;
-                o.y = r1 * a.invd;
-            }
-            *reinterpret_cast<double2*>(a.dst + i) = o;
-        }
-        return;
-    }
     if (xa < x1) {
         const double du = ufB - ufA;
 #pragma unroll

@@ -183,6 +183,14 @@ int mfc_max_wave_rate(mfc_ctx* ctx, const double* q, double* d_out, void* stream
 int mfc_cfl_dt(mfc_ctx* ctx, const double* q, double cfl, double* dt_out, double* d_scratch,
                void* stream);
 
+/* Admissibility guard ("positivity/mixture guard"; DESIGN.md AMB-14:
+ * detection, no limiter): writes to the device int64 *d_count the number of interior
+ * cells (over all ranks with the NCCL transport) whose conserved state is not finite or
+ * whose mixture density or squared sound speed ((Gamma+1)p + Pi)/(rho Gamma) is not
+ * positive, computed from the bitwise-specified cons -> prim (S2).  Enqueued on `stream`,
+ * no host sync.  Errors: EINVAL (NULL / misaligned), ECUDA, ENCCL. */
+int mfc_count_inadmissible(mfc_ctx* ctx, const double* q, int64_t* d_count, void* stream);
+
 /* Fill the 3 ghost layers of every active dimension of q: physical faces by the
  * boundary condition, faces shared with another rank by the halo exchange
  * (P:94).  Face ghosts only (edges/corners are never read).  Only ghost cells of

@@ -23,6 +23,10 @@ struct EosArgs {
     Materials mat;
 };
 
+// number of inadmissible interior cells (non-finite, rho <= 0 or c^2 <= 0) added to *out
+template <int N>
+cudaError_t launch_admissible(int D, const EosArgs& a, unsigned long long* out, cudaStream_t s);
+
 // to_cons = true: primitive -> conserved, false: conserved -> primitive
 template <int N>
 cudaError_t launch_eos(int D, bool to_cons, const EosArgs& a, cudaStream_t s);

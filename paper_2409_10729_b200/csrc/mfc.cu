@@ -1731,6 +1731,37 @@ int mfc_max_wave_rate(mfc_ctx* c, const double* q, double* d_out, void* stream) 
     return MFC_OK;
 }
 
+int mfc_count_inadmissible(mfc_ctx* c, const double* q, int64_t* d_count, void* stream) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    int st;
+    if ((st = check_ptr(q, "q")) || (st = set_device(c))) return st;
+    if (!d_count || ((uintptr_t)d_count) % 8) return fail(MFC_EINVAL, "d_count NULL or misaligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    EosArgs a;
+    a.in = q;
+    a.out = nullptr;
+    a.sE = c->stride[0];
+    a.sZ = c->stride[1];
+    a.sY = c->stride[2];
+    a.base = c->offset;
+    a.nx = (int32_t)c->nl[0];
+    a.ny = (int32_t)c->nl[1];
+    a.nz = (int32_t)c->nl[2];
+    a.mat = c->mat;
+    CU_TRY(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+    auto* o = reinterpret_cast<unsigned long long*>(d_count);
+    cudaError_t e;
+    switch (c->N) {
+        case 1: e = launch_admissible<1>(c->D, a, o, s); break;
+        case 2: e = launch_admissible<2>(c->D, a, o, s); break;
+        default: e = launch_admissible<3>(c->D, a, o, s); break;
+    }
+    if (e != cudaSuccess) return fail(MFC_ECUDA, "admissibility launch: %s", cudaGetErrorString(e));
+    if (c->comm)
+        NCCL_TRY(ncclAllReduce(d_count, d_count, 1, ncclInt64, ncclSum, c->comm, s));
+    return MFC_OK;
+}
+
 int mfc_cfl_dt(mfc_ctx* c, const double* q, double cfl, double* dt_out, double* d_scratch,
                void* stream) {
     if (!c || !dt_out || !d_scratch) return fail(MFC_EINVAL, "NULL argument");

@@ -98,6 +98,54 @@ static int set_smem_attr(K* kernel, size_t smem) {
     return 0;
 }
 
+// Admissibility guard (F3): count interior cells whose conserved state is not finite, or
+// whose mixture density or squared sound speed c^2 = ((Gamma+1)p + Pi)/(rho Gamma) is not
+// positive (the oracle's orc_count_inadmissible, AMB-14: detection, no limiter).
+// The primitives come from the bitwise-specified cons_to_prim.
+template <class M>
+__global__ void __launch_bounds__(256) admissible_kernel(const EosArgs a,
+                                                         unsigned long long* out) {
+    __shared__ unsigned long long red[256];
+    const int64_t n = (int64_t)a.nx * a.ny * a.nz;
+    unsigned long long bad = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % a.nx);
+        const int j = (int)((t / a.nx) % a.ny);
+        const int k = (int)(t / ((int64_t)a.nx * a.ny));
+        const int64_t c = a.base + (int64_t)k * a.sZ + (int64_t)j * a.sY + i;
+        double x[M::E], v[M::E];
+        bool finite = true;
+#pragma unroll
+        for (int e = 0; e < M::E; ++e) {
+            x[e] = a.in[c + e * a.sE];
+            finite = finite && isfinite(x[e]);
+        }
+        if (!finite) {
+            ++bad;
+            continue;
+        }
+        cons_to_prim<M>(x, v, a.mat);
+        double rho = v[0], G = __dmul_rn(v[M::IA], a.mat.Gam[0]), P = __dmul_rn(v[M::IA], a.mat.Pi[0]);
+#pragma unroll
+        for (int f = 1; f < M::N; ++f) {
+            rho = __dadd_rn(rho, v[f]);
+            G = __dadd_rn(G, __dmul_rn(v[M::IA + f], a.mat.Gam[f]));
+            P = __dadd_rn(P, __dmul_rn(v[M::IA + f], a.mat.Pi[f]));
+        }
+        const double c2 = __ddiv_rn(__dadd_rn(__dmul_rn(__dadd_rn(G, 1.0), v[M::IE]), P),
+                                    __dmul_rn(rho, G));
+        if (!(rho > 0.0) || !(c2 > 0.0) || !isfinite(c2)) ++bad;
+    }
+    red[threadIdx.x] = bad;
+    __syncthreads();
+    for (int s2 = 128; s2 > 0; s2 >>= 1) {
+        if (threadIdx.x < s2) red[threadIdx.x] += red[threadIdx.x + s2];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && red[0]) atomicAdd(out, red[0]);
+}
+
 template <class M, int DIR, int MODE, int ORD, bool PEER = false>
 static cudaError_t launch_ring(const SweepArgs& a, dim3 g, dim3 b, cudaStream_t s) {
     constexpr int NTH = sweep_nth<M, DIR, MODE>();
@@ -268,6 +316,20 @@ cudaError_t launch_wave_rate<MFC_NF>(int D, const EosArgs& a, double3 inv_dx, co
         case 1: wave_rate_kernel<Model<MFC_NF, 1>><<<blocks, 256, 0, s>>>(a, inv_dx, wg, o); break;
         case 2: wave_rate_kernel<Model<MFC_NF, 2>><<<blocks, 256, 0, s>>>(a, inv_dx, wg, o); break;
         case 3: wave_rate_kernel<Model<MFC_NF, 3>><<<blocks, 256, 0, s>>>(a, inv_dx, wg, o); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_admissible<MFC_NF>(int D, const EosArgs& a, unsigned long long* out,
+                                      cudaStream_t s) {
+    const int64_t n = (int64_t)a.nx * a.ny * a.nz;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    switch (D) {
+        case 1: admissible_kernel<Model<MFC_NF, 1>><<<blocks, 256, 0, s>>>(a, out); break;
+        case 2: admissible_kernel<Model<MFC_NF, 2>><<<blocks, 256, 0, s>>>(a, out); break;
+        case 3: admissible_kernel<Model<MFC_NF, 3>><<<blocks, 256, 0, s>>>(a, out); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

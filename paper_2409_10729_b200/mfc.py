@@ -31,7 +31,7 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ES
 EXPORTED = [
     "mfc_init", "mfc_get_layout", "mfc_get_neighbors", "mfc_bind_workspace", "mfc_set_weno_eps",
     "mfc_set_weno_order", "mfc_set_weno_mapped", "mfc_set_grid",
-    "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
+    "mfc_prim_to_cons", "mfc_cons_to_prim", "mfc_count_inadmissible", "mfc_halo_exchange", "mfc_rhs", "mfc_rk3_step",
     "mfc_rk3_steps", "mfc_max_wave_rate", "mfc_cfl_dt",
     "mfc_advance_host", "mfc_set_stream_chunks", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
     "mfc_fused_halo_group", "mfc_peer_export", "mfc_peer_import",
@@ -82,6 +82,7 @@ def _load():
         "mfc_set_grid": [vp, i32, ctypes.POINTER(dbl), i64],
         "mfc_prim_to_cons": [vp, vp, vp, vp],
         "mfc_cons_to_prim": [vp, vp, vp, vp],
+        "mfc_count_inadmissible": [vp, vp, vp, vp],
         "mfc_halo_exchange": [vp, vp, vp],
         "mfc_rhs": [vp, vp, vp, vp],
         "mfc_rk3_step": [vp, vp, dbl, vp],
@@ -300,6 +301,13 @@ class Solver:
             raise ValueError("out must be a float64 tensor on the solver's device")
         _check(lib.mfc_max_wave_rate(self._h, self._sp(q), _ptr(out), _stream(stream)),
                "mfc_max_wave_rate")
+        return out
+
+    def count_inadmissible(self, q, stream=None) -> torch.Tensor:
+        """Device int64: interior cells that are not finite or have rho <= 0 or c^2 <= 0."""
+        out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        _check(lib.mfc_count_inadmissible(self._h, self._sp(q), ctypes.c_void_p(out.data_ptr()),
+                                          _stream(stream)), "mfc_count_inadmissible")
         return out
 
     def cfl_dt(self, q, cfl: float, stream=None) -> float:

@@ -345,3 +345,22 @@ def test_gpu_extrapolation_is_the_constant_extension(axis, side):
     sl = [slice(None)] * 4
     sl[ax] = slice(3, 3 + n[axis]) if side == 0 else slice(0, n[axis])
     assert np.array_equal(r_ext[tuple(sl)], r)
+
+
+@pytest.mark.parametrize("N,d", [(1, 1), (2, 2), (3, 3)])
+def test_count_inadmissible_matches_oracle(N, d):
+    """F3's admissibility guard (mfc_count_inadmissible) counts what the oracle counts."""
+    pb = W.random_problem(d, (23, 17, 11)[:d], N, "water")
+    P, v, q = oracle_inputs(pb)
+    s = gpu_solver(pb)
+    assert s.count_inadmissible(s.state_from_cons(q)).item() == 0
+    bad = q.copy()
+    flat = bad.reshape(pb.E, -1)
+    nc = flat.shape[1]
+    flat[0, 1] = np.nan
+    flat[N + d, nc // 2] = -1e12                              # rhoE far below Pi: c^2 < 0
+    for i in range(N):
+        flat[i, nc - 2] = -abs(flat[i, nc - 2]) - 1.0         # rho < 0
+    want = O.count_inadmissible(P, bad)
+    assert want == 3
+    assert s.count_inadmissible(s.state_from_cons(bad)).item() == want

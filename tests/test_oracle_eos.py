@@ -105,3 +105,24 @@ def test_pressure_equilibrium_of_mixture_rule():
     v2 = O.cons_to_prim(P, O.prim_to_cons(P, v))
     bound = 8 * np.finfo(float).eps * (1 + (a * Pi[0]) / ((a * G[0] + (1 - a) * G[1]) * p0))
     assert np.all(np.abs(v2[3] / p0 - 1) <= bound)
+
+
+def test_count_inadmissible_counts_the_corrupted_cells():
+    """The admissibility guard (AMB-14, F3) counts exactly the cells that are not finite,
+    have a non-positive mixture density, or a non-positive c^2 (negative pressure in an
+    ideal gas), and nothing else."""
+    import oracle as O
+    from paper_2409_10729_b200 import workloads as W
+    pb = W.random_problem(3, (9, 8, 7), 2, "gas")
+    P = O.Problem.from_spec(pb)
+    v = W.random_prims(pb, seed=3)
+    q = O.prim_to_cons(P, v)
+    assert O.count_inadmissible(P, q) == 0
+    bad = q.copy()
+    bad[0, 1, 2, 3] = np.nan                                   # not finite
+    bad[0, 2, 2, 2] = -bad[0, 2, 2, 2] - bad[1, 2, 2, 2] - 1   # rho < 0
+    vneg = v.copy()
+    vneg[pb.n_fluids + 3, 4, 5, 6] = -0.5                      # p < 0 with pi_inf = 0
+    qneg = O.prim_to_cons(P, vneg)
+    bad[:, 4, 5, 6] = qneg[:, 4, 5, 6]
+    assert O.count_inadmissible(P, bad) == 3

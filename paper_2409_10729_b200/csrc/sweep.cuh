@@ -552,6 +552,7 @@ sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
     }
 }
 
+
 }  // namespace mfc
 
 namespace mfc {

@@ -211,9 +211,10 @@ int mfc_rk3_step(mfc_ctx* ctx, double* q, double dt, void* stream);
 
 /* nsteps SSP-RK3 steps of size dt on q (as nsteps calls of mfc_rk3_step), replayed
  * from a CUDA graph of one step that the library captures on first use and keeps
- * while q and dt stay the same (NCCL halo calls are captured too).  Removes the
- * per-kernel launch latency that dominates small grids.  With profiling enabled
- * the steps are launched individually. */
+ * while q and dt stay the same (single domain, loopback and IPC-peer contexts; the
+ * fused halo's stream memory operations are captured).  Removes the per-kernel launch
+ * latency that dominates small grids.  With profiling enabled, and for contexts with an
+ * NCCL communicator, the steps are launched individually. */
 int mfc_rk3_steps(mfc_ctx* ctx, double* q, double dt, int64_t nsteps, void* stream);
 
 /* End-to-end call with HOST buffers: copy the dense interior q_in[E][nz][ny][nx]

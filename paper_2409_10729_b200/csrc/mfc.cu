@@ -1816,8 +1816,10 @@ int mfc_rk3_steps(mfc_ctx* c, double* q, double dt, int64_t nsteps, void* stream
     int st = set_device(c);
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    if (c->prof) {
-        // per-launch event timing needs the plain launches
+    if (c->prof || c->comm) {
+        // per-launch event timing needs the plain launches; NCCL contexts launch every
+        // step plainly too (capturing NCCL send/recv in a graph has never run on more than
+        // one GPU with this build)
         for (int64_t i = 0; i < nsteps; ++i)
             if ((st = rk3_group(&c, &q, 1, dt, s))) return st;
         return MFC_OK;

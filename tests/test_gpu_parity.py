@@ -364,3 +364,53 @@ def test_count_inadmissible_matches_oracle(N, d):
     want = O.count_inadmissible(P, bad)
     assert want == 3
     assert s.count_inadmissible(s.state_from_cons(bad)).item() == want
+
+
+# ------------------------------------------------------ invariants on the GPU itself
+# (independent of the oracle: what the discretisation guarantees by construction)
+
+@pytest.mark.parametrize("stretch", [False, True])
+def test_gpu_discrete_conservation(stretch):
+    """I2 on the GPU: on a periodic domain the cell-width-weighted sum of the RHS of
+    every conserved variable (partial densities, momenta, energy) is zero to round-off
+    of the flux scale (telescoping face fluxes); not the volume fractions (alpha div u)."""
+    pb = W.random_problem(3, (24, 20, 18), 2, "water")
+    if stretch:
+        pb = W.stretched(pb)
+    P, v, q = oracle_inputs(pb)
+    r = gpu_rhs(pb, q)
+    wx, wy, wz = (np.diff(pb.boundaries(k)) for k in range(3))
+    vol = wz[:, None, None] * wy[None, :, None] * wx[None, None, :]
+    phi = rhs_flux_scale(pb, v, q)
+    N, d = pb.n_fluids, pb.ndim
+    for e in range(N + d + 1):
+        total = (r[e] * vol).sum()
+        bound = 64 * np.finfo(float).eps * phi[e] * vol.sum() * np.sqrt(q[0].size)
+        assert abs(total) <= bound, (e, total, bound)
+
+
+def test_gpu_pressure_velocity_equilibrium_100_steps():
+    """I3 on the GPU: uniform p and u with a stepped water/air volume fraction stay
+    uniform over 100 RK3 steps to within the stiffened-gas round-off 1e-13 (1 + Pi/(Gamma p))."""
+    pb = W.random_problem(3, (32, 12, 10), 2, "water")
+    N, d = pb.n_fluids, pb.ndim
+    X = pb.centres()[0]
+    a1 = np.where((X > 0.3) & (X < 0.6), 1 - 1e-6, 1e-6) * np.ones((pb.n[2], pb.n[1], 1))
+    v = np.empty(pb.shape)
+    v[0] = a1 * 1000.0
+    v[1] = (1 - a1) * 1.2
+    v[N] = 100.0
+    v[N + 1:N + d] = 0.0
+    v[N + d] = 1e5
+    v[N + d + 1] = a1
+    v[N + d + 2] = 1 - a1
+    P = O.Problem.from_spec(pb)
+    q = O.prim_to_cons(P, v)
+    dt = stable_dt(pb, v, 0.3)
+    got = gpu_steps(pb, q, dt, 100)
+    vv = O.cons_to_prim(P, got)
+    G = (4.4 - 1) ** -1
+    Pi = 4.4 * 6e8 / 3.4
+    tol = 1e-13 * (1 + Pi / (G * 1e5))
+    assert np.abs(vv[N + d] / 1e5 - 1).max() <= tol
+    assert np.abs(vv[N] / 100.0 - 1).max() <= tol

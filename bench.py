@@ -4,8 +4,10 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N = 1: BASELINE.json configs[2] (C3: 3D two-fluid shock-droplet, 256^3 cells, E = 8).
-N > 1 (launched by torchrun, one rank per GPU, NCCL): configs[3] (C4 weak scaling):
-      C3's 256^3 block on every rank, z-slabs, periodic in z, halo exchange over NCCL.
+N > 1 (launched by torchrun, one rank per GPU): configs[3] (C4 weak scaling): C3's 256^3
+      block on every rank, z-slabs, periodic in z; the halo is fused into the stage's
+      last sweep (F1: stores into the neighbours' IPC-mapped ghost layers, --halo fused),
+      or the NCCL pack / send-recv / unpack baseline (--halo nccl).
 One "step" = one SSP-RK3 step = 3 RHS evaluations (ghost fill + x/y/z fused sweeps each).
 Metric (BASELINE.json): grind time = device time / (cells * E * RHS evaluations), in ns,
 aggregate over all ranks (lower is better), plus achieved HBM GB/s of the sweeps.
@@ -479,10 +481,12 @@ def main():
                     help="cells per dimension of the per-GPU block")
     ap.add_argument("--config", default="C3", choices=["C3", "C5", "C2"],
                     help="C3/C4 (default; weak scaling for N > 1), C5 (strong scaling), C2")
-    ap.add_argument("--halo", default="nccl", choices=["nccl", "fused", "peer"],
-                    help="N>1: NCCL pack/send/recv/unpack; 'fused': F1 stores into the "
-                         "neighbours' CUDA-IPC-mapped ghost layers (NCCL kept for the "
-                         "plumbing); 'peer': the same with gloo plumbing and no NCCL")
+    ap.add_argument("--halo", default="fused", choices=["nccl", "fused", "peer"],
+                    help="N>1: 'fused' (default, F1): the last sweep of each RK stage stores "
+                         "its boundary layers into the neighbours' CUDA-IPC-mapped ghost "
+                         "layers over NVLink, NCCL only for the plumbing; 'nccl': the "
+                         "baseline pack / NCCL send-recv / unpack; 'peer': fused with gloo "
+                         "plumbing and no NCCL")
     ap.add_argument("--same-device", action="store_true",
                     help="put every rank on GPU 0 (multi-process protocol check on one GPU; "
                          "its timings are time-sliced and not a scaling number)")

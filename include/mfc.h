@@ -4,16 +4,21 @@
  *
  * What the library computes (PAPER.md = /root/reference/PAPER.md, line numbers):
  *   - the Allaire 5-equation model (§II-A) closed by the stiffened-gas
- *     mixture EOS, with N in {1,2,3} fluids on a uniform Cartesian grid
- *      in d in {1,2,3} dimensions;
+ *     mixture EOS, with N in {1,2,3} fluids on a structured Cartesian grid,
+ *     uniform or tanh-stretched per axis (mfc_set_grid), in d in {1,2,3}
+ *     dimensions;
  *   - its finite-volume semi-discretisation (eq. (1) integrated over a
  *     cell): WENO5 reconstruction of the primitive variables and the HLLC flux
- *     (P:84), flux differencing plus the non-conservative -h(q) div(u) term;
+ *     (WENO3 and mapped WENO5-M as options), flux differencing plus the
+ *     non-conservative -h(q) div(u) term;
  *   - an SSP-RK3 time step (BASELINE.json north_star; the paper's grind unit is the
  *     "right-hand-side evaluation");
- *   - the 3-deep halo exchange between subdomains (§III-A) over NCCL.
+ *   - the 3-deep halo exchange between subdomains (§III-A): NCCL send/recv,
+ *     or fused into the stage's last sweep as stores into the neighbours' ghost
+ *     layers over peer memory (F1).
  * The readings of the paper where it is silent or garbled are listed in
- * DESIGN.md §3 (AMB-1..22); the arithmetic is specified there step by step.
+ * DESIGN.md §4 (AMB-1..30); the arithmetic is specified in DESIGN.md §2-§3 step by
+ * step.
  *
  * Variables (E = 2N + d + 1 equations, this order):
  *   conserved q = (a_1 r_1 .. a_N r_N, r u_1 .. r u_d, r E, a_1 .. a_N)
@@ -65,7 +70,8 @@ typedef enum {
  *   EXTRAPOLATION: every ghost <- the adjacent interior cell (zeroth order) */
 enum { MFC_BC_PERIODIC = -1, MFC_BC_REFLECTIVE = -2, MFC_BC_EXTRAPOLATION = -3 };
 
-/* Global grid: uniform spacing dx_k = (hi_k - lo_k)/n_global[k].
+/* Global grid: uniform spacing dx_k = (hi_k - lo_k)/n_global[k] unless
+ * mfc_set_grid gives the axis explicit cell boundaries.
  * Inactive dimensions (k >= ndim) must have n_global[k] == 1 and procs[k] == 1. */
 typedef struct {
     int32_t ndim;           /* 1..3 */
@@ -125,7 +131,9 @@ int mfc_get_neighbors(const mfc_ctx* ctx, int32_t nbr[6]);
 
 /* Hand the library a device buffer of >= layout.workspace_bytes bytes, 256-byte
  * aligned (torch-owned; the library never frees it).  It holds two RK stage
- * buffers, the RHS accumulator and the halo pack buffers.  Must be bound before
+ * buffers, the RHS accumulator, the halo pack buffers, the staging slots of the
+ * streamed mfc_advance_host and the stretched-grid coefficient tables (re-uploaded on
+ * a rebind).  The caller must not write it while the library uses it.  Must be bound before
  * mfc_rk3_step.  Rebinding drops the captured CUDA graph of mfc_rk3_steps.
  * Errors: EINVAL (NULL, misaligned), ENOMEM (too small), ESTATE (the fused halo is
  * attached: neighbours hold pointers into the bound stage buffers). */
@@ -139,14 +147,16 @@ int mfc_set_weno_eps(mfc_ctx* ctx, double eps);
 
 /* Reconstruction order: 5 (WENO5-JS, default) or 3 (WENO3-JS), the two options of
  * P:84 ("third or fifth-order accurate WENO reconstructions").
- * The ghost depth stays 3; WENO3 reads the inner two layers. */
+ * The ghost depth stays 3; WENO3 reads the inner two layers.  EUNSUPPORTED for 3 on
+ * a context with a stretched axis (mfc_set_grid). */
 int mfc_set_weno_order(mfc_ctx* ctx, int32_t order);
 
 /* on = 1: WENO5 with mapped nonlinear weights (WENO5-M: Henrick, Aslam & Powers, JCP 207
  * (2005) 542, eq. (8); SURVEY §8(f) F2 "optionally, mapped WENO-M"): the Jiang-Shu
  * omega_k are mapped by g_k(w) = w (d_k + d_k^2 - 3 d_k w + w^2)/(d_k^2 + w (1 - 2 d_k))
  * and renormalised; same stencils, beta_k and eps.  on = 0 (default): WENO5-JS.  No
- * effect with order 3.  EINVAL unless on is 0 or 1; a captured step graph is dropped. */
+ * effect with order 3.  EINVAL unless on is 0 or 1; EUNSUPPORTED for on = 1 on a
+ * context with a stretched axis; a captured step graph is dropped. */
 int mfc_set_weno_mapped(mfc_ctx* ctx, int32_t on);
 
 /* Non-uniform grid along dimension dim ("local mesh refinement

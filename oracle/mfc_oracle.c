@@ -10,9 +10,13 @@
  *
  * Pins (tests/test_oracle_*.py): EOS closed forms, WENO5 exactness on
  * quadratics and order of accuracy, HLLC consistency / upwinding / contact
- * and an independent textbook HLLC, exact Riemann solutions (Toro ch. 4),
- * uniform-state and p-u equilibrium preservation, discrete conservation,
- * RK3 amplification factor.
+ * and an independent textbook HLLC, exact Riemann solutions (Toro ch. 4;
+ * Sod and C1 convergence and plateaus), uniform-state and p-u equilibrium
+ * preservation, discrete conservation, RK3 amplification factor, the
+ * reflective / extrapolation ghost maps (mirror and constant-extension
+ * identities), the non-uniform-grid WENO5 (quadratic / quartic exactness,
+ * smoothness-indicator closed forms, fifth order on a tanh grid) and the
+ * admissibility count.
  */
 #include "mfc_oracle.h"
 

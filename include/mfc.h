@@ -297,6 +297,15 @@ int mfc_peer_import(mfc_ctx* ctx, int32_t face, const void* blob);
  * e.g. over torch.distributed, before every rank calls mfc_init). */
 int mfc_nccl_get_unique_id(void* out128);
 
+/* Poll the NCCL communicator for an asynchronous error (ncclCommGetAsyncError: a peer
+ * that died, a transport failure), which NCCL reports nowhere else.  MFC_OK without a
+ * communicator (nranks == 1, loopback, peer transport) or while healthy; MFC_ENCCL with
+ * the reason in mfc_last_error otherwise.  The library also polls before every enqueue
+ * of NCCL work (halo exchange, the max / sum reductions), so such a call returns
+ * MFC_ENCCL instead of hanging; mfc_finalize then aborts the communicator instead of
+ * waiting for it (ncclCommAbort). */
+int mfc_comm_status(mfc_ctx* ctx);
+
 /* Number of kernels the last mfc_rhs / mfc_rk3_step / mfc_halo_exchange call
  * launched (for the bench's launch count). */
 int64_t mfc_last_launch_count(const mfc_ctx* ctx);
@@ -310,7 +319,11 @@ int64_t mfc_last_launch_count(const mfc_ctx* ctx);
 int mfc_profile_enable(mfc_ctx* ctx, int32_t on);
 int mfc_profile_read(mfc_ctx* ctx, double* ms, int64_t* count, int32_t nkinds);
 
-/* Release streams, events and the NCCL communicator (not the caller's buffers). */
+/* Release streams, events and the NCCL communicator (not the caller's buffers).
+ *
+ * Tracing: every C-ABI call that enqueues work, every RK stage and every sweep / ghost /
+ * halo launch is an NVTX push/pop range in the domain "mfc" (names after the method's
+ * steps S1-S4), for nsys timelines and `ncu --nvtx --nvtx-include "mfc@<range>/"`. */
 int mfc_finalize(mfc_ctx* ctx);
 
 /* Thread-local message describing the last error ("" if none). */

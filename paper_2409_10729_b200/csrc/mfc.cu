@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -120,6 +121,7 @@ struct mfc_ctx {
     int rank = 0, nranks = 1, procs[3] = {1, 1, 1}, coords[3] = {0, 0, 0};
     bool loopback = false;
     ncclComm_t comm = nullptr;
+    bool comm_failed = false;   // an asynchronous NCCL error was seen: abort, not destroy
     // workspace
     char* ws = nullptr;
     size_t ws_bytes = 0, ws_need = 0;
@@ -501,13 +503,43 @@ cudaEvent_t prof_event(mfc_ctx* c) {
     return c->ev_pool[c->ev_used++];
 }
 
-// Brackets one kernel launch with events on its stream when profiling is on.
+// NVTX ranges (SURVEY §5 tracing) in the domain "mfc": one per C-ABI call, RK stage,
+// sweep and ghost/halo launch, named after the steps of the method, so an nsys
+// timeline or `ncu --nvtx --nvtx-include "mfc@..."` selects them.  They mark the host
+// side's enqueue; without an attached tool each push/pop is a test of a function pointer.
+nvtxDomainHandle_t nvtx_domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("mfc");
+    return d;
+}
+
+struct NvtxRange {
+    explicit NvtxRange(const char* name) {
+        nvtxEventAttributes_t at = {};
+        at.version = NVTX_VERSION;
+        at.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        at.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        at.message.ascii = name;
+        nvtxDomainRangePushEx(nvtx_domain(), &at);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// sweep d = S2-S3 along d (cons->prim, WENO, HLLC, differencing, the RK stage epilogue);
+// ghost fill = S1 physical faces; halo = S1 neighbour faces (pack / unpack / peer stores)
+const char* const kKindName[K_NKIND] = {"sweep x", "sweep y", "sweep z", "ghost fill", "halo",
+                                        "EOS"};
+
+// Brackets one kernel launch with events on its stream when profiling is on, and with
+// an NVTX range always.
 struct ProfScope {
     mfc_ctx* c;
     cudaStream_t s;
     int kind;
     cudaEvent_t a = nullptr;
-    ProfScope(mfc_ctx* c_, cudaStream_t s_, int k) : c(c_), s(s_), kind(k) {
+    NvtxRange nv;
+    ProfScope(mfc_ctx* c_, cudaStream_t s_, int k) : c(c_), s(s_), kind(k), nv(kKindName[k]) {
         if (c->prof && (a = prof_event(c))) cudaEventRecord(a, s);
     }
     ~ProfScope() {
@@ -588,6 +620,21 @@ int exchange_fused(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_
                    bool physical);
 bool group_fused(mfc_ctx* const* cs, int count, int* err);
 
+// An asynchronous NCCL failure (a peer that died, a network error) is reported by
+// ncclCommGetAsyncError only; it is polled before every enqueue of NCCL work and by
+// mfc_comm_status, and turns into MFC_ENCCL instead of a hang at the next collective.
+int comm_async_error(mfc_ctx* c) {
+    if (!c->comm) return MFC_OK;
+    ncclResult_t ar = ncclSuccess;
+    const ncclResult_t r = ncclCommGetAsyncError(c->comm, &ar);
+    if (r != ncclSuccess) return fail(MFC_ENCCL, "ncclCommGetAsyncError: %s", ncclGetErrorString(r));
+    if (ar != ncclSuccess && ar != ncclInProgress) {
+        c->comm_failed = true;
+        return fail(MFC_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ar));
+    }
+    return MFC_OK;
+}
+
 int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
              bool physical = true) {
     {
@@ -606,6 +653,8 @@ int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
     if (count == 1 && cs[0]->nranks > 1 && !cs[0]->loopback) {
         mfc_ctx* c = cs[0];
         if (has_neighbors(c)) {
+            int st = comm_async_error(c);
+            if (st) return st;
             // NCCL pairs the k-th send A->B with the k-th receive on B from A.  The
             // message of my face f lands in the neighbour's face f^1, and every rank
             // posts its receives in ascending face order, so sends are posted in
@@ -939,7 +988,11 @@ int rk3_group(mfc_ctx* const* cs, double* const* qs, int count, double dt, cudaS
         if (qs[r] != cs[r]->fused_q)
             return fail(MFC_ESTATE, "fused halo: q is not the registered state buffer");
     std::vector<double*> in(count);
+    // S4: stage 1 q1 = qn + dt L(qn), 2: q2 = 3/4 qn + 1/4 (q1 + dt L(q1)),
+    // 3: qn+1 = 1/3 qn + 2/3 (q2 + dt L(q2))
+    static const char* const kStage[3] = {"RK3 stage 1", "RK3 stage 2", "RK3 stage 3"};
     for (int stage = 0; stage < 3; ++stage) {
+        NvtxRange nv(kStage[stage]);
         for (int r = 0; r < count; ++r)
             in[r] = stage == 0 ? qs[r] : (stage == 1 ? cs[r]->S1 : cs[r]->S2);
         cudaEvent_t halo = nullptr;
@@ -1694,6 +1747,7 @@ static int eos(mfc_ctx* c, const double* in, double* out, bool to_cons, void* st
 }
 
 int mfc_max_wave_rate(mfc_ctx* c, const double* q, double* d_out, void* stream) {
+    NvtxRange nv("mfc_max_wave_rate");
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     if (c->nranks > 1 && c->transport != MFC_TRANSPORT_NCCL)
         return fail(MFC_EUNSUPPORTED, "max wave rate over %d ranks needs the NCCL transport "
@@ -1727,11 +1781,15 @@ int mfc_max_wave_rate(mfc_ctx* c, const double* q, double* d_out, void* stream) 
         default: e = launch_wave_rate<3>(c->D, a, inv, wg, d_out, s); break;
     }
     if (e != cudaSuccess) return fail(MFC_ECUDA, "wave rate launch: %s", cudaGetErrorString(e));
-    if (c->comm) NCCL_TRY(ncclAllReduce(d_out, d_out, 1, ncclFloat64, ncclMax, c->comm, s));
+    if (c->comm) {
+        if ((st = comm_async_error(c))) return st;
+        NCCL_TRY(ncclAllReduce(d_out, d_out, 1, ncclFloat64, ncclMax, c->comm, s));
+    }
     return MFC_OK;
 }
 
 int mfc_count_inadmissible(mfc_ctx* c, const double* q, int64_t* d_count, void* stream) {
+    NvtxRange nv("mfc_count_inadmissible");
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     int st;
     if ((st = check_ptr(q, "q")) || (st = set_device(c))) return st;
@@ -1758,12 +1816,14 @@ int mfc_count_inadmissible(mfc_ctx* c, const double* q, int64_t* d_count, void* 
     }
     if (e != cudaSuccess) return fail(MFC_ECUDA, "admissibility launch: %s", cudaGetErrorString(e));
     if (c->comm)
+        if ((st = comm_async_error(c))) return st;
         NCCL_TRY(ncclAllReduce(d_count, d_count, 1, ncclInt64, ncclSum, c->comm, s));
     return MFC_OK;
 }
 
 int mfc_cfl_dt(mfc_ctx* c, const double* q, double cfl, double* dt_out, double* d_scratch,
                void* stream) {
+    NvtxRange nv("mfc_cfl_dt");
     if (!c || !dt_out || !d_scratch) return fail(MFC_EINVAL, "NULL argument");
     if (!(cfl > 0.0) || !std::isfinite(cfl)) return fail(MFC_EINVAL, "cfl must be > 0");
     int st = mfc_max_wave_rate(c, q, d_scratch, stream);
@@ -1787,6 +1847,7 @@ int mfc_cons_to_prim(mfc_ctx* c, const double* q, double* v, void* stream) {
 }
 
 int mfc_halo_exchange(mfc_ctx* c, double* q, void* stream) {
+    NvtxRange nv("mfc_halo_exchange");
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     int st;
     if ((st = check_ptr(q, "q")) || (st = set_device(c))) return st;
@@ -1795,6 +1856,7 @@ int mfc_halo_exchange(mfc_ctx* c, double* q, void* stream) {
 }
 
 int mfc_rhs(mfc_ctx* c, double* q, double* rhs, void* stream) {
+    NvtxRange nv("mfc_rhs");
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     int st = set_device(c);
     if (st) return st;
@@ -1802,6 +1864,7 @@ int mfc_rhs(mfc_ctx* c, double* q, double* rhs, void* stream) {
 }
 
 int mfc_rk3_step(mfc_ctx* c, double* q, double dt, void* stream) {
+    NvtxRange nv("mfc_rk3_step");
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     if (!std::isfinite(dt)) return fail(MFC_EINVAL, "dt not finite");
     int st = set_device(c);
@@ -1810,6 +1873,7 @@ int mfc_rk3_step(mfc_ctx* c, double* q, double dt, void* stream) {
 }
 
 int mfc_rk3_steps(mfc_ctx* c, double* q, double dt, int64_t nsteps, void* stream) {
+    NvtxRange nv("mfc_rk3_steps");
     if (!c) return fail(MFC_EINVAL, "NULL ctx");
     if (!std::isfinite(dt)) return fail(MFC_EINVAL, "dt not finite");
     if (nsteps < 0) return fail(MFC_EINVAL, "nsteps < 0");
@@ -1876,6 +1940,7 @@ int mfc_rk3_steps(mfc_ctx* c, double* q, double dt, int64_t nsteps, void* stream
 
 int mfc_advance_host(mfc_ctx* c, const double* q_in, double* q_out, double* q_dev,
                      int64_t nsteps, double dt, void* stream) {
+    NvtxRange nv("mfc_advance_host");
     if (!c || !q_in || !q_out) return fail(MFC_EINVAL, "NULL argument");
     if (nsteps < 0) return fail(MFC_EINVAL, "nsteps < 0");
     int st;
@@ -1915,6 +1980,7 @@ int mfc_advance_host(mfc_ctx* c, const double* q_in, double* q_out, double* q_de
 }
 
 int mfc_halo_exchange_group(mfc_ctx* const* cs, double* const* qs, int32_t count, void* stream) {
+    NvtxRange nv("mfc_halo_exchange_group");
     if (!cs || !qs || count < 1) return fail(MFC_EINVAL, "bad group");
     int st = set_device(cs[0]);
     if (st) return st;
@@ -1924,6 +1990,7 @@ int mfc_halo_exchange_group(mfc_ctx* const* cs, double* const* qs, int32_t count
 
 int mfc_rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, int32_t count,
                   void* stream) {
+    NvtxRange nv("mfc_rhs_group");
     if (!cs || !qs || !rhss || count < 1) return fail(MFC_EINVAL, "bad group");
     int st = set_device(cs[0]);
     if (st) return st;
@@ -1932,6 +1999,7 @@ int mfc_rhs_group(mfc_ctx* const* cs, double* const* qs, double* const* rhss, in
 
 int mfc_rk3_step_group(mfc_ctx* const* cs, double* const* qs, int32_t count, double dt,
                        void* stream) {
+    NvtxRange nv("mfc_rk3_step_group");
     if (!cs || !qs || count < 1) return fail(MFC_EINVAL, "bad group");
     int st = set_device(cs[0]);
     if (st) return st;
@@ -2085,6 +2153,11 @@ int mfc_profile_read(mfc_ctx* c, double* ms, int64_t* count, int32_t nkinds) {
     return MFC_OK;
 }
 
+int mfc_comm_status(mfc_ctx* c) {
+    if (!c) return fail(MFC_EINVAL, "NULL ctx");
+    return comm_async_error(c);
+}
+
 int mfc_finalize(mfc_ctx* c) {
     if (!c) return MFC_OK;
     for (void* p : c->ipc_maps) ipc_release(p);
@@ -2095,7 +2168,16 @@ int mfc_finalize(mfc_ctx* c) {
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm) {
+        // a communicator with an asynchronous error may never finish its pending work:
+        // abort it instead of waiting in ncclCommDestroy
+        ncclResult_t ar = ncclSuccess;
+        if (!c->comm_failed && ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess &&
+            (ar == ncclSuccess || ar == ncclInProgress))
+            ncclCommDestroy(c->comm);
+        else
+            ncclCommAbort(c->comm);
+    }
     for (auto e : c->ev_piece) cudaEventDestroy(e);
     for (auto e : c->ev_comp) cudaEventDestroy(e);
     for (auto e : c->ev_out) cudaEventDestroy(e);

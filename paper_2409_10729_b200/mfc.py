@@ -35,7 +35,7 @@ EXPORTED = [
     "mfc_rk3_steps", "mfc_max_wave_rate", "mfc_cfl_dt",
     "mfc_advance_host", "mfc_set_stream_chunks", "mfc_halo_exchange_group", "mfc_rhs_group", "mfc_rk3_step_group",
     "mfc_fused_halo_group", "mfc_peer_export", "mfc_peer_import",
-    "mfc_nccl_get_unique_id", "mfc_last_launch_count", "mfc_profile_enable", "mfc_profile_read", "mfc_finalize", "mfc_last_error",
+    "mfc_nccl_get_unique_id", "mfc_comm_status", "mfc_last_launch_count", "mfc_profile_enable", "mfc_profile_read", "mfc_finalize", "mfc_last_error",
     "mfc_version",
 ]
 
@@ -98,6 +98,7 @@ def _load():
         "mfc_peer_export": [vp, vp, vp],
         "mfc_peer_import": [vp, i32, vp],
         "mfc_nccl_get_unique_id": [vp],
+        "mfc_comm_status": [vp],
         "mfc_last_launch_count": [vp],
         "mfc_profile_enable": [vp, i32],
         "mfc_profile_read": [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), i32],
@@ -381,6 +382,11 @@ class Solver:
 
     def last_launch_count(self) -> int:
         return int(lib.mfc_last_launch_count(self._h))
+
+    def comm_status(self):
+        """Raise MfcError if the NCCL communicator saw an asynchronous error
+        (ncclCommGetAsyncError); a no-op without NCCL."""
+        _check(lib.mfc_comm_status(self._h), "mfc_comm_status")
 
     def close(self):
         if getattr(self, "_h", None):

@@ -155,6 +155,8 @@ def test_new_entry_points_validate_arguments(mfc):
         assert mfc.lib.mfc_rk3_steps(h, None, 1e-3, 1, None) != 0
         assert mfc.lib.mfc_rk3_steps(h, None, float("nan"), 1, None) == -1
         assert mfc.lib.mfc_rk3_step(h, None, 1e-3, None) != 0   # no workspace / NULL q
+        assert mfc.lib.mfc_comm_status(h) == 0                   # no NCCL communicator
+        assert mfc.lib.mfc_comm_status(None) == -1
     finally:
         mfc.lib.mfc_finalize(h)
 

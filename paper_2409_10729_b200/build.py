@@ -14,7 +14,7 @@ SO = os.path.join(HERE, "libmfc.so")
 SOURCES = ["mfc.cu", "sweep_n1.cu", "sweep_n2.cu", "sweep_n3.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "-Xptxas", "-v",
          f"-I{os.path.join(ROOT, 'include')}"]
 
 

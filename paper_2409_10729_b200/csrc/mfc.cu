@@ -1488,8 +1488,9 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
         c->lo_g[k] = ci * base + std::min<int64_t>(ci, rem);
         c->dx[k] = k < D ? (grid->hi[k] - grid->lo[k]) / (double)n : 1.0;
         if (k < D && p > 1 && c->nl[k] < kGhost) {
+            const long long nl = (long long)c->nl[k];
             delete c;
-            return fail(MFC_EINVAL, "dim %d: local extent %lld < 3", k, (long long)c->nl[k]);
+            return fail(MFC_EINVAL, "dim %d: local extent %lld < 3", k, nl);
         }
         if (k < D && bc[2 * k] == MFC_BC_PERIODIC && n < kGhost) {
             delete c;
@@ -1815,9 +1816,10 @@ int mfc_count_inadmissible(mfc_ctx* c, const double* q, int64_t* d_count, void* 
         default: e = launch_admissible<3>(c->D, a, o, s); break;
     }
     if (e != cudaSuccess) return fail(MFC_ECUDA, "admissibility launch: %s", cudaGetErrorString(e));
-    if (c->comm)
+    if (c->comm) {
         if ((st = comm_async_error(c))) return st;
         NCCL_TRY(ncclAllReduce(d_count, d_count, 1, ncclInt64, ncclSum, c->comm, s));
+    }
     return MFC_OK;
 }
 

@@ -164,6 +164,11 @@ def test_new_entry_points_validate_arguments(mfc):
 def test_ndim_needs_three_cells(mfc):
     rc, msg = _init(mfc, W.Problem("tiny", 2, 2, (8, 2, 1), gamma=(1.4, 1.4), pi_inf=(0, 0)))
     assert rc == -1 and "< 3" in msg
+    # a split dimension whose subdomains would be thinner than the ghost depth (the
+    # message reports the extent, read before the context is released)
+    pb = W.random_problem(3, (8, 8, 8), 2, "gas")
+    rc, msg = _init(mfc, pb, procs=(1, 1, 4), rank=0, nranks=4)
+    assert rc == -1 and "local extent 2 < 3" in msg
 
 
 def _ctx(mfc, pb, procs, rank, nranks, transport):

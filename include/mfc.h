@@ -80,8 +80,8 @@ typedef struct {
     int32_t procs[3];       /* rank grid; product == comm.nranks; {1,1,P} = z-slabs */
 } mfc_grid;
 
-/* Communicator.  nranks == 1: single domain, no NCCL.  For nranks > 1 the field
- * `loopback` selects the transport:
+/* Communicator.  nranks == 1: single domain, no NCCL (but see MFC_TRANSPORT_NCCL_SELF).
+ * For nranks > 1 the field `loopback` selects the transport:
  *   MFC_TRANSPORT_NCCL (0): one process per GPU, NCCL over NVLink; nccl_unique_id
  *       points to the 128-byte ncclUniqueId every rank received (e.g. broadcast with
  *       torch.distributed);
@@ -90,8 +90,18 @@ typedef struct {
  *   MFC_TRANSPORT_PEER (2): one process per rank, no NCCL; halos travel only as
  *       fused-halo stores into the neighbours' CUDA-IPC-mapped buffers
  *       (mfc_peer_export / mfc_peer_import below).  Works across GPUs with peer
- *       access and between processes sharing one GPU. */
-enum { MFC_TRANSPORT_NCCL = 0, MFC_TRANSPORT_LOOPBACK = 1, MFC_TRANSPORT_PEER = 2 };
+ *       access and between processes sharing one GPU;
+ *   MFC_TRANSPORT_NCCL_SELF (3): nranks == 1 only.  Every PERIODIC face is treated as a
+ *       rank face whose neighbour is this rank itself, and its ghost layers travel
+ *       through the NCCL halo path (pack -> ncclSend / ncclRecv to self on a one-rank
+ *       communicator -> unpack, overlapped on the comm stream) instead of the sweeps'
+ *       index maps; the reductions run as one-rank NCCL all-reduces.  Results are
+ *       bitwise those of the plain single domain.  A verification mode for the NCCL
+ *       code on one GPU (NCCL refuses two ranks on one device); nccl_unique_id may be
+ *       NULL (the context generates its own).  No streamed mfc_advance_host, no fused
+ *       halo. */
+enum { MFC_TRANSPORT_NCCL = 0, MFC_TRANSPORT_LOOPBACK = 1, MFC_TRANSPORT_PEER = 2,
+       MFC_TRANSPORT_NCCL_SELF = 3 };
 typedef struct {
     int32_t rank, nranks;
     const void* nccl_unique_id;

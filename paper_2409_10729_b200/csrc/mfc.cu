@@ -650,7 +650,8 @@ int exchange(mfc_ctx* const* cs, double* const* qs, int count, cudaStream_t s,
         if (physical && (st = bc_fill(cs[r], qs[r], s))) return st;
         if ((st = halo_pack(cs[r], qs[r], s))) return st;
     }
-    if (count == 1 && cs[0]->nranks > 1 && !cs[0]->loopback) {
+    if (count == 1 && (cs[0]->nranks > 1 || cs[0]->transport == MFC_TRANSPORT_NCCL_SELF) &&
+        !cs[0]->loopback) {
         mfc_ctx* c = cs[0];
         if (has_neighbors(c)) {
             int st = comm_async_error(c);
@@ -1071,7 +1072,8 @@ int copy_planes_h(const mfc_ctx* c, bool h2d, const double* host_in, double* hos
 // Chunk depth of the streamed step, 0 when the step is not streamed.
 int64_t stream_cz(const mfc_ctx* c) {
     const int chunks = c->stream_chunks;
-    if (chunks == 0 || c->D != 3 || c->nranks != 1 || c->fused || !c->ws) return 0;
+    if (chunks == 0 || c->D != 3 || c->nranks != 1 || c->fused || !c->ws || has_neighbors(c))
+        return 0;
     const int64_t nz = c->nl[2];
     const int64_t want = chunks > 1 ? chunks : kStreamChunks;
     const int64_t cz = std::max<int64_t>(kStageReach, (nz + want - 1) / want);
@@ -1472,9 +1474,13 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
     c->rank = rank;
     c->nranks = nranks;
     c->transport = comm ? comm->loopback : MFC_TRANSPORT_NCCL;
-    if (c->transport < MFC_TRANSPORT_NCCL || c->transport > MFC_TRANSPORT_PEER) {
+    if (c->transport < MFC_TRANSPORT_NCCL || c->transport > MFC_TRANSPORT_NCCL_SELF) {
         delete c;
-        return fail(MFC_EINVAL, "comm.loopback (transport) must be 0, 1 or 2");
+        return fail(MFC_EINVAL, "comm.loopback (transport) must be 0, 1, 2 or 3");
+    }
+    if (c->transport == MFC_TRANSPORT_NCCL_SELF && nranks != 1) {
+        delete c;
+        return fail(MFC_EINVAL, "MFC_TRANSPORT_NCCL_SELF is a one-rank mode (nranks = %d)", nranks);
     }
     c->loopback = c->transport == MFC_TRANSPORT_LOOPBACK;
     for (int k = 0; k < 3; ++k) c->procs[k] = grid->procs[k] > 0 ? grid->procs[k] : 1;
@@ -1504,6 +1510,11 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
             const int f = 2 * k + sd;
             c->bc[f] = bc[f];
             c->bc_phys[f] = bc[f];
+            if (c->transport == MFC_TRANSPORT_NCCL_SELF && bc[f] == MFC_BC_PERIODIC) {
+                c->bc[f] = BC_NEIGHBOR;      // a periodic face is a rank face with myself
+                c->nbr[f] = rank;
+                continue;
+            }
             if (c->procs[k] == 1) continue;
             int cc[3] = {c->coords[0], c->coords[1], c->coords[2]};
             cc[k] += sd ? 1 : -1;
@@ -1541,7 +1552,8 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
     // non-uniform grid coefficient tables, one per active axis (F4)
     for (int k = 0; k < D; ++k) need += nu_table_bytes(c, k);
     // streamed advance_host (single-rank 3D): dense staging rings for the PCIe copies
-    if (D == 3 && nranks == 1 && c->nl[2] >= 3 * kStageCzMin) {
+    if (D == 3 && nranks == 1 && c->transport != MFC_TRANSPORT_NCCL_SELF &&
+        c->nl[2] >= 3 * kStageCzMin) {
         c->stage_cz = std::max<int64_t>(kStageCzMin, (c->nl[2] + kStreamChunks - 1) / kStreamChunks);
         need += 2 * kStageSlots * stage_slot_bytes(c);
     }
@@ -1550,17 +1562,25 @@ int mfc_init(mfc_ctx** out, const mfc_grid* grid, int32_t n_fluids, const double
     // The device is only touched here when NCCL needs it; single-domain and loopback
     // contexts are pure host bookkeeping until the first GPU call (so layouts can be
     // queried on a machine without a GPU).
-    if (nranks > 1 && c->transport == MFC_TRANSPORT_NCCL) {
+    const bool self = c->transport == MFC_TRANSPORT_NCCL_SELF;
+    if ((nranks > 1 && c->transport == MFC_TRANSPORT_NCCL) || self) {
         if (cudaSetDevice(device) != cudaSuccess) {
             delete c;
             return fail(MFC_ECUDA, "cudaSetDevice(%d) failed", device);
         }
-        if (!comm->nccl_unique_id) {
+        ncclUniqueId id;
+        if (comm->nccl_unique_id) {
+            memcpy(&id, comm->nccl_unique_id, sizeof id);
+        } else if (self) {           // a one-rank communicator: its own id
+            const ncclResult_t r = ncclGetUniqueId(&id);
+            if (r != ncclSuccess) {
+                delete c;
+                return fail(MFC_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+            }
+        } else {
             delete c;
             return fail(MFC_EINVAL, "nccl_unique_id is NULL with nranks > 1");
         }
-        ncclUniqueId id;
-        memcpy(&id, comm->nccl_unique_id, sizeof id);
         ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
         if (r != ncclSuccess) {
             delete c;
@@ -2014,7 +2034,8 @@ int mfc_fused_halo_group(mfc_ctx* const* cs, double* const* qs, int32_t count) {
         int st;
         if (!cs[r]) return fail(MFC_EINVAL, "NULL ctx");
         if ((st = need_ws(cs[r], true)) || (st = check_ptr(qs[r], "q"))) return st;
-        if (cs[r]->transport != MFC_TRANSPORT_LOOPBACK && count > 1)
+        if ((cs[r]->transport != MFC_TRANSPORT_LOOPBACK && count > 1) ||
+            cs[r]->transport == MFC_TRANSPORT_NCCL_SELF)
             return fail(MFC_EINVAL, "fused group needs loopback contexts");
     }
     for (int r = 0; r < count; ++r) {

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # MFC_LIB: an alternative in-tree build (same-box A/B timing, tools/build_ab.sh)
 SO_PATH = os.environ.get("MFC_LIB") or os.path.join(_HERE, "libmfc.so")
 
-TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER = 0, 1, 2
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER, TRANSPORT_NCCL_SELF = 0, 1, 2, 3
 PEER_BLOB_BYTES = 512
 
 BC_PERIODIC = -1
@@ -179,7 +179,10 @@ class Solver:
     """One subdomain (rank) of the 5-equation RHS / SSP-RK3 path on one GPU."""
 
     def __init__(self, problem, *, procs=(1, 1, 1), rank=0, nranks=1, nccl_id: bytes | None = None,
-                 loopback=False, peer=False, device=None, weno_eps=None, n_global=None):
+                 loopback=False, peer=False, nccl_self=False, device=None, weno_eps=None,
+                 n_global=None):
+        """nccl_self: one rank whose periodic faces go through the NCCL halo path
+        (send / recv to itself; MFC_TRANSPORT_NCCL_SELF, a one-GPU check of that code)."""
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device)
@@ -198,7 +201,8 @@ class Solver:
         bc = (ctypes.c_int32 * 6)(*problem.bc)
         comm = _Comm()
         comm.rank, comm.nranks = rank, nranks
-        comm.loopback = TRANSPORT_PEER if peer else (TRANSPORT_LOOPBACK if loopback else TRANSPORT_NCCL)
+        comm.loopback = (TRANSPORT_NCCL_SELF if nccl_self else TRANSPORT_PEER if peer
+                         else TRANSPORT_LOOPBACK if loopback else TRANSPORT_NCCL)
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         comm.nccl_unique_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id else None
         h = ctypes.c_void_p()

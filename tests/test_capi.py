@@ -45,7 +45,8 @@ def test_library_is_sm100a_cubin():
     assert "sm_100a" in out
 
 
-def _init(mfc, pb, procs=(1, 1, 1), rank=0, nranks=1, gamma=None, pinf=None, bc=None):
+def _init(mfc, pb, procs=(1, 1, 1), rank=0, nranks=1, gamma=None, pinf=None, bc=None,
+          transport=1):
     g = mfc._Grid()
     g.ndim = pb.ndim
     for k in range(3):
@@ -57,7 +58,7 @@ def _init(mfc, pb, procs=(1, 1, 1), rank=0, nranks=1, gamma=None, pinf=None, bc=
     pi = (ctypes.c_double * N)(*(pinf or pb.pi_inf))
     b = (ctypes.c_int32 * 6)(*(bc or pb.bc))
     c = mfc._Comm()
-    c.rank, c.nranks, c.loopback = rank, nranks, 1
+    c.rank, c.nranks, c.loopback = rank, nranks, transport
     h = ctypes.c_void_p()
     rc = mfc.lib.mfc_init(ctypes.byref(h), ctypes.byref(g), N, gam, pi, b, ctypes.byref(c), 0)
     if rc == 0:
@@ -76,6 +77,9 @@ def test_argument_validation(mfc):
     assert _init(mfc, pb, procs=(1, 1, 8), nranks=8)[0] == -1      # 2 cells per rank < 3
     rc, msg = _init(mfc, W.Problem("bad", 4, 1, (8, 1, 1), gamma=(1.4,) * 4, pi_inf=(0,) * 4))
     assert rc == -1 and "n_fluids" in msg
+    assert _init(mfc, pb, transport=4)[0] == -1                    # unknown transport
+    rc, msg = _init(mfc, pb, procs=(1, 1, 2), nranks=2, transport=mfc.TRANSPORT_NCCL_SELF)
+    assert rc == -1 and "one-rank" in msg                          # NCCL self: 1 rank only
 
 
 def test_layout_alignment_and_sizes(mfc):

@@ -3,7 +3,9 @@ problem on the same device) with the exchanged halo (pack -> device copy -> unpa
 stage, overlapped on a comm stream) versus the fused halo (the last sweep of each stage
 stores boundary layers straight into the neighbours' ghost layers).
 
-usage: python tools/halo_bench.py [--steps 10] > profiles/halo_<tag>.jsonl
+usage: python tools/halo_bench.py [--steps 10] [--nccl-self] > profiles/halo_<tag>.jsonl
+(--nccl-self: the single domain against MFC_TRANSPORT_NCCL_SELF, where every periodic face
+goes pack -> NCCL send/recv to self -> unpack: the NCCL path's cost on one GPU.)
 Each line: config, mode, ms per step (CUDA events), halo-kernel ms per step, kernel
 launches per step.  Synthetic C3 fields (workloads.c3_prims), fp64.
 """
@@ -26,7 +28,10 @@ def run(n, procs, mode, steps, warmup):
     pb = W.c3_droplet(n)
     v = W.c3_prims(pb)
     P = int(np.prod(procs))
-    solvers = [mfc.Solver(pb, procs=procs, rank=r, nranks=P, loopback=True) for r in range(P)]
+    if mode == "nccl-self":   # one rank, every periodic face through NCCL send/recv to self
+        solvers = [mfc.Solver(pb, nccl_self=True)]
+    else:
+        solvers = [mfc.Solver(pb, procs=procs, rank=r, nranks=P, loopback=True) for r in range(P)]
     qs = []
     for s in solvers:
         L = s.layout
@@ -53,7 +58,9 @@ def run(n, procs, mode, steps, warmup):
     finite = all(bool(torch.isfinite(s.interior(q)).all()) for s, q in zip(solvers, qs))
     for s in solvers:
         s.close()
-    return {"config": f"C3 {n}^3 as {procs} loopback subdomains on 1 GPU", "mode": mode,
+    cfg = (f"C3 {n}^3, one rank, all 6 periodic faces through libmfc's NCCL halo (self)"
+           if mode == "nccl-self" else f"C3 {n}^3 as {procs} loopback subdomains on 1 GPU")
+    return {"config": cfg, "mode": mode,
             "ms_per_step": e0.elapsed_time(e1) / steps, "halo_kernel_ms_per_step": halo_ms / steps,
             "launches_per_step": launches / steps, "finite": finite}
 
@@ -62,7 +69,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="only the single domain and the NCCL self-exchange of C3 256^3")
     args = ap.parse_args()
+    if args.nccl_self:
+        for mode in ("single", "nccl-self"):
+            print(json.dumps(run(256, (1, 1, 1), mode, args.steps, args.warmup)), flush=True)
+        return
     for n in (256, 128, 64):              # the single domain of each size, for reference
         print(json.dumps(run(n, (1, 1, 1), "single", args.steps, args.warmup)), flush=True)
     for n, procs in ((256, (1, 1, 2)), (256, (1, 2, 2)), (128, (2, 2, 2)), (64, (2, 2, 2))):

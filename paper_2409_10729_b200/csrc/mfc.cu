@@ -195,21 +195,48 @@ struct FaceGeom {
     int32_t E;
 };
 
+// Element t of the 3 layers next to a face of dimension dir (E x 3 x area elements):
+// consecutive t walk along x wherever x is a transverse axis, so the warps' loads and
+// stores are coalesced rows:  dir z: (x, y, j, e), dir y: (x, z, j, e);  across an x
+// face, where a row holds only the 3 layer cells, the layer index runs fastest:
+// (j, y, z, e).  Returns e; off = the element's offset from g.base + e g.sE with the
+// coordinate along dir at 0, j = its layer, sd = the stride along dir.  (Scalars and
+// selects only: a coordinate array indexed by the runtime dir lives in local memory.)
+__device__ __forceinline__ int face_elem(int64_t t, const FaceGeom& g, int dir, int64_t& off,
+                                         int& j, int64_t& sd) {
+    int64_t r = t;
+    if (dir == 0) {
+        j = (int)(r % kGhost); r /= kGhost;
+        const int64_t y = r % g.n[1]; r /= g.n[1];
+        const int64_t z = r % g.n[2]; r /= g.n[2];
+        off = y * g.s[1] + z * g.s[2];
+        sd = 1;
+    } else {
+        const int64_t x = r % g.n[0]; r /= g.n[0];
+        const int no = dir == 1 ? g.n[2] : g.n[1];
+        const int64_t o = r % no; r /= no;
+        j = (int)(r % kGhost); r /= kGhost;
+        off = x + o * (dir == 1 ? g.s[2] : g.s[1]);
+        sd = dir == 1 ? g.s[1] : g.s[2];
+    }
+    return (int)r;
+}
+
 // Physical-boundary ghost fill along dimension `dir`, both sides (S1 of DESIGN.md §3):
 // periodic: ghost -1-j <- n-1-j, ghost n+j <- j; extrapolation: <- adjacent interior;
 // reflective: mirror with the normal momentum (equation mom) negated.
-__global__ void bc_fill_kernel(double* q, FaceGeom g, int dir, int bc_lo, int bc_hi, int mom) {
+__global__ void bc_fill_kernel(double* q, const __grid_constant__ FaceGeom g, int dir, int bc_lo, int bc_hi, int mom) {
     const int t1 = (dir + 1) % 3, t2 = (dir + 2) % 3;
-    const int64_t area = (int64_t)g.n[t1] * g.n[t2];
-    const int64_t total = area * kGhost * 2 * g.E;
+    const int64_t face = (int64_t)g.n[t1] * g.n[t2] * kGhost;
+    const int64_t total = face * 2 * g.E;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = t;
-        const int a = (int)(r % g.n[t1]); r /= g.n[t1];
-        const int b = (int)(r % g.n[t2]); r /= g.n[t2];
-        const int j = (int)(r % kGhost); r /= kGhost;
-        const int side = (int)(r % 2); r /= 2;
-        const int e = (int)r;
+        const int64_t es = t / face;           // (side, e) = (es % 2, es / 2)
+        const int side = (int)(es % 2);
+        const int e = (int)(es / 2);
+        int64_t off, sd;
+        int j;
+        face_elem(t - es * face, g, dir, off, j, sd);
         const int bc = side ? bc_hi : bc_lo;
         if (bc == BC_NEIGHBOR) continue;
         const int n = g.n[dir];
@@ -221,38 +248,70 @@ __global__ void bc_fill_kernel(double* q, FaceGeom g, int dir, int bc_lo, int bc
             ghost = n + j;
             src = bc == MFC_BC_PERIODIC ? j : (bc == MFC_BC_REFLECTIVE ? n - 1 - j : n - 1);
         }
-        const int64_t c0 = g.base + e * g.sE + a * g.s[t1] + b * g.s[t2];
-        double v = q[c0 + (int64_t)src * g.s[dir]];
+        const int64_t c0 = g.base + e * g.sE + off;
+        double v = q[c0 + (int64_t)src * sd];
         if (bc == MFC_BC_REFLECTIVE && e == mom) v = -v;
-        q[c0 + (int64_t)ghost * g.s[dir]] = v;
+        q[c0 + (int64_t)ghost * sd] = v;
     }
 }
 
-// Halo pack/unpack for the face `side` of dimension `dir`: buffer layout
-// [e][layer j = 0..2][b][a] (a fastest).  Pack reads the 3 interior layers next to
-// the face (layer j = interior index j on the low side, n-3+j on the high side);
-// unpack writes the 3 ghost layers (-3+j low, n+j high), so a buffer packed on one
-// rank's high face unpacks verbatim into the neighbour's low ghosts.
-__global__ void halo_pack_kernel(const double* q, double* buf, FaceGeom g, int dir, int side,
-                                 bool unpack, double* qout) {
-    const int t1 = (dir + 1) % 3, t2 = (dir + 2) % 3;
-    const int64_t area = (int64_t)g.n[t1] * g.n[t2];
-    const int64_t total = area * kGhost * g.E;
+// Halo pack/unpack of every rank face of a subdomain in ONE launch.  Buffer element t
+// of a face is face_elem's element t (x fastest where x is transverse, the layer index
+// across an x face), viewed as rows of length L: z and y faces rows of n_x cells (one
+// per (other transverse coordinate, layer, e)), x faces rows of 3 n_y (layer, y) pairs
+// (one per (z, e)).  Block (row, face): the row's coordinates are formed once per
+// block, in 32-bit arithmetic; its threads stride along the row (coalesced).  Pack
+// reads the 3 interior layers next to the face (layer j = interior index j on the low
+// side, n-3+j on the high side); unpack writes the 3 ghost layers (-3+j low, n+j high),
+// so a buffer packed on one rank's high face unpacks verbatim into the neighbour's low
+// ghosts.
+struct FaceSet {
+    int nf;
+    int dir[6], side[6];
+    double* buf[6];
+};
+
+__device__ __forceinline__ int face_rows(const int32_t n[3], int E, int dir) {
+    return dir == 0 ? n[2] * E : (dir == 1 ? n[2] : n[1]) * kGhost * E;
+}
+
+// (__grid_constant__: fs stays in the parameter bank and is indexed by blockIdx.y there;
+//  a by-value copy indexed dynamically went through every thread's local memory: 23x
+//  the L2 write traffic of the packed data, r221)
+__global__ void halo_pack_kernel(double* q, const __grid_constant__ FaceGeom g,
+                                 const __grid_constant__ FaceSet fs,
+                                 bool unpack) {
+    const int f = blockIdx.y;
+    const int dir = fs.dir[f], side = fs.side[f];
+    const int rows = face_rows(g.n, g.E, dir);
     const int n = g.n[dir];
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = t;
-        const int a = (int)(r % g.n[t1]); r /= g.n[t1];
-        const int b = (int)(r % g.n[t2]); r /= g.n[t2];
-        const int j = (int)(r % kGhost); r /= kGhost;
-        const int e = (int)r;
-        const int64_t c0 = g.base + e * g.sE + a * g.s[t1] + b * g.s[t2];
-        if (!unpack) {
-            const int src = side == 0 ? j : n - kGhost + j;
-            buf[t] = q[c0 + (int64_t)src * g.s[dir]];
-        } else {
-            const int dst = side == 0 ? j - kGhost : n + j;
-            qout[c0 + (int64_t)dst * g.s[dir]] = buf[t];
+    const int L = dir == 0 ? kGhost * g.n[1] : g.n[0];
+    const int64_t sd = dir == 0 ? 1 : (dir == 1 ? g.s[1] : g.s[2]);     // stride along dir
+    double* const buf = fs.buf[f];
+    auto layer = [&](int j) {             // the index along dir that layer j reads / writes
+        return !unpack ? (side == 0 ? j : n - kGhost + j) : (side == 0 ? j - kGhost : n + j);
+    };
+    for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+        double* const b = buf + (int64_t)row * L;
+        if (dir == 0) {                       // row = z + n_z e; element i = j + 3 y
+            const int z = row % g.n[2], e = row / g.n[2];
+            const int64_t r0 = g.base + e * g.sE + z * g.s[2];
+            for (int i = threadIdx.x; i < L; i += blockDim.x) {
+                const int j = i % kGhost, y = i / kGhost;
+                const int64_t a = r0 + y * g.s[1] + layer(j);
+                if (!unpack) b[i] = q[a];
+                else q[a] = b[i];
+            }
+        } else {                              // row = o + n_o (j + 3 e); element i = x
+            const int no = dir == 1 ? g.n[2] : g.n[1];
+            const int64_t so = dir == 1 ? g.s[2] : g.s[1];
+            const int o = row % no, je = row / no;
+            const int j = je % kGhost, e = je / kGhost;
+            const int64_t r0 = g.base + e * g.sE + o * so + layer(j) * sd;
+            for (int i = threadIdx.x; i < L; i += blockDim.x) {
+                if (!unpack) b[i] = q[r0 + i];
+                else q[r0 + i] = b[i];
+            }
         }
     }
 }
@@ -328,20 +387,34 @@ PeerFace make_peer_face(const mfc_ctx* c, int f, double* nbuf, const Lay& L, con
 
 // Fused-halo exchange of a state (mfc_halo_exchange / mfc_rhs in fused mode): my 3
 // interior layers next to face p go straight into the neighbour's ghost layers.
-__global__ void peer_exchange_kernel(const double* q, FaceGeom g, PeerFace p) {
+__global__ void peer_exchange_kernel(const double* q, const __grid_constant__ FaceGeom g,
+                                     PeerFace p) {
     const int k = p.dim, t1 = (k + 1) % 3, t2 = (k + 2) % 3;
-    const int64_t area = (int64_t)g.n[t1] * g.n[t2];
-    const int64_t total = area * kGhost * g.E;
+    const int64_t total = (int64_t)g.n[t1] * g.n[t2] * kGhost * g.E;
+    // the neighbour's strides along the transverse axes and along k
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = t;
-        int xyz[3];
-        xyz[t1] = (int)(r % g.n[t1]); r /= g.n[t1];
-        xyz[t2] = (int)(r % g.n[t2]); r /= g.n[t2];
-        xyz[k] = p.lo + (int)(r % kGhost); r /= kGhost;
-        const int64_t e = r;
-        const double v = q[g.base + e * g.sE + xyz[0] + xyz[1] * g.s[1] + xyz[2] * g.s[2]];
-        p.dst[p.off + e * p.sE + xyz[0] + xyz[1] * p.sy + xyz[2] * p.sz] = v;
+        int64_t off, sd;
+        int j;
+        const int64_t e = face_elem(t, g, k, off, j, sd);
+        // my element (x, y, z) -> the neighbour's (x, y, z) + p.off: recompute its offset
+        // from my coordinates (the layouts differ in padding)
+        int64_t x, y, z;
+        if (k == 0) {
+            x = p.lo + j;
+            y = (t / kGhost) % g.n[1];
+            z = (t / kGhost / g.n[1]) % g.n[2];
+        } else if (k == 1) {
+            x = t % g.n[0];
+            z = (t / g.n[0]) % g.n[2];
+            y = p.lo + j;
+        } else {
+            x = t % g.n[0];
+            y = (t / g.n[0]) % g.n[1];
+            z = p.lo + j;
+        }
+        const double v = q[g.base + e * g.sE + off + (int64_t)(p.lo + j) * sd];
+        p.dst[p.off + e * p.sE + x + y * p.sy + z * p.sz] = v;
     }
 }
 
@@ -573,33 +646,35 @@ int bc_fill(mfc_ctx* c, double* q, cudaStream_t s) {
     return MFC_OK;
 }
 
-int halo_pack(mfc_ctx* c, const double* q, cudaStream_t s) {
+// one launch packs (or unpacks) every rank face of c
+int halo_faces(mfc_ctx* c, double* q, bool unpack, cudaStream_t s) {
     const FaceGeom g = geom(c);
+    FaceSet fs{};
+    int rows = 0;
     for (int f = 0; f < 2 * c->D; ++f) {
         if (c->bc[f] != BC_NEIGHBOR) continue;
         const int dir = f / 2;
-        ProfScope ps(c, s, K_HALO);
-        halo_pack_kernel<<<grid_for(c->face_elems[dir], 256), 256, 0, s>>>(
-            q, c->sendb[f], g, dir, f % 2, false, nullptr);
-        CU_TRY(cudaGetLastError());
-        ++c->launches;
+        fs.dir[fs.nf] = dir;
+        fs.side[fs.nf] = f % 2;
+        fs.buf[fs.nf] = unpack ? c->recvb[f] : c->sendb[f];
+        ++fs.nf;
+        const int64_t r = dir == 0 ? c->nl[2] * c->E : (dir == 1 ? c->nl[2] : c->nl[1]) * kGhost * c->E;
+        rows = (int)std::max<int64_t>(rows, r);
     }
+    if (fs.nf == 0) return MFC_OK;
+    ProfScope ps(c, s, K_HALO);
+    const dim3 grid((unsigned)std::min(rows, 148 * 64), (unsigned)fs.nf);
+    halo_pack_kernel<<<grid, 256, 0, s>>>(q, g, fs, unpack);
+    CU_TRY(cudaGetLastError());
+    ++c->launches;
     return MFC_OK;
 }
 
-int halo_unpack(mfc_ctx* c, double* q, cudaStream_t s) {
-    const FaceGeom g = geom(c);
-    for (int f = 0; f < 2 * c->D; ++f) {
-        if (c->bc[f] != BC_NEIGHBOR) continue;
-        const int dir = f / 2;
-        ProfScope ps(c, s, K_HALO);
-        halo_pack_kernel<<<grid_for(c->face_elems[dir], 256), 256, 0, s>>>(
-            nullptr, c->recvb[f], g, dir, f % 2, true, q);
-        CU_TRY(cudaGetLastError());
-        ++c->launches;
-    }
-    return MFC_OK;
+int halo_pack(mfc_ctx* c, const double* q, cudaStream_t s) {
+    return halo_faces(c, const_cast<double*>(q), false, s);
 }
+
+int halo_unpack(mfc_ctx* c, double* q, cudaStream_t s) { return halo_faces(c, q, true, s); }
 
 bool has_neighbors(const mfc_ctx* c) {
     for (int f = 0; f < 2 * c->D; ++f)

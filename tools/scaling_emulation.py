@@ -14,12 +14,15 @@ measure what decomposition costs in kernels (halo work, per-rank kernel efficien
 the smaller slab, launch count) -- not the NVLink transfer, which a real P-GPU run adds
 (25 MB per rank per RHS for C4, overlapped with the x/y sweeps).
 
-usage: python tools/scaling_emulation.py [--steps 5] > profiles/scaling_emulation_<tag>.jsonl
+usage: python tools/scaling_emulation.py [--steps 5] [--soak 3] > profiles/scaling_emulation_<tag>.jsonl
+(every configuration is timed after --soak seconds of untimed steps, so all of them run in
+the same power-capped state; r214/r224 had no soak and timed the single domain cold.)
 """
 import argparse
 import json
 import os
 import sys
+import time
 
 import numpy as np
 import torch
@@ -31,7 +34,7 @@ from paper_2409_10729_b200 import mfc  # noqa: E402
 from paper_2409_10729_b200 import workloads as W  # noqa: E402
 
 
-def group_step_ms(pb, prims_of, P, mode, steps, warmup):
+def group_step_ms(pb, prims_of, P, mode, steps, warmup, soak=0.0):
     procs = (1, 1, P)
     solvers = [mfc.Solver(pb, procs=procs, rank=r, nranks=P, loopback=True) for r in range(P)]
     qs = []
@@ -45,6 +48,12 @@ def group_step_ms(pb, prims_of, P, mode, steps, warmup):
     for _ in range(warmup):
         mfc.rk3_step_group(solvers, qs, pb.dt)
     torch.cuda.synchronize()
+    # heat soak: the boards cap power near 380 W and an FP64-bound step reaches the cap
+    # within about a second, so every configuration is timed in the same (hot) state
+    t0 = time.time()
+    while time.time() - t0 < soak:
+        mfc.rk3_step_group(solvers, qs, pb.dt)
+        torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     launches = 0
@@ -67,6 +76,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--ranks", default="1,2,4,8")
     ap.add_argument("--cases", default="C4,C5")
+    ap.add_argument("--soak", type=float, default=3.0,
+                    help="seconds of untimed steps before each timed run (power-cap state)")
     args = ap.parse_args()
     ranks = [int(x) for x in args.ranks.split(",")]
     for case in args.cases.split(","):
@@ -81,7 +92,8 @@ def main():
                 pb = W.c5_three_fluid(512)
                 prims_of = lambda z0, z1, pb=pb: W.c5_prims(pb, z0, z1)
             for mode in (("exchanged", "fused") if P > 1 else ("single",)):
-                ms, launches, finite = group_step_ms(pb, prims_of, P, mode, args.steps, args.warmup)
+                ms, launches, finite = group_step_ms(pb, prims_of, P, mode, args.steps, args.warmup,
+                                                     args.soak)
                 if P == 1:
                     base = ms
                 eff = (base / (ms / P)) if case == "C4" else (base / ms)

@@ -50,7 +50,7 @@ def _run(pb, q, dt, nsteps, **kw):
     return out
 
 
-@pytest.mark.parametrize("case", range(len(CASES)))
+@pytest.mark.parametrize("case", range(len(CASES)), ids=[f"case{i}" for i in range(len(CASES))])
 def test_nccl_self_exchange_bitwise(case):
     d, n, N, bc = CASES[case]
     pb = W.random_problem(d, n[:d], N, "water", bc=bc)

@@ -246,55 +246,97 @@ def run_ours(args):
         return p
 
     n = args.n
-    nid = mfc.broadcast_unique_id() if world > 1 and not peer else None
     procs = (1, 1, world)
-    if args.config == "C3":
-        block = W.c3_droplet(n)                  # the per-GPU block (C3 / C4)
-        if world == 1:
-            pb = block
-            workload = f"C3 3D two-fluid shock-droplet {n}^3 (BASELINE configs[2])"
-        else:
-            pb = W.c3_droplet(n, nz=n * world)   # global domain: blocks stacked along z
-            workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
-        if args.stretch:      # F4: tanh-refined grid on every axis of the global domain
-            pb = W.stretched(pb)
-            block = W.stretched(block)
-            workload += ", tanh-stretched grid (F4)"
-        s = mfc.Solver(variant(pb), procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
-                       peer=peer)
-        # every rank holds the same C3 block (its local prims), converted on the GPU
-        q = s.state_from_prims(W.c3_prims(block))
-        dt = block.dt
-        if args.stretch:      # CFL of the smallest cell
-            dt *= min(np.diff(pb.boundaries(k)).min() for k in range(3)) / min(pb.dx)
-    elif args.config == "C5" and args.stretch:
-        raise SystemExit("--stretch runs C3 / C4 only")
-    elif args.config == "C5":
-        nn = args.n if args.n != 256 else 512
-        pb = W.c5_three_fluid(nn)                # strong scaling: fixed 512^3 split in z-slabs
-        workload = f"C5 3D three-fluid shock-droplet {nn}^3 total, z-slabs x{world} (BASELINE configs[4])"
-        s = mfc.Solver(variant(pb), procs=procs, rank=rank, nranks=world, nccl_id=nid, device=local,
-                       peer=peer)
-        L0 = s.layout
-        v = s.empty_state()
-        vi = s.interior(v)
-        z0, nzl = L0.lo_global[2], L0.n_local[2]
-        for zz in range(0, nzl, 64):             # slab-wise host generation
-            vi[:, zz:zz + 64].copy_(torch.as_tensor(W.c5_prims(pb, z0 + zz, z0 + min(zz + 64, nzl))))
-        q = s.empty_state()
-        s.prim_to_cons(v, q)
-        del v, vi
-        dt = pb.dt
-    else:                                        # C2, single GPU
-        pb = W.c2_shock_bubble()
-        workload = "C2 2D air-helium shock-bubble 1024x512 (BASELINE configs[1])"
-        s = mfc.Solver(variant(pb), procs=(1, 1, 1), device=local)
-        q = s.state_from_prims(W.c2_prims(pb))
-        dt = pb.dt
-    if world > 1 and args.halo in ("fused", "peer"):
-        # F1: stage sweeps store boundary layers into the neighbours' IPC-mapped ghosts
-        s.attach_fused_halo(q)
-        s.halo_exchange(q)
+
+    def make(halo):
+        """(solver, state, dt, problem, block, workload) of the configuration; `halo` picks
+        the N > 1 transport (NCCL for 'nccl' and 'fused', none for the gloo 'peer' mode)."""
+        nid = mfc.broadcast_unique_id() if world > 1 and halo != "peer" else None
+        pm = halo == "peer"
+        block = None
+        if args.config == "C3":
+            block = W.c3_droplet(n)                  # the per-GPU block (C3 / C4)
+            if world == 1:
+                pb = block
+                workload = f"C3 3D two-fluid shock-droplet {n}^3 (BASELINE configs[2])"
+            else:
+                pb = W.c3_droplet(n, nz=n * world)   # global domain: blocks stacked along z
+                workload = f"C4 weak scaling: C3 {n}^3 block per GPU, z-slabs (BASELINE configs[3])"
+            if args.stretch:      # F4: tanh-refined grid on every axis of the global domain
+                pb = W.stretched(pb)
+                block = W.stretched(block)
+                workload += ", tanh-stretched grid (F4)"
+            s = mfc.Solver(variant(pb), procs=procs, rank=rank, nranks=world, nccl_id=nid,
+                           device=local, peer=pm)
+            # every rank holds the same C3 block (its local prims), converted on the GPU
+            q = s.state_from_prims(W.c3_prims(block))
+            dt = block.dt
+            if args.stretch:      # CFL of the smallest cell
+                dt *= min(np.diff(pb.boundaries(k)).min() for k in range(3)) / min(pb.dx)
+        elif args.config == "C5" and args.stretch:
+            raise SystemExit("--stretch runs C3 / C4 only")
+        elif args.config == "C5":
+            nn = args.n if args.n != 256 else 512
+            pb = W.c5_three_fluid(nn)                # strong scaling: fixed 512^3 split in z-slabs
+            workload = f"C5 3D three-fluid shock-droplet {nn}^3 total, z-slabs x{world} (BASELINE configs[4])"
+            s = mfc.Solver(variant(pb), procs=procs, rank=rank, nranks=world, nccl_id=nid,
+                           device=local, peer=pm)
+            L0 = s.layout
+            v = s.empty_state()
+            vi = s.interior(v)
+            z0, nzl = L0.lo_global[2], L0.n_local[2]
+            for zz in range(0, nzl, 64):             # slab-wise host generation
+                vi[:, zz:zz + 64].copy_(torch.as_tensor(W.c5_prims(pb, z0 + zz, z0 + min(zz + 64, nzl))))
+            q = s.empty_state()
+            s.prim_to_cons(v, q)
+            del v, vi
+            dt = pb.dt
+        else:                                        # C2, single GPU
+            pb = W.c2_shock_bubble()
+            workload = "C2 2D air-helium shock-bubble 1024x512 (BASELINE configs[1])"
+            s = mfc.Solver(variant(pb), procs=(1, 1, 1), device=local)
+            q = s.state_from_prims(W.c2_prims(pb))
+            dt = pb.dt
+        return s, q, dt, pb, block, workload
+
+    halo = args.halo if world > 1 else "none"
+    halo_fallback = None
+    s, q, dt, pb, block, workload = make(halo)
+    if world > 1 and halo in ("fused", "peer"):
+        # F1: stage sweeps store boundary layers into the neighbours' IPC-mapped ghosts.
+        # The attach and one trial step are checked collectively: if CUDA IPC or the stream
+        # memory operations are unavailable between these GPUs on ANY rank, every rank
+        # drops to the NCCL pack / send-recv / unpack halo (reported in config.halo_fallback)
+        err = None
+        try:
+            blob = s.peer_export(q)
+            torch.cuda.synchronize()
+            blobs = [None] * world
+            dist.all_gather_object(blobs, blob)
+            for face, blob_f in mfc.face_blobs(s.neighbors, blobs).items():
+                s.peer_import(face, blob_f)
+        except mfc.MfcError as ex:
+            err = str(ex)
+        ok = [err is None]
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)
+        if all(o[0] for o in oks):
+            try:
+                s.halo_exchange(q)
+                s.rk3_step(q, dt)
+                torch.cuda.synchronize()
+            except mfc.MfcError as ex:
+                err = str(ex)
+            dist.all_gather_object(oks, [err is None])
+        if not all(o[0] for o in oks):
+            if halo == "peer":
+                raise SystemExit(f"--halo peer: fused halo unavailable ({err})")
+            halo_fallback = f"fused halo unavailable ({err or 'on another rank'}); NCCL halo"
+            s.close()
+            del q
+            halo = "nccl"
+            s, q, dt, pb, block, workload = make(halo)
+        dist.barrier()
     L = s.layout
     stream = torch.cuda.current_stream()
 
@@ -436,7 +478,8 @@ def run_ours(args):
                           "before every timed step, outside its events" if flush else
                           f"inputs > L2: each state buffer {8 * L.n_elems / 1e9:.2f} GB >> 126 MB, no flush"),
                    "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
-                   "halo": (args.halo if world > 1 else "none"),
+                   "halo": halo,
+                   **({"halo_fallback": halo_fallback} if halo_fallback else {}),
                    **({"grid": "tanh-refined on every axis (F4): cells 0.625x finer in "
                               "[0.3, 0.7], workloads.tanh_boundaries"} if args.stretch else {}),
                    **({"weno": {"3": "WENO3-JS", "5m": "WENO5-M (mapped)"}[args.weno]}

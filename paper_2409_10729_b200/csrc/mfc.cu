@@ -431,8 +431,15 @@ __global__ void peer_exchange_kernel(const double* q, const __grid_constant__ Fa
 // t = (x - x_m)/dx_m of cell m (widths and positions scaled by dx_m), so b = q'(0) and
 // c = q''(0)/2 are the t-polynomial's coefficients and beta = b^2 + (13/3) c^2.
 
+// the coefficient-major table (NU_NCOEF rows of n + 6 cells; the x tile reads a row per
+// coefficient across its lanes), then a cell-major copy (NU_CM doubles per cell, 256-byte
+// aligned; a march step reads the 31 coefficients of one cell, warp-uniform)
+size_t nu_cm_offset(const mfc_ctx* c, int k) {       // in doubles
+    return ((size_t)NU_NCOEF * (c->nl[k] + 2 * kGhost) + NU_CM - 1) / NU_CM * NU_CM;
+}
 size_t nu_table_bytes(const mfc_ctx* c, int k) {
-    return ((size_t)NU_NCOEF * (c->nl[k] + 2 * kGhost) * sizeof(double) + 255) / 256 * 256;
+    return ((nu_cm_offset(c, k) + (size_t)NU_CM * (c->nl[k] + 2 * kGhost)) * sizeof(double) + 255) /
+           256 * 256;
 }
 
 bool any_stretched(const mfc_ctx* c) {
@@ -560,6 +567,11 @@ int upload_nu_table(mfc_ctx* c, int k) {
         T(NU_INV, m) = 1.0 / h;
     }
     CU_TRY(cudaMemcpy(c->nu[k], tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    std::vector<double> cm((size_t)NU_CM * ld, 0.0);
+    for (int64_t m = 0; m < ld; ++m)
+        for (int cf = 0; cf < NU_NCOEF; ++cf) cm[(size_t)m * NU_CM + cf] = tab[(size_t)cf * ld + m];
+    CU_TRY(cudaMemcpy(c->nu[k] + nu_cm_offset(c, k), cm.data(), cm.size() * sizeof(double),
+                      cudaMemcpyHostToDevice));
     return MFC_OK;
 }
 
@@ -958,6 +970,7 @@ int launch_sweep_dir(mfc_ctx* c, int dir, int mode, const double* q, const doubl
     const bool nu = !c->xcb[dir].empty();
     const int ord = nu ? 7 : ((c->weno_order == 5 && c->weno_mapped) ? 6 : c->weno_order);
     a.nu = nu ? c->nu[dir] : nullptr;
+    a.nuc = nu ? c->nu[dir] + nu_cm_offset(c, dir) : nullptr;
     a.nu_ld = c->nl[dir] + 2 * kGhost;
     switch (c->N) {
         case 1: e = launch_sweep<1>(c->D, dir, mode, ord, a, grid, block, s); break;

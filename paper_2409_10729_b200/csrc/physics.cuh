@@ -308,6 +308,14 @@ __device__ __forceinline__ void weno5_fewop(double a, double b, double c, double
 //   beta_k = b_k² + s_k²,  t_k = (beta_k + eps)²,  P_k = product of the other two t_j,
 //   v- = v_m + (sum_k d-_k P_k A-_k) / (sum_k d-_k P_k),  A-_k = q_k(x_{m+1/2}) - v_m
 //   (the same with d+ and A+ for v+), one reciprocal for both sides as in weno5_fewop_s.
+// (PLAIN: K is a register array or shared memory, read with plain loads; else read-only
+//  global loads)
+template <bool PLAIN>
+__device__ __forceinline__ double nu_ld(const double* K) {
+    if constexpr (PLAIN) return *K;
+    else return __ldg(K);
+}
+template <bool PLAIN = false>
 __device__ __forceinline__ void weno5_nu(double D0, double D1, double D2, double D3, double c,
                                          const double* __restrict__ K, int64_t ld, double eps,
                                          double& vm, double& vp) {
@@ -315,18 +323,18 @@ __device__ __forceinline__ void weno5_nu(double D0, double D1, double D2, double
     double t[3], Am[3], Ap[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const double b = fma(__ldg(K + (2 * k) * ld), Da[k], __ldg(K + (2 * k + 1) * ld) * Db[k]);
-        const double sc = fma(__ldg(K + (6 + 2 * k) * ld), Da[k], __ldg(K + (7 + 2 * k) * ld) * Db[k]);
+        const double b = fma(nu_ld<PLAIN>(K + (2 * k) * ld), Da[k], nu_ld<PLAIN>(K + (2 * k + 1) * ld) * Db[k]);
+        const double sc = fma(nu_ld<PLAIN>(K + (6 + 2 * k) * ld), Da[k], nu_ld<PLAIN>(K + (7 + 2 * k) * ld) * Db[k]);
         double tk = fma(b, b, fma(sc, sc, eps));
         t[k] = tk * tk;
-        Am[k] = fma(__ldg(K + (12 + 2 * k) * ld), Da[k], __ldg(K + (13 + 2 * k) * ld) * Db[k]);
-        Ap[k] = fma(__ldg(K + (18 + 2 * k) * ld), Da[k], __ldg(K + (19 + 2 * k) * ld) * Db[k]);
+        Am[k] = fma(nu_ld<PLAIN>(K + (12 + 2 * k) * ld), Da[k], nu_ld<PLAIN>(K + (13 + 2 * k) * ld) * Db[k]);
+        Ap[k] = fma(nu_ld<PLAIN>(K + (18 + 2 * k) * ld), Da[k], nu_ld<PLAIN>(K + (19 + 2 * k) * ld) * Db[k]);
     }
     const double P0 = t[1] * t[2], P1 = t[0] * t[2], P2 = t[0] * t[1];
-    const double wm0 = __ldg(K + 24 * ld) * P0, wm1 = __ldg(K + 25 * ld) * P1,
-                 wm2 = __ldg(K + 26 * ld) * P2;
-    const double wp0 = __ldg(K + 27 * ld) * P0, wp1 = __ldg(K + 28 * ld) * P1,
-                 wp2 = __ldg(K + 29 * ld) * P2;
+    const double wm0 = nu_ld<PLAIN>(K + 24 * ld) * P0, wm1 = nu_ld<PLAIN>(K + 25 * ld) * P1,
+                 wm2 = nu_ld<PLAIN>(K + 26 * ld) * P2;
+    const double wp0 = nu_ld<PLAIN>(K + 27 * ld) * P0, wp1 = nu_ld<PLAIN>(K + 28 * ld) * P1,
+                 wp2 = nu_ld<PLAIN>(K + 29 * ld) * P2;
     const double Zm = (wm0 + wm1) + wm2, Zp = (wp0 + wp1) + wp2;
     const double Nm = fma(wm2, Am[2], fma(wm1, Am[1], wm0 * Am[0]));
     const double Np = fma(wp2, Ap[2], fma(wp1, Ap[1], wp0 * Ap[0]));

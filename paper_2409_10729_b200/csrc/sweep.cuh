@@ -134,7 +134,10 @@ __device__ __forceinline__ void peer_copy(const PeerOut& po, int x, int y, int z
 // (candidate k's differences: k = 0: (D0, D1), 1: (D1, D2), 2: (D2, D3), D_i = v_{m-1+i} -
 //  v_{m-2+i})
 enum { NU_B = 0, NU_C = 6, NU_PM = 12, NU_PP = 18, NU_DM = 24, NU_DP = 27, NU_INV = 30,
-       NU_NCOEF = 31 };
+       NU_NCOEF = 31, NU_CM = 32 };
+// The same table cell-major (nuc[(m + 3) * NU_CM + c], 256 bytes per cell): the marches
+// read one cell's coefficients per step, the same for the whole warp, from two cache lines
+// instead of 31 rows.
 
 struct SweepArgs {
     const double* __restrict__ q;   // stencil state (padded layout, ghosts filled)
@@ -156,6 +159,7 @@ struct SweepArgs {
     Materials mat;
     PeerOut po;                     // fused halo stores (last sweep of a stage only)
     const double* nu;               // non-uniform coefficients of the sweep axis (ORD 7)
+    const double* nuc;              // the same, cell-major (marches)
     int64_t nu_ld;                  // their cell stride (n + 6)
 };
 
@@ -453,6 +457,20 @@ sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
 
         double vm[E], vp[E];
         double bAn[M::N];      // (DW) volume fractions of cell j, the next step's b_alpha
+        // stretched axis: cell j's coefficients, one warp-uniform 256-byte row of the
+        // cell-major table read as 16-byte loads (E <= 8; E = 10 has not the registers to
+        // hold the row and reads each coefficient where it is used)
+        constexpr bool KV = ORD == 7 && M::E <= 8;
+        double Kc[KV ? NU_CM : 1];
+        if constexpr (KV) {
+            const double2* k2 = reinterpret_cast<const double2*>(a.nuc + (int64_t)(j + 3) * NU_CM);
+#pragma unroll
+            for (int i = 0; i < NU_CM / 2; ++i) {
+                const double2 kv = __ldg(k2 + i);
+                Kc[2 * i] = kv.x;
+                Kc[2 * i + 1] = kv.y;
+            }
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             if constexpr (DW) {
@@ -475,8 +493,13 @@ sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
                 w[2][e] = w[3][e];
                 w[3][e] = w[4][e];
             } else if constexpr (ORD == 7) {      // non-uniform grid: cell j's coefficients
-                weno5_nu(w[1][e] - w[0][e], w[2][e] - w[1][e], w[3][e] - w[2][e],
-                         w[4][e] - w[3][e], w[2][e], a.nu + (j + 3), a.nu_ld, a.eps, vm[e], vp[e]);
+                if constexpr (KV)
+                    weno5_nu<true>(w[1][e] - w[0][e], w[2][e] - w[1][e], w[3][e] - w[2][e],
+                                   w[4][e] - w[3][e], w[2][e], Kc, 1, a.eps, vm[e], vp[e]);
+                else
+                    weno5_nu(w[1][e] - w[0][e], w[2][e] - w[1][e], w[3][e] - w[2][e],
+                             w[4][e] - w[3][e], w[2][e], a.nuc + (int64_t)(j + 3) * NU_CM, 1,
+                             a.eps, vm[e], vp[e]);
             } else {
                 reconstruct<ORD, march_fewop<M, DIR, MODE>()>(w[0][e], w[1][e], w[2][e], w[3][e],
                                                                 w[4][e], a.eps4, a.eps, vm[e], vp[e]);
@@ -492,7 +515,8 @@ sweep_kernel(const SweepArgs a, const __grid_constant__ MarchMaps mm) {
                 const int64_t c = line + (int64_t)cc * a.sS;
                 const double du = uf - uf_prev;
                 // 1/dx of cell j-1: uniform, or its own width on a stretched axis
-                const double invd = ORD == 7 ? __ldg(a.nu + NU_INV * a.nu_ld + cc + 3) : a.invd;
+                const double invd =
+                    ORD == 7 ? __ldg(a.nuc + (int64_t)(cc + 3) * NU_CM + NU_INV) : a.invd;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     double r = F_prev[e] - F[e];                 // dx * c_e

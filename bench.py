@@ -48,60 +48,124 @@ def _peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event reasons sampled DURING the timed region.
+
+    NVML is polled every 5 ms on a thread; only the samples taken between begin() (just
+    before the timed steps are enqueued) and end() (after the synchronize that closes
+    them) are reported, so the median is the clock under load.  Fallback: nvidia-smi
+    -lms 50 over the whole window (marked "source")."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []        # (t, sm_mhz, sm_max_mhz, power_w, reason bits)
+        self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self._h = None
+        self._smi = None
+        self.e0 = self.e1 = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50", "-i", str(self.device)],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByUUID(
+                uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            self._t = threading.Thread(target=self._poll, daemon=True)
             self._t.start()
-            time.sleep(0.3)
         except Exception:
-            self.proc = None
+            self._h = None
+            self._start_smi()
+        time.sleep(0.05)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _poll(self):
+        nv, h = self._nv, self._h
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                self.samples.append((time.perf_counter(),
+                                     nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), smax,
+                                     nv.nvmlDeviceGetPowerUsage(h) / 1000.0, int(fn(h))))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def _start_smi(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._smi = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self._t = threading.Thread(target=self._read_smi, daemon=True)
+            self._t.start()
+            time.sleep(0.25)
+        except Exception:
+            self._smi = None
+
+    def _read_smi(self):
+        for ln in self._smi.stdout:
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                bits = sum(b for (nm, b), v in zip(self.REASONS[:4], f[3:7]) if v.lower() == "active")
+                self.samples.append((time.perf_counter(), float(f[0]), float(f[1]), float(f[2]), bits))
+            except (ValueError, IndexError):
+                continue
+
+    def _energy_mj(self):
+        try:
+            return self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h) if self._h else None
+        except Exception:
+            return None
+
+    def begin(self):
+        self.e0 = self._energy_mj()
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
+        self.e1 = self._energy_mj()
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, smax, reasons, power = [], [], set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
+        if self.t1 is None:
+            self.end()
+        if self._h is not None:
+            time.sleep(0.01)
+            self._stop.set()
+            self._t.join(timeout=1)
+        elif self._smi is not None:
+            time.sleep(0.1)
+            self._smi.terminate()
             try:
-                sm.append(float(f[0]))
-                smax.append(float(f[1]))
-                power.append(float(f[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "power_w_max": max(power) if power else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                self._smi.wait(timeout=5)
+            except Exception:
+                self._smi.kill()
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["NVML and nvidia-smi unavailable"]}
+        win = [s for s in self.samples if self.t0 is not None and self.t0 <= s[0] <= self.t1]
+        src = "NVML every 5 ms inside the timed region" if self._h is not None else \
+            "nvidia-smi -lms 50 inside the timed region"
+        if not win:             # (a window shorter than one poll)
+            win = self.samples
+            src += " (no sample inside: all samples)"
+        reasons = sorted({nm for nm, b in self.REASONS for s in win if s[4] & b})
+        return {"sm_mhz": statistics.median(s[1] for s in win) if win else None,
+                "sm_min_mhz": min(s[1] for s in win) if win else None,
+                "sm_max_mhz": max(s[2] for s in win) if win else None,
+                "power_w_max": max(s[3] for s in win) if win else None,
+                "samples": len(win), "source": src, "reasons": reasons,
+                **({"energy_j": (self.e1 - self.e0) / 1000.0,
+                    "window_s": self.t1 - self.t0}
+                   if self.e0 is not None and self.e1 is not None else {})}
 
 
 # ------------------------------------------------------------ cpu baseline
@@ -363,6 +427,7 @@ def run_ours(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     launches = 0
+    clk.begin()
     for i in range(args.steps):
         if flush:
             scratch.fill_(float(i))
@@ -371,6 +436,7 @@ def run_ours(args):
         launches += s.last_launch_count()
         evs[i][1].record(stream)
     torch.cuda.synchronize()
+    clk.end()
     barrier()
     clocks = clk.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -413,6 +479,7 @@ def run_ours(args):
         clk2.start()
         evs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in range(20)]
+        clk2.begin()
         for i in range(20):
             if flush:
                 scratch.fill_(float(i))
@@ -420,6 +487,7 @@ def run_ours(args):
             s.rk3_step(q, dt)
             evs2[i][1].record(stream)
         torch.cuda.synchronize()
+        clk2.end()
         barrier()
         clocks2 = clk2.stop()
         st_ms = [a.elapsed_time(b) for a, b in evs2]
@@ -488,8 +556,11 @@ def run_ours(args):
                                       "scaling number"} if args.same_device else {})},
         "step_ms": {"median": statistics.median(step_ms), "min": srt[0], "max": srt[-1],
                     "p10": srt[len(srt) // 10], "p90": srt[(9 * len(srt)) // 10],
+                    "all": [round(x, 4) for x in step_ms],
                     "timing": "one CUDA event pair per step on the launching stream, "
-                              "library profiling off; value = sum over the K steps"},
+                              "library profiling off; value = sum over the K steps (the "
+                              "steps slow down in order as the board heats up: "
+                              "profiles/pattern_r302.txt)"},
         "hbm_gbs_step": hbm_step,
         "hbm_frac_step": hbm_step / hbm_peak,
         "fp64_tflops_step": step_flops / (ms_max / args.steps * 1e-3) / 1e12,
@@ -512,6 +583,7 @@ def run_ours(args):
                                   "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
                      "hbm_per_sweep": {k: hbm_of(k) for k in sorted(sweeps)}},
         "clocks": clocks,
+        **({"energy_j_per_step": clocks["energy_j"] / args.steps} if "energy_j" in clocks else {}),
         **({"sustained": sustained} if sustained else {}),
         "gpu_launches": launches,
         "state_finite": finite,

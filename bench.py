@@ -522,9 +522,16 @@ def run_ours(args):
     flops = algorithmic_flops(dom, pb.n_fluids, pb.ndim) * cells_local
     achieved_tf = flops / (per_launch(dom) * 1e-3) / 1e12
     traffic, traffic_src = None, None
-    try:   # DRAM bytes of this kernel from the committed ncu --set full capture
+    # DRAM bytes of this kernel from the committed ncu capture -- of the workload it was
+    # measured on only (C3 256^3, uniform WENO5); any other workload reports null
+    wl_key = (f"{args.config}-{n}-weno{args.weno}-{'stretched' if args.stretch else 'uniform'}"
+              if args.config == "C3" else args.config)
+    try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic, traffic_src = tr.get(dom), tr.get("source")
+        if tr.get("workload") == wl_key:
+            traffic, traffic_src = tr.get(dom), tr.get("source")
+        else:
+            traffic_src = f"null: profiles/ncu_traffic.json holds {tr.get('workload')}, not {wl_key}"
     except Exception:
         pass
     # per step: 3 x (16E + 24E + 24E) + q^n reads in stages 2 and 3 (2 x 8E) = 208E B/cell
@@ -560,7 +567,7 @@ def run_ours(args):
                     "timing": "one CUDA event pair per step on the launching stream, "
                               "library profiling off; value = sum over the K steps (the "
                               "steps slow down in order as the board heats up: "
-                              "profiles/pattern_r302.txt)"},
+                              "profiles/r3/pattern_r302.txt)"},
         "hbm_gbs_step": hbm_step,
         "hbm_frac_step": hbm_step / hbm_peak,
         "fp64_tflops_step": step_flops / (ms_max / args.steps * 1e-3) / 1e12,

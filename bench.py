@@ -65,7 +65,6 @@ class ClockSampler:
         self._stop = threading.Event()
         self._h = None
         self._smi = None
-        self.e0 = self.e1 = None
 
     def start(self):
         try:
@@ -81,7 +80,7 @@ class ClockSampler:
         except Exception:
             self._h = None
             self._start_smi()
-        time.sleep(0.05)
+        time.sleep(0.3)     # (the r1/r2 sampler's start-up pause before the timed steps, kept)
 
     def _poll(self):
         nv, h = self._nv, self._h
@@ -121,25 +120,17 @@ class ClockSampler:
             except (ValueError, IndexError):
                 continue
 
-    def _energy_mj(self):
-        try:
-            return self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h) if self._h else None
-        except Exception:
-            return None
-
     def begin(self):
-        self.e0 = self._energy_mj()
         self.t0 = time.perf_counter()
 
     def end(self):
         self.t1 = time.perf_counter()
-        self.e1 = self._energy_mj()
 
     def stop(self):
         if self.t1 is None:
             self.end()
         if self._h is not None:
-            time.sleep(0.01)
+            time.sleep(0.15)
             self._stop.set()
             self._t.join(timeout=1)
         elif self._smi is not None:
@@ -158,14 +149,20 @@ class ClockSampler:
             win = self.samples
             src += " (no sample inside: all samples)"
         reasons = sorted({nm for nm, b in self.REASONS for s in win if s[4] & b})
+        after = [s for s in self.samples if self.t1 < s[0] <= self.t1 + 0.15]
+        bits = 0
+        for smp in win + after:
+            bits |= smp[4]
         return {"sm_mhz": statistics.median(s[1] for s in win) if win else None,
                 "sm_min_mhz": min(s[1] for s in win) if win else None,
                 "sm_max_mhz": max(s[2] for s in win) if win else None,
                 "power_w_max": max(s[3] for s in win) if win else None,
                 "samples": len(win), "source": src, "reasons": reasons,
-                **({"energy_j": (self.e1 - self.e0) / 1000.0,
-                    "window_s": self.t1 - self.t0}
-                   if self.e0 is not None and self.e1 is not None else {})}
+                # the driver raises the reason flags after the clock has already dropped:
+                # what it reports in the 150 ms after the timed region, and every bit seen
+                "reasons_next_150ms": sorted({nm for nm, b in self.REASONS for s in after
+                                              if s[4] & b}),
+                "reason_bits_seen": hex(bits)}
 
 
 # ------------------------------------------------------------ cpu baseline
@@ -590,7 +587,6 @@ def run_ours(args):
                                   "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
                      "hbm_per_sweep": {k: hbm_of(k) for k in sorted(sweeps)}},
         "clocks": clocks,
-        **({"energy_j_per_step": clocks["energy_j"] / args.steps} if "energy_j" in clocks else {}),
         **({"sustained": sustained} if sustained else {}),
         "gpu_launches": launches,
         "state_finite": finite,

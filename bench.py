@@ -443,10 +443,21 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
 
-    # separate profiled pass (same configuration, right after the timed region): every
-    # kernel launch bracketed by events on its own stream -> the per-kernel split and
-    # the roofline of the dominant kernel
-    nprof = max(3, min(args.steps, 10))
+    # separate profiled pass (same configuration): every kernel launch bracketed by
+    # events on its own stream -> the per-kernel split and the roofline of the dominant
+    # kernel.  It repeats the timed region's thermal history -- an idle pause, the
+    # warm-up steps, the sampler's pause, then as many steps as were timed -- because
+    # the board lowers the SM clock ~60 ms into a full FP64 load (profiles/r3/
+    # pattern_r303.txt): run straight after the timed region it would see only the
+    # lowered clock, and the split would not add up to the timed step
+    barrier()
+    time.sleep(args.prof_cool)
+    for _ in range(args.warmup):
+        s.rk3_step(q, dt)
+    torch.cuda.synchronize()
+    barrier()
+    time.sleep(0.3)
+    nprof = args.steps
     s.profile(True)
     for i in range(nprof):
         if flush:
@@ -570,7 +581,9 @@ def run_ours(args):
         "fp64_tflops_step": step_flops / (ms_max / args.steps * 1e-3) / 1e12,
         "kernel_ms_per_step": {k: v[0] / nprof for k, v in prof.items() if v[1]},
         "kernel_split_source": f"separate profiled pass of {nprof} steps after the timed "
-                               "region (events around every launch)",
+                               f"region, {args.prof_cool} s idle + {args.warmup} warm-up steps "
+                               "before it as before the timed steps (events around every "
+                               "launch)",
         "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved_tf,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
@@ -638,6 +651,9 @@ def main():
     ap.add_argument("--sustained", type=float, default=2.0,
                     help="seconds of untimed steps before a 20-step sustained (power-limited) "
                          "timing reported beside the value; 0 disables")
+    ap.add_argument("--prof-cool", type=float, default=1.0,
+                    help="idle seconds before the profiled (per-kernel) pass, so that it "
+                         "starts from the timed region's thermal state; 0 under ncu")
     ap.add_argument("--halo", default="fused", choices=["nccl", "fused", "peer"],
                     help="N>1: 'fused' (default, F1): the last sweep of each RK stage stores "
                          "its boundary layers into the neighbours' CUDA-IPC-mapped ghost "

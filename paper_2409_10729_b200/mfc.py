@@ -250,8 +250,12 @@ class Solver:
         """(E, nz, ny, nx) strided view of the interior cells of a state buffer."""
         L = self.layout
         nx, ny, nz = L.n_local
+        if t.dim() != 1 or not t.is_contiguous() or t.numel() < L.n_elems:
+            raise ValueError(f"state buffer needs >= {L.n_elems} contiguous float64 elements")
+        # as_strided's offset counts from the start of the STORAGE: a buffer that is itself
+        # a view (t.storage_offset() > 0) starts that far in
         return t.as_strided((L.E, nz, ny, nx), (L.stride[0], L.stride[1], L.stride[2], 1),
-                            L.offset)
+                            t.storage_offset() + L.offset)
 
     def state_from_prims(self, prims: np.ndarray | torch.Tensor) -> torch.Tensor:
         """Upload primitive fields (E, nz, ny, nx) and convert them with mfc_prim_to_cons."""
